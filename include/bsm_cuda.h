@@ -1,0 +1,133 @@
+/*
+ * bsm_cuda.h -- C ABI of the B200-native Binary Stereo Matching hot path.
+ *
+ * The drop-in boundary for the reference library's hot path
+ * (/root/reference/proj/include/bsm, a header-only C++20 library with no FFI of
+ * its own).  Every entry point below replaces one reference function; the C++
+ * shim in include/bsm/ re-exposes them under the reference's own names and
+ * signatures, and a ctypes / cgo / JNI binding can bind them directly
+ * (INTEGRATION.md).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Conventions
+ *  - Host buffers are caller-owned; any OUTPUT pointer may be NULL to skip it.
+ *  - Bit strings use the reference layout: bit i in 64-bit word i>>6 at
+ *    position i&63, pad bits zero (bitstring.hpp:21-23,47-51); fields are AoS
+ *    with index ((y*W + x) * words64) (descriptor.hpp:48-50).
+ *  - Disparity maps are float disparity + uint8 valid (image.hpp:243-263).
+ *  - Return value: BSM_OK or an error code; bsm_last_error() holds the
+ *    thread-local message (the reference's exception text where one exists).
+ *  - Device work runs on the context's own stream; a context is re-entrant
+ *    but not shared between threads without external locking.
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point returns BSM_CUDA_ERROR.
+ */
+#ifndef BSM_CUDA_H
+#define BSM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -> reference exception types (errors.hpp:8-34). */
+enum {
+    BSM_OK = 0,
+    BSM_INVALID_ARGUMENT = 1,   /* bsm::InvalidArgument */
+    BSM_DIMENSION_MISMATCH = 2, /* bsm::DimensionMismatch */
+    BSM_CUDA_ERROR = 3,         /* device failure / no device */
+    BSM_UNSUPPORTED = 4,        /* valid input outside this build's envelope */
+    BSM_NCCL_ERROR = 5
+};
+
+typedef struct bsm_ctx bsm_ctx;
+
+/* Pipeline parameters: the BsmConfig fields run_pipeline reads
+ * (config.hpp:16-28, pipeline.hpp:150-167). */
+typedef struct {
+    int d_max;            /* hypotheses d in [0, d_max - 1]; no default (config.hpp:14-15) */
+    double lambda_c;      /* 9.0 */
+    double lambda_e;      /* 16.0 */
+    double lr_tolerance;  /* 1.0 */
+    int vote_radius;      /* 20 */
+} bsm_params;
+
+/* PipelineResult (pipeline.hpp:14-20); every member optional. */
+typedef struct {
+    float* refined_d;
+    uint8_t* refined_v;
+    float* left_d;     /* left_wta (all valid) */
+    float* right_d;    /* right_wta (all valid) */
+    float* checked_d;
+    uint8_t* checked_v;
+    float* unmasked_d; /* only when want_unmasked */
+} bsm_maps;
+
+const char* bsm_last_error(void);
+const char* bsm_version(void);
+
+/* Context: owns a device, a stream, the uploaded pattern and scratch. */
+int bsm_ctx_create(int device, bsm_ctx** out);
+int bsm_ctx_destroy(bsm_ctx* ctx);
+
+/* generate_pattern(n, window, spread, seed) (pattern.hpp:74-103); host-side,
+ * out_pairs = n x {px, py, qx, qy}. */
+int bsm_generate_pattern(int n, int window, double spread, uint64_t seed, int16_t* out_pairs);
+
+/* Upload a SamplingPattern (pattern.hpp:62-72).  |offset| <= window/2. */
+int bsm_set_pattern(bsm_ctx* ctx, const int16_t* pairs, int n, int window);
+
+/* to_gray / to_lab of the gray pixel (v,v,v), v = 0..255 (image.hpp:90-140). */
+int bsm_gray_lab_lut(float* gray256, float* lab768);
+
+/* compute_field (descriptor.hpp:200-239) of a grayscale view (r=g=b=img).
+ * desc/mask: W*H*words64 uint64 each, AoS. */
+int bsm_compute_field_u8(bsm_ctx* ctx, const uint8_t* img, int W, int H, uint64_t* desc, uint64_t* mask);
+
+/* wta (matcher.hpp:80-113) over AoS fields with the context's pattern length n.
+ * right_ref = 0: RefView::left (x - d); 1: RefView::right (x + d). */
+int bsm_wta(bsm_ctx* ctx, const uint64_t* desc_ref, const uint64_t* mask_ref, const uint64_t* desc_other,
+            int W, int H, int n, int d_max, int right_ref, int use_mask, float* out_d);
+
+/* lr_check (refine.hpp:39-54); input validity is ignored, as in the reference. */
+int bsm_lr_check(bsm_ctx* ctx, const float* left_d, const float* right_d, int W, int H, double tol,
+                 float* out_d, uint8_t* out_v);
+
+/* vote_refine (refine.hpp:62-111) with the Lab image of a grayscale view. */
+int bsm_vote_refine_u8(bsm_ctx* ctx, const float* d, const uint8_t* v, const uint8_t* gray_img, int W, int H,
+                       double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v);
+
+/* run_pipeline (pipeline.hpp:25-56) of a grayscale pair (r=g=b), host buffers. */
+int bsm_pipeline_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H,
+                    const bsm_params* params, int want_unmasked, bsm_maps* out);
+
+/* Device-resident variant: left/right are device pointers; results stay on the
+ * device in context-owned buffers (read them with bsm_fetch_maps). */
+int bsm_pipeline_u8_device(bsm_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int W, int H,
+                           const bsm_params* params, int want_unmasked);
+int bsm_fetch_maps(bsm_ctx* ctx, bsm_maps* out);
+
+/* Multi-GPU row band (c5): compute rows [y0, y1) of the refined map of a
+ * W x H pair whose full views are given; the checked map is computed for
+ * [y0 - radius, y1 + radius) locally (redundant halo, no exchange).
+ * refined_d / refined_v receive (y1 - y0) rows. */
+int bsm_pipeline_band_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H, int y0, int y1,
+                         const bsm_params* params, float* refined_d, uint8_t* refined_v);
+
+/* Instrumentation.  bsm_stream returns the cudaStream_t the context launches
+ * on.  When profiling is enabled, bsm_last_timings reports the device time (ms)
+ * of the last pipeline's kernels, in the order of bsm_timing_names. */
+int bsm_stream(bsm_ctx* ctx, void** stream);
+int bsm_set_profiling(bsm_ctx* ctx, int enable);
+int bsm_last_timings(bsm_ctx* ctx, float* ms, int max, int* count);
+const char* bsm_timing_names(void);
+/* Kernel launches issued by the last pipeline call. */
+int bsm_last_launch_count(bsm_ctx* ctx, int* count);
+/* Measured POPC word-op throughput of this device (ops/s), microbenchmark. */
+int bsm_measure_popc_peak(bsm_ctx* ctx, double* ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSM_CUDA_H */

@@ -1,0 +1,149 @@
+// bsm_host.cpp -- see bsm_host.h.  Everything here is O(pattern) or O(256^2)
+// setup work that the reference also does on the host; none of it scales with
+// the image.  Compiled with g++ -O2 -march=x86-64-v3 (FMA contraction, like
+// the reference's -march=native default) -- the colour tables are checked
+// bit-for-bit against the compiled reference in tests/test_host.py.
+#include "bsm_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <random>
+#include <thread>
+
+namespace bsmh {
+
+// pattern.hpp:24-48 -- mt19937_64 uniform bits, explicit Box-Muller with spare.
+namespace {
+class Normal {
+public:
+    explicit Normal(uint64_t seed) : mt_(seed) {}
+    double operator()() {
+        if (spare_ok_) {
+            spare_ok_ = false;
+            return spare_;
+        }
+        const double u1 = 1.0 - unit();
+        const double u2 = unit();
+        const double rad = std::sqrt(-2.0 * std::log(u1));
+        const double ang = 2.0 * 3.141592653589793238462643383279502884 * u2;
+        spare_ = rad * std::sin(ang);
+        spare_ok_ = true;
+        return rad * std::cos(ang);
+    }
+
+private:
+    double unit() { return double(mt_() >> 11) * 0x1.0p-53; }
+    std::mt19937_64 mt_;
+    bool spare_ok_ = false;
+    double spare_ = 0.0;
+};
+}  // namespace
+
+bool generate_pattern(int n, int window, double spread, uint64_t seed, int16_t* out, std::string& err) {
+    if (n < 1) { err = "pattern: n must be >= 1"; return false; }
+    if (window < 2) { err = "pattern: window must be >= 2"; return false; }
+    if (!(spread > 0.0)) { err = "pattern: spread must be > 0"; return false; }
+    Normal normal(seed);
+    const long half = window / 2;
+    auto offset = [&]() {
+        const long v = std::lround(spread * normal());
+        return int16_t(std::clamp(v, -half, half));
+    };
+    for (int i = 0; i < n; ++i) {
+        int16_t* p = out + 4 * i;
+        do {  // endpoints drawn px, py, qx, qy; degenerate pairs redrawn
+            p[0] = offset();
+            p[1] = offset();
+            p[2] = offset();
+            p[3] = offset();
+        } while (p[0] == p[2] && p[1] == p[3]);
+    }
+    return true;
+}
+
+namespace {
+// sRGB decode and the CIE f() with its linear toe (image.hpp:101-106).
+double decode(double c) { return c <= 0.04045 ? c / 12.92 : std::pow((c + 0.055) / 1.055, 2.4); }
+double cie_f(double t) {
+    return t > 216.0 / 24389.0 ? std::cbrt(t) : ((24389.0 / 27.0) * t + 16.0) / 116.0;
+}
+}  // namespace
+
+void gray_lab_lut(float* gray256, float* lab768) {
+    for (int v = 0; v < 256; ++v) {
+        const uint8_t c = uint8_t(v);
+        // BT.601 luma in float, same expression shape as image.hpp:95.
+        gray256[v] = 0.299f * float(c) + 0.587f * float(c) + 0.114f * float(c);
+        const double r = decode(c / 255.0), g = decode(c / 255.0), b = decode(c / 255.0);
+        // sRGB -> XYZ (D65) normalised by the matrix row sums (image.hpp:113-115).
+        const double X = (0.4124564 * r + 0.3575761 * g + 0.1804375 * b) / 0.9504700;
+        const double Y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
+        const double Z = (0.0193339 * r + 0.1191920 * g + 0.9503041 * b) / 1.0888300;
+        const double fx = cie_f(X), fy = cie_f(Y), fz = cie_f(Z);
+        lab768[3 * v + 0] = float(std::clamp(116.0 * fy - 16.0, 0.0, 100.0));
+        lab768[3 * v + 1] = float(500.0 * (fx - fy));
+        lab768[3 * v + 2] = float(200.0 * (fy - fz));
+    }
+}
+
+namespace {
+float sad(const float* a, const float* b) {  // image.hpp:144-146, same association
+    return std::fabs(a[0] - b[0]) + std::fabs(a[1] - b[1]) + std::fabs(a[2] - b[2]);
+}
+}  // namespace
+
+void sad_rank_table(const float* lab, uint8_t* rank) {
+    for (int c = 0; c < 256; ++c) {
+        float row[256];
+        for (int v = 0; v < 256; ++v) row[v] = sad(lab + 3 * c, lab + 3 * v);
+        float sorted[256];
+        std::copy(row, row + 256, sorted);
+        std::sort(sorted, sorted + 256);
+        const int distinct = int(std::unique(sorted, sorted + 256) - sorted);
+        for (int v = 0; v < 256; ++v)
+            rank[c * 256 + v] = uint8_t(std::lower_bound(sorted, sorted + distinct, row[v]) - sorted);
+    }
+}
+
+void vote_weight_table(const float* lab, double lc, double le, int radius, std::vector<double>& w,
+                       std::vector<int16_t>& s2col, int& ncol) {
+    const int smax = 2 * radius * radius;
+    s2col.assign(size_t(smax) + 1, -1);
+    for (int dy = 0; dy <= radius; ++dy)
+        for (int dx = 0; dx <= radius; ++dx) s2col[size_t(dx * dx + dy * dy)] = 0;
+    std::vector<int> cols;
+    for (int s = 0; s <= smax; ++s)
+        if (s2col[size_t(s)] == 0) {
+            s2col[size_t(s)] = int16_t(cols.size());
+            cols.push_back(s);
+        }
+    ncol = int(cols.size());
+    std::vector<double> e(static_cast<size_t>(ncol));
+    for (int k = 0; k < ncol; ++k) {
+        // sqrt(double(dx)*dx + double(dy)*dy): the sum is an exact integer.
+        e[size_t(k)] = std::sqrt(double(cols[size_t(k)]));
+    }
+    const int npair = 256 * 257 / 2;
+    w.assign(size_t(npair) * size_t(ncol), 0.0);
+    auto work = [&](int v0, int v1) {
+        for (int v = v0; v < v1; ++v)
+            for (int u = 0; u <= v; ++u) {
+                const double c = double(sad(lab + 3 * v, lab + 3 * u));
+                double* row = &w[(size_t(v) * (v + 1) / 2 + u) * size_t(ncol)];
+                for (int k = 0; k < ncol; ++k) row[k] = std::exp(-(c / lc + e[size_t(k)] / le));
+            }
+    };
+    // Rows are independent; split by v with balanced triangle areas.
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    int v0 = 0;
+    for (unsigned t = 0; t < nt; ++t) {
+        const double frac = double(t + 1) / nt;
+        const int v1 = t + 1 == nt ? 256 : int(256.0 * std::sqrt(frac));
+        if (v1 > v0) pool.emplace_back(work, v0, v1);
+        v0 = std::max(v0, v1);
+    }
+    for (auto& th : pool) th.join();
+}
+
+}  // namespace bsmh

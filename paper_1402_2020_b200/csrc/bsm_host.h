@@ -1,0 +1,32 @@
+// bsm_host.h -- host-side pieces of the product library that stay on the CPU
+// (SURVEY.md section 8(a) rows R2-R4, R9, R18/R19): the sampling pattern, the
+// 256-entry colour-conversion tables, the per-centre rank table the mask
+// kernel selects over, and the exact vote-weight table.  Compiled by g++ with
+// FP contraction on (bsm_host.cpp), so its floating point matches the
+// reference's default -O3 -march=native build.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace bsmh {
+
+// pattern.hpp:74-103.  Returns false (and sets err) on invalid arguments.
+bool generate_pattern(int n, int window, double spread, uint64_t seed, int16_t* out, std::string& err);
+
+// image.hpp:90-140 for (v,v,v).
+void gray_lab_lut(float* gray256, float* lab768);
+
+// rank[c*256 + v] = dense rank of lab_sad(Lab[c], Lab[v]) among the 256 values
+// of row c (equal values share a rank).  lab_sad: image.hpp:144-146.
+void sad_rank_table(const float* lab768, uint8_t* rank65536);
+
+// Exact refine weights (refine.hpp:30-35) for grayscale views:
+//   w[tri(u,v) * ncol + col(s)] = exp(-(double(lab_sad(u,v)) / lc + sqrt(s) / le))
+// for every gray pair u <= v (tri(u,v) = v*(v+1)/2 + u) and every distinct
+// squared offset s = dx^2 + dy^2 with |dx|,|dy| <= radius.  s2col has
+// 2*radius^2 + 1 entries (-1 where s is not a sum of two squares in range).
+void vote_weight_table(const float* lab768, double lc, double le, int radius, std::vector<double>& w,
+                       std::vector<int16_t>& s2col, int& ncol);
+
+}  // namespace bsmh

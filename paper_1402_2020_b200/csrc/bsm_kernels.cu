@@ -1,0 +1,1306 @@
+// bsm_kernels.cu -- sm_100a kernels and the C ABI (include/bsm_cuda.h) of the
+// Binary Stereo Matching hot path.  See DESIGN.md for the data layout, each
+// kernel's roofline, and the reference function (file:line) it replaces.
+//
+// Device layout (per view, W x H, n bits, NW = 2*ceil(n/64) u32 words):
+//   field[(y*NW + w)*Wp + x]   word-major ("bit-plane rows"), Wp = W rounded up
+//   to 128, so a row segment of one word is a contiguous, 16-B-aligned span:
+//   the cost kernel stages [K words x span] boxes with cp.async and every
+//   shared-memory read is a conflict-free 16-B lane-contiguous LDS.128.
+//   u32 word w of a pixel = bits 32w..32w+31 = the low/high half of the
+//   reference's u64 word w>>1 (bitstring.hpp:47-51).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bsm_cuda.h"
+#include "bsm_host.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define BSM_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return set_err(BSM_CUDA_ERROR, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                               " at " #call);                            \
+    } while (0)
+
+constexpr int kMaxPairs = 8192;      // mask kernel keeps 2*ceil(n/128) regs/lane of ranks
+constexpr int kCostTile = 128;       // pixels per cost CTA
+constexpr int kCostDisp = 64;        // disparities per cost CTA
+constexpr int kCostK = 8;            // u32 words per pipeline stage
+constexpr int kCostStages = 3;
+
+inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// K1 -- descriptor.  descriptor.hpp:95-105 (border), :214-219/:226-230
+// (interior), pack_bits :83-93.  Thread per pixel column, PY rows per thread;
+// the CTA stages its (32 + 2h) x (8*PY + 2h) image window (coordinates clamped
+// exactly like clamp_coord, image.hpp:148-150) in shared memory, so every
+// sample of a warp is one 32-byte conflict-free LDS.  Pair offsets are
+// warp-uniform (broadcast).  Gray values are compared as uint8: the gray
+// conversion table is strictly increasing (checked at context creation), so
+// I(p) > I(q) on floats is the same predicate.
+// Output word w of pixel (x, y): bit k = pair 32w + k.
+constexpr int kDescTX = 32, kDescTY = 8, kDescPY = 4;
+
+__global__ void __launch_bounds__(kDescTX* kDescTY)
+    k_descriptor(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
+                 int n, int half, int NW, int Wp, uint32_t* __restrict__ desc) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int TW = kDescTX + 2 * half;
+    const int TH = kDescTY * kDescPY + 2 * half;
+    int2* s_off = reinterpret_cast<int2*>(smem);
+    uint8_t* tile = smem + size_t(n) * sizeof(int2);
+    const int tid = threadIdx.y * kDescTX + threadIdx.x;
+    const int gx0 = blockIdx.x * kDescTX - half;
+    const int ly0 = blockIdx.y * kDescTY * kDescPY;  // local row of the CTA's first pixel
+    const int gy0 = ybeg + ly0 - half;
+    for (int i = tid; i < n; i += kDescTX * kDescTY) {
+        // tile-relative offset of each endpoint (dy*TW + dx)
+        const int2 o = offs[i];
+        s_off[i] = make_int2(o.x, o.y);
+    }
+    for (int idx = tid; idx < TW * TH; idx += kDescTX * kDescTY) {
+        const int r = idx / TW, c = idx - r * TW;
+        const int gx = min(max(gx0 + c, 0), W - 1);
+        const int gy = min(max(gy0 + r, 0), H - 1);
+        tile[idx] = img[size_t(gy) * W + gx];
+    }
+    __syncthreads();
+
+    const int x = blockIdx.x * kDescTX + threadIdx.x;
+    const int base = (threadIdx.y * kDescPY + half) * TW + threadIdx.x + half;
+    const int full = n >> 5;
+    for (int w = 0; w < NW; ++w) {
+        uint32_t acc[kDescPY];
+#pragma unroll
+        for (int j = 0; j < kDescPY; ++j) acc[j] = 0;
+        if (w < full) {
+            const int2* o = s_off + 32 * w;
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) {
+                const int2 ok = o[k];
+#pragma unroll
+                for (int j = 0; j < kDescPY; ++j) {
+                    const uint8_t* t = tile + base + j * TW;
+                    acc[j] |= uint32_t(t[ok.x] > t[ok.y]) << k;
+                }
+            }
+        } else if (w == full && (n & 31)) {
+            for (int k = 0; k < (n & 31); ++k) {
+                const int2 ok = s_off[32 * w + k];
+#pragma unroll
+                for (int j = 0; j < kDescPY; ++j) {
+                    const uint8_t* t = tile + base + j * TW;
+                    acc[j] |= uint32_t(t[ok.x] > t[ok.y]) << k;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kDescPY; ++j) {
+            const int ly = ly0 + threadIdx.y * kDescPY + j;
+            if (ly < rows) desc[(size_t(ly) * NW + w) * Wp + x] = acc[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2 -- mask.  descriptor.hpp:118-154 (mask_at_pixel), quarter_threshold
+// :64-76.  Warp per pixel.
+//   1. rho[k] = dense rank of lab_sad(centre, window pixel k) for the u window
+//      offsets the pattern uses (gray views: rank[c][v], a 256x256 host table,
+//      so the float order and ties of the reference are preserved exactly).
+//   2. lane l of group g holds a = max(rho[P], rho[Q]) of pair 32g + l: the
+//      rank of the reference's weight max(t[p], t[q]).  Four groups per
+//      register, split into even/odd byte halves (16-bit SWAR lanes).
+//   3. T = k-th smallest a, k = max(1, n/4), by an 8-step bisection over the
+//      byte range: count(a <= mid) via SWAR borrow tests + one REDUX per step.
+//   4. bit = a <= T (ties at T included, descriptor.hpp:153), one ballot per
+//      group of 32 pairs = one output word; staged per CTA, then stored as
+//      coalesced 128-B rows.
+// CTA = 8 warps x 4 pixels = 32 consecutive pixels of one row.
+constexpr int kMaskWarps = 8, kMaskPxPerWarp = 4, kMaskTile = kMaskWarps * kMaskPxPerWarp;
+
+template <int MAXG4>
+__global__ void __launch_bounds__(kMaskWarps * 32)
+    k_mask(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint32_t* __restrict__ pq,
+           int n, const int32_t* __restrict__ uoff, int u, int upad, const uint8_t* __restrict__ rank,
+           int half, int NW, int Wp, uint32_t* __restrict__ mask) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int TW = kMaskTile + 2 * half;
+    const int TH = 2 * half + 1;
+    const int G = (n + 31) >> 5;
+    uint32_t* s_pq = reinterpret_cast<uint32_t*>(smem);         // n
+    int32_t* s_uoff = reinterpret_cast<int32_t*>(s_pq + n);     // u
+    uint32_t* stage = reinterpret_cast<uint32_t*>(s_uoff + u);  // G * 32
+    uint8_t* rho_all = reinterpret_cast<uint8_t*>(stage + G * kMaskTile);  // warps * upad
+    uint8_t* tile = rho_all + kMaskWarps * upad;                           // TH * TW
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int x0 = blockIdx.x * kMaskTile;
+    const int ly = blockIdx.y;
+    const int y = ybeg + ly;
+    for (int i = tid; i < n; i += blockDim.x) s_pq[i] = pq[i];
+    for (int i = tid; i < u; i += blockDim.x) s_uoff[i] = uoff[i];
+    for (int idx = tid; idx < TW * TH; idx += blockDim.x) {
+        const int r = idx / TW, c = idx - r * TW;
+        const int gx = min(max(x0 - half + c, 0), W - 1);
+        const int gy = min(max(y - half + r, 0), H - 1);
+        tile[idx] = img[size_t(gy) * W + gx];
+    }
+    __syncthreads();
+
+    uint8_t* rho = rho_all + warp * upad;
+    const int k = max(1, n / 4);
+    for (int q = 0; q < kMaskPxPerWarp; ++q) {
+        const int px = warp * kMaskPxPerWarp + q;
+        const int ci = half * TW + half + px;
+        const uint8_t* rrow = rank + 256 * int(tile[ci]);
+        for (int j = lane; j < u; j += 32) rho[j] = __ldg(rrow + tile[ci + s_uoff[j]]);
+        __syncwarp();
+
+        uint32_t E[MAXG4], O[MAXG4];
+#pragma unroll
+        for (int j = 0; j < MAXG4; ++j) {
+            uint32_t r = 0xFFFFFFFFu;
+            if (4 * j < G) {
+                r = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int i = 32 * (4 * j + b) + lane;
+                    uint32_t a = 255;
+                    if (i < n) {
+                        const uint32_t e = s_pq[i];
+                        a = max(uint32_t(rho[e & 0xFFFF]), uint32_t(rho[e >> 16]));
+                    }
+                    r |= a << (8 * b);
+                }
+            }
+            E[j] = r & 0x00FF00FFu;
+            O[j] = (r >> 8) & 0x00FF00FFu;
+        }
+        // Smallest R with #{a <= R} >= k.  Pads (a = 255) are never counted:
+        // every probed mid is < 255.
+        int lo = 0, hi = 255;
+#pragma unroll 1
+        for (int it = 0; it < 8; ++it) {
+            const int mid = (lo + hi) >> 1;
+            const uint32_t T9 = uint32_t(0x100 + mid) * 0x00010001u;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < MAXG4; ++j) acc += ((T9 - E[j]) & 0x01000100u) + ((T9 - O[j]) & 0x01000100u);
+            const uint32_t cnt = __reduce_add_sync(0xFFFFFFFFu, ((acc & 0xFFFFu) + (acc >> 16)) >> 8);
+            if (int(cnt) >= k) hi = mid;
+            else lo = mid + 1;
+        }
+        const uint32_t T9 = uint32_t(0x100 + lo) * 0x00010001u;
+#pragma unroll
+        for (int j = 0; j < MAXG4; ++j) {
+            if (4 * j < G) {
+                const uint32_t fe = T9 - E[j], fo = T9 - O[j];
+                uint32_t wd[4];
+                wd[0] = __ballot_sync(0xFFFFFFFFu, fe & 0x100u);
+                wd[1] = __ballot_sync(0xFFFFFFFFu, fo & 0x100u);
+                wd[2] = __ballot_sync(0xFFFFFFFFu, fe & 0x1000000u);
+                wd[3] = __ballot_sync(0xFFFFFFFFu, fo & 0x1000000u);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int g = 4 * j + b;
+                    if (g < G && lane == (g & 31)) {
+                        uint32_t v = wd[b];
+                        const int rem = n - 32 * g;
+                        if (rem < 32) v &= (1u << rem) - 1u;
+                        stage[g * kMaskTile + px] = v;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int idx = tid; idx < NW * kMaskTile; idx += blockDim.x) {
+        const int w = idx / kMaskTile, j = idx - w * kMaskTile;
+        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = w < G ? stage[w * kMaskTile + j] : 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
+// (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
+// :68-75 (ties -> smaller d).  No cost volume is materialised.
+// CTA tile: 128 reference pixels of one row x 64 disparities; 8 warps, warp wi
+// owns disparities [d0 + 8wi, +8), lane l owns pixels [x0 + 4l, +4): a 4 x 8
+// register block of costs, so each staged word feeds 32 LOP3+POPC+IADD from
+// 5 LDS.128 (ref desc, ref mask, a 12-word window of the other view).
+// Words stream through a 3-stage cp.async ring of K = 8 words
+// ([8 x 128] desc, [8 x 128] mask, [8 x 192] other-view span).  The argmin
+// key is (cost << 16) | d (min cost, then smaller d); d-split CTAs merge
+// with atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_ptr));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gptr), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <bool RIGHT, bool MASKED>
+__global__ void __launch_bounds__(256, 2)
+    k_cost_wta(const uint32_t* __restrict__ dref, const uint32_t* __restrict__ mref,
+               const uint32_t* __restrict__ doth, int W, int rows, int NW, int Wp, int D,
+               uint32_t* __restrict__ keys) {
+    constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
+    __shared__ __align__(16) uint32_t sa[ST][K][T];
+    __shared__ __align__(16) uint32_t sm[MASKED ? ST : 1][K][MASKED ? T : 4];
+    __shared__ __align__(16) uint32_t sb[ST][K][BW];
+    __shared__ uint32_t red[8][T];
+
+    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const int x0 = blockIdx.x * T;
+    const int y = blockIdx.y;
+    const int d0 = blockIdx.z * DC;
+    const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
+    const size_t rowbase = size_t(y) * NW;
+    const int nchunks = (NW + K - 1) / K;
+
+    auto load_stage = [&](int c, int st) {
+        const int w0 = c * K;
+        {
+            const int w = tid >> 5, col = (tid & 31) * 4;
+            const bool ok = w0 + w < NW;
+            const size_t off = (rowbase + w0 + w) * Wp + x0 + col;
+            cp_async16(&sa[st][w][col], ok ? dref + off : dref, ok);
+            if constexpr (MASKED) cp_async16(&sm[st][w][col], ok ? mref + off : mref, ok);
+        }
+        for (int t = tid; t < K * (BW / 4); t += 256) {
+            const int w = t / (BW / 4), col = (t - w * (BW / 4)) * 4;
+            const int gcol = bbase + col;
+            const bool ok = (w0 + w < NW) && gcol >= 0 && gcol < Wp;
+            cp_async16(&sb[st][w][col], ok ? doth + (rowbase + w0 + w) * Wp + gcol : doth, ok);
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < nchunks) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    uint32_t acc[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[j][s] = 0;
+
+    const int xs = lane * 4;
+    const int ds = wi * 8;
+    const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
+
+#pragma unroll 1
+    for (int c = 0; c < nchunks; ++c) {
+        cp_async_wait<ST - 2>();
+        __syncthreads();
+        if (c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
+        cp_async_commit();
+        const int st = c % ST;
+#pragma unroll 2
+        for (int w = 0; w < K; ++w) {
+            const uint4 a4 = *reinterpret_cast<const uint4*>(&sa[st][w][xs]);
+            uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(&sm[st][w][xs]);
+            const uint4 b0 = *reinterpret_cast<const uint4*>(&sb[st][w][c0]);
+            const uint4 b1 = *reinterpret_cast<const uint4*>(&sb[st][w][c0 + 4]);
+            const uint4 b2 = *reinterpret_cast<const uint4*>(&sb[st][w][c0 + 8]);
+            const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
+            const uint32_t m[4] = {m4.x, m4.y, m4.z, m4.w};
+            const uint32_t b[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const int e = RIGHT ? j + s : j - s + 8;
+                    uint32_t v = a[j] ^ b[e];
+                    if constexpr (MASKED) v &= m[j];
+                    acc[j][s] += __popc(v);
+                }
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int x = x0 + xs + j;
+        uint32_t best = 0xFFFFFFFFu;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int d = d0 + ds + s;
+            const int xo = RIGHT ? x + d : x - d;
+            const bool ok = d < D && x < W && xo >= 0 && xo < W;
+            const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
+            if (ok && key < best) best = key;
+        }
+        red[wi][xs + j] = best;
+    }
+    __syncthreads();
+    if (tid < T) {
+        uint32_t best = red[0][tid];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) best = min(best, red[w][tid]);
+        const int x = x0 + tid;
+        if (x < W && best != 0xFFFFFFFFu) {
+            if (gridDim.z == 1) keys[size_t(y) * W + x] = best;
+            else atomicMin(&keys[size_t(y) * W + x], best);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5 -- left/right check on WTA keys.  refine.hpp:39-54: valid(x) <=>
+// xr = lround(x - dL) in [0, W) and |dL - dR(xr)| <= tol (inclusive, double).
+// Also emits the (all-valid) WTA maps as float when requested, the band-local
+// max_bin of the checked map (refine.hpp:68-72) and the list of invalid
+// pixels in the refine band [rb0, rb1).
+__global__ void k_lr_check_keys(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr, int W,
+                                int rows, double tol, float* __restrict__ chk_d, uint8_t* __restrict__ chk_v,
+                                float* __restrict__ left_d, float* __restrict__ right_d, int rb0, int rb1,
+                                int* __restrict__ counters, int* __restrict__ inv) {
+    const size_t total = size_t(rows) * W;
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = i < total;
+    int dl = 0;
+    bool ok = false;
+    int yy = 0;
+    if (in) {
+        yy = int(i / W);
+        const int x = int(i - size_t(yy) * W);
+        dl = int(kl[i] & 0xFFFFu);
+        const int xr = x - dl;
+        ok = xr >= 0 && xr < W;
+        if (ok) ok = fabs(double(dl) - double(kr[size_t(yy) * W + xr] & 0xFFFFu)) <= tol;
+        chk_d[i] = float(dl);
+        chk_v[i] = ok ? 1 : 0;
+        if (left_d) left_d[i] = float(dl);
+        if (right_d) right_d[i] = float(kr[i] & 0xFFFFu);
+    }
+    const unsigned full = 0xFFFFFFFFu;
+    const int mb = __reduce_max_sync(full, (in && ok) ? dl : 0);
+    const bool need = in && !ok && yy >= rb0 && yy < rb1;
+    const unsigned ballot = __ballot_sync(full, need);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) {
+        atomicMax(&counters[0], mb);
+        if (ballot) base = atomicAdd(&counters[1], __popc(ballot));
+    }
+    base = __shfl_sync(full, base, 0);
+    if (need) inv[base + __popc(ballot & ((1u << lane) - 1u))] = int(i);
+}
+
+// lr_check on float maps (per-stage API, refine.hpp:39-54).
+__global__ void k_lr_check_float(const float* __restrict__ dl, const float* __restrict__ dr, int W, int H,
+                                 double tol, float* __restrict__ od, uint8_t* __restrict__ ov) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= size_t(W) * H) return;
+    const int y = int(i / W), x = int(i - size_t(y) * W);
+    const float d = dl[i];
+    const long long xr = llround(double(x) - double(d));
+    bool ok = xr >= 0 && xr < W;
+    if (ok) ok = fabs(double(d) - double(dr[size_t(y) * W + xr])) <= tol;
+    od[i] = d;
+    ov[i] = ok ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// K6 -- bilateral voting refinement.  refine.hpp:62-111.  Warp per invalid
+// pixel.  Voters of one window row are examined 32 at a time (lane = column);
+// their bin lround(d) and weight (exact host table, refine.hpp:30-35) are
+// formed in parallel, then folded into the per-warp double bins strictly in
+// row-major voter order (the owner lane of a bin performs its adds in
+// sequence), so every bin sum is bit-identical to the reference's.  Argmax:
+// strict '>' from bin 0 == smallest bin among the maxima.
+__global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __restrict__ cv,
+                              const uint8_t* __restrict__ gray, int W, int rows, int radius,
+                              const double* __restrict__ wtab, int ncol, const int16_t* __restrict__ s2col,
+                              const int* __restrict__ counters, const int* __restrict__ inv,
+                              int nbins_cap, float* __restrict__ od, uint8_t* __restrict__ ov) {
+    extern __shared__ __align__(16) double sbins[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    double* bins = sbins + size_t(warp) * nbins_cap;
+    const int max_bin = counters[0];
+    const int n_inv = counters[1];
+    const unsigned full = 0xFFFFFFFFu;
+    for (int idx = blockIdx.x * nwarps + warp; idx < n_inv; idx += gridDim.x * nwarps) {
+        const int p = inv[idx];
+        const int y = p / W, x = p - y * W;
+        const int u = gray[p];
+        for (int b = lane; b <= max_bin; b += 32) bins[b] = 0.0;
+        __syncwarp();
+        const int y0 = max(0, y - radius), y1 = min(rows - 1, y + radius);
+        const int x0 = max(0, x - radius), x1 = min(W - 1, x + radius);
+        bool any = false;
+        for (int py = y0; py <= y1; ++py) {
+            const int dy2 = (py - y) * (py - y);
+            for (int cx = x0; cx <= x1; cx += 32) {
+                const int px = cx + lane;
+                const size_t j = size_t(py) * W + px;
+                const bool valid = px <= x1 && cv[j];
+                int bin = 0;
+                double wgt = 0.0;
+                if (valid) {
+                    bin = int(llround(double(cd[j])));
+                    const int v = gray[j];
+                    const int hi = max(u, v), lo = min(u, v);
+                    const int s = (px - x) * (px - x) + dy2;
+                    wgt = __ldg(wtab + (size_t(hi * (hi + 1) / 2 + lo) * ncol + s2col[s]));
+                }
+                unsigned m = __ballot_sync(full, valid);
+                any |= m != 0;
+                while (m) {
+                    const int i = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int b = __shfl_sync(full, bin, i);
+                    const double wv = __shfl_sync(full, wgt, i);
+                    if (lane == (b & 31)) bins[b] += wv;
+                }
+            }
+        }
+        __syncwarp();
+        if (!any) {
+            if (lane == 0) {
+                od[p] = 0.0f;
+                ov[p] = 0;
+            }
+            continue;
+        }
+        double bv = -1.0;
+        int bb = 0x7FFFFFFF;
+        for (int b = lane; b <= max_bin; b += 32)
+            if (bins[b] > bv) {
+                bv = bins[b];
+                bb = b;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov2 = __shfl_xor_sync(full, bv, o);
+            const int ob = __shfl_xor_sync(full, bb, o);
+            if (ov2 > bv || (ov2 == bv && ob < bb)) {
+                bv = ov2;
+                bb = ob;
+            }
+        }
+        if (lane == 0) {
+            od[p] = float(bb);
+            ov[p] = 1;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Layout converters for the per-stage API (reference AoS u64 <-> device SoA).
+__global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+                             uint32_t* __restrict__ dst) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, w, x)
+    const size_t total = size_t(H) * NW * Wp;
+    if (i >= total) return;
+    const int x = int(i % Wp);
+    const size_t yw = i / Wp;
+    const int w = int(yw % NW), y = int(yw / NW);
+    dst[i] = x < W ? src[(size_t(y) * W + x) * NW + w] : 0u;
+}
+
+__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+                             uint32_t* __restrict__ dst) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
+    const size_t total = size_t(H) * W * NW;
+    if (i >= total) return;
+    const int w = int(i % NW);
+    const size_t yx = i / NW;
+    const int x = int(yx % W), y = int(yx / W);
+    dst[i] = src[(size_t(y) * NW + w) * Wp + x];
+}
+
+__global__ void k_keys_to_float(const uint32_t* __restrict__ keys, size_t n, float* __restrict__ out) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = float(keys[i] & 0xFFFFu);
+}
+
+// POPC-bound microbenchmark of the cost kernel's word-op (LOP3 + POPC + IADD).
+__global__ void __launch_bounds__(512) k_popc_peak(uint32_t* out, uint32_t seed, int iters) {
+    uint32_t a[8], b[8], m[8], s[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        a[i] = seed * (threadIdx.x + i + 1);
+        b[i] = a[i] ^ (0x9e3779b9u * i);
+        m[i] = ~a[i] + i;
+        s[i] = 0;
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t x = __popc((a[i] ^ b[i]) & m[i]);
+            s[i] += x;
+            b[i] += x;
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r += s[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Context.
+enum Timing { T_H2D, T_DESC, T_MASK, T_WTA_L, T_WTA_R, T_WTA_U, T_LR, T_REFINE, T_D2H, T_COUNT };
+static const char* kTimingNames = "h2d,descriptor,mask,wta_left,wta_right,wta_unmasked,lr_check,refine,d2h";
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap) return BSM_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMalloc: ") + cudaGetErrorString(e));
+        cap = bytes;
+        return BSM_OK;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct bsm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+    // pattern
+    int n = 0, window = 0, half = 0, NW = 0, u = 0, upad = 0;
+    std::vector<int16_t> pairs;
+    std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
+    std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
+    DevBuf d_desc_off, d_pq, d_uoff;
+    int desc_off_tw = -1, uoff_tw = -1;
+    // tables
+    float gray_lut[256], lab_lut[768];
+    DevBuf d_rank;
+    DevBuf d_wtab, d_s2col;
+    double wt_lc = 0, wt_le = 0;
+    int wt_radius = -1, wt_ncol = 0;
+    // scratch
+    DevBuf img_l, img_r, fdl, fml, fdr, fmr, keys_l, keys_r, keys_u;
+    DevBuf chk_d, chk_v, ref_d, ref_v, lw_d, rw_d, un_d, counters, inv;
+    DevBuf aux0, aux1, aux2, aux3;
+    int last_W = 0, last_rows = 0, last_unmasked = 0, last_r0 = 0, last_out0 = 0, last_out_rows = 0;
+    // instrumentation
+    bool profiling = false;
+    cudaEvent_t ev[T_COUNT][2] = {};
+    bool ev_used[T_COUNT] = {};
+    int launches = 0;
+    DevBuf popc_out;
+};
+
+namespace {
+
+struct Scope {  // brackets one pipeline stage with events when profiling
+    bsm_ctx* c;
+    int t;
+    Scope(bsm_ctx* c_, int t_) : c(c_), t(t_) {
+        if (c->profiling) {
+            cudaEventRecord(c->ev[t][0], c->stream);
+            c->ev_used[t] = true;
+        }
+    }
+    ~Scope() {
+        if (c->profiling) cudaEventRecord(c->ev[t][1], c->stream);
+    }
+};
+
+int check_launch(bsm_ctx* c, const char* what) {
+    ++c->launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(BSM_CUDA_ERROR, std::string("CUDA: launch ") + what + ": " + cudaGetErrorString(e));
+    return BSM_OK;
+}
+
+#define BSM_TRY(x)                  \
+    do {                            \
+        int rc_ = (x);              \
+        if (rc_ != BSM_OK) return rc_; \
+    } while (0)
+
+// Tile-relative offset tables depend on the staged tile width.
+int ensure_desc_offsets(bsm_ctx* c) {
+    const int TW = kDescTX + 2 * c->half;
+    if (c->desc_off_tw == TW) return BSM_OK;
+    std::vector<int2> o(size_t(c->n));
+    for (int i = 0; i < c->n; ++i) {
+        const int16_t* p = &c->pairs[4 * size_t(i)];
+        o[size_t(i)] = make_int2(p[1] * TW + p[0], p[3] * TW + p[2]);
+    }
+    BSM_TRY(c->d_desc_off.ensure(o.size() * sizeof(int2)));
+    BSM_CUDA(cudaMemcpy(c->d_desc_off.p, o.data(), o.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    c->desc_off_tw = TW;
+    return BSM_OK;
+}
+
+int ensure_mask_offsets(bsm_ctx* c) {
+    const int TW = kMaskTile + 2 * c->half;
+    if (c->uoff_tw == TW) return BSM_OK;
+    const int side = 2 * c->half + 1;
+    std::vector<int32_t> o(c->used.size());
+    for (size_t k = 0; k < c->used.size(); ++k) {
+        const int dy = c->used[k] / side - c->half, dx = c->used[k] % side - c->half;
+        o[k] = dy * TW + dx;
+    }
+    BSM_TRY(c->d_uoff.ensure(std::max<size_t>(4, o.size() * 4)));
+    BSM_CUDA(cudaMemcpy(c->d_uoff.p, o.data(), o.size() * 4, cudaMemcpyHostToDevice));
+    c->uoff_tw = TW;
+    return BSM_OK;
+}
+
+int ensure_weight_table(bsm_ctx* c, double lc, double le, int radius) {
+    if (c->wt_radius == radius && c->wt_lc == lc && c->wt_le == le) return BSM_OK;
+    std::vector<double> w;
+    std::vector<int16_t> s2col;
+    int ncol = 0;
+    bsmh::vote_weight_table(c->lab_lut, lc, le, radius, w, s2col, ncol);
+    BSM_TRY(c->d_wtab.ensure(w.size() * 8));
+    BSM_TRY(c->d_s2col.ensure(s2col.size() * 2));
+    BSM_CUDA(cudaMemcpy(c->d_wtab.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+    BSM_CUDA(cudaMemcpy(c->d_s2col.p, s2col.data(), s2col.size() * 2, cudaMemcpyHostToDevice));
+    c->wt_lc = lc;
+    c->wt_le = le;
+    c->wt_radius = radius;
+    c->wt_ncol = ncol;
+    return BSM_OK;
+}
+
+int check_pattern(bsm_ctx* c) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    if (c->n <= 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: no sampling pattern set (bsm_set_pattern)");
+    return BSM_OK;
+}
+
+size_t desc_smem(const bsm_ctx* c) {
+    const int TW = kDescTX + 2 * c->half, TH = kDescTY * kDescPY + 2 * c->half;
+    return size_t(c->n) * sizeof(int2) + size_t(TW) * TH;
+}
+
+size_t mask_smem(const bsm_ctx* c) {
+    const int TW = kMaskTile + 2 * c->half, TH = 2 * c->half + 1, G = (c->n + 31) / 32;
+    return size_t(c->n) * 4 + size_t(c->u) * 4 + size_t(G) * kMaskTile * 4 + size_t(kMaskWarps) * c->upad +
+           size_t(TW) * TH;
+}
+
+// Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
+int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
+    const int Wp = round_up(W, 128);
+    BSM_TRY(ensure_desc_offsets(c));
+    BSM_TRY(ensure_mask_offsets(c));
+    {
+        Scope s(c, T_DESC);
+        const size_t sm = desc_smem(c);
+        dim3 grid(Wp / kDescTX, (rows + kDescTY * kDescPY - 1) / (kDescTY * kDescPY));
+        BSM_CUDA(cudaFuncSetAttribute(k_descriptor, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_descriptor<<<grid, dim3(kDescTX, kDescTY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc_off.as<int2>(),
+                                                                       c->n, c->half, c->NW, Wp, desc);
+        BSM_TRY(check_launch(c, "descriptor"));
+    }
+    {
+        Scope s(c, T_MASK);
+        const size_t sm = mask_smem(c);
+        dim3 grid(Wp / kMaskTile, rows);
+        if (c->n <= 4096) {
+            BSM_CUDA(cudaFuncSetAttribute(k_mask<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            k_mask<32><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
+                                                                 c->d_uoff.as<int32_t>(), c->u, c->upad,
+                                                                 c->d_rank.as<uint8_t>(), c->half, c->NW, Wp, mask);
+        } else {
+            BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            k_mask<64><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
+                                                                 c->d_uoff.as<int32_t>(), c->u, c->upad,
+                                                                 c->d_rank.as<uint8_t>(), c->half, c->NW, Wp, mask);
+        }
+        BSM_TRY(check_launch(c, "mask"));
+    }
+    return BSM_OK;
+}
+
+// WTA keys of rows [0, rows) of device fields (SoA); keys: rows x W.
+int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uint32_t* doth, int W, int rows,
+               int d_max, bool right, bool masked, uint32_t* keys, int timing) {
+    Scope s(c, timing);
+    const int Wp = round_up(W, 128);
+    const int dz = (d_max + kCostDisp - 1) / kCostDisp;
+    if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
+    dim3 grid(Wp / kCostTile, rows, dz);
+    if (right) {
+        if (masked) k_cost_wta<true, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+        else k_cost_wta<true, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+    } else {
+        if (masked) k_cost_wta<false, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+        else k_cost_wta<false, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+    }
+    return check_launch(c, "cost_wta");
+}
+
+int validate_params(const bsm_params* p) {
+    if (!p) return set_err(BSM_INVALID_ARGUMENT, "bsm: null params");
+    if (p->d_max < 1) return set_err(BSM_INVALID_ARGUMENT, "config: d_max must be set (>= 1)");
+    if (p->d_max > 65535) return set_err(BSM_UNSUPPORTED, "bsm: d_max > 65535 is outside this build's envelope");
+    if (!(p->lambda_c > 0)) return set_err(BSM_INVALID_ARGUMENT, "config: lambda_c must be > 0");
+    if (!(p->lambda_e > 0)) return set_err(BSM_INVALID_ARGUMENT, "config: lambda_e must be > 0");
+    if (p->lr_tolerance < 0) return set_err(BSM_INVALID_ARGUMENT, "config: lr_tolerance must be >= 0");
+    if (p->vote_radius < 1) return set_err(BSM_INVALID_ARGUMENT, "config: vote_radius must be >= 1");
+    if (p->vote_radius > 180) return set_err(BSM_UNSUPPORTED, "bsm: vote_radius > 180 is outside this build's envelope");
+    return BSM_OK;
+}
+
+// The fused device pipeline.  Views are full W x H device images; the
+// refined output covers rows [out0, out0 + out_rows); fields, WTA and the
+// check cover the halo-extended rows [r0, r1).
+int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int H, int out0, int out_rows,
+                    const bsm_params* p, bool want_unmasked) {
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(validate_params(p));
+    BSM_TRY(ensure_weight_table(c, p->lambda_c, p->lambda_e, p->vote_radius));
+    const int r0 = std::max(0, out0 - p->vote_radius);
+    const int r1 = std::min(H, out0 + out_rows + p->vote_radius);
+    const int rows = r1 - r0;
+    const int Wp = round_up(W, 128);
+    const size_t fbytes = size_t(rows) * c->NW * Wp * 4;
+    const size_t px = size_t(rows) * W;
+    BSM_TRY(c->fdl.ensure(fbytes));
+    BSM_TRY(c->fml.ensure(fbytes));
+    BSM_TRY(c->fdr.ensure(fbytes));
+    BSM_TRY(c->fmr.ensure(fbytes));
+    BSM_TRY(c->keys_l.ensure(px * 4));
+    BSM_TRY(c->keys_r.ensure(px * 4));
+    if (want_unmasked) BSM_TRY(c->keys_u.ensure(px * 4));
+    BSM_TRY(c->chk_d.ensure(px * 4));
+    BSM_TRY(c->chk_v.ensure(px));
+    BSM_TRY(c->ref_d.ensure(px * 4));
+    BSM_TRY(c->ref_v.ensure(px));
+    BSM_TRY(c->lw_d.ensure(px * 4));
+    BSM_TRY(c->rw_d.ensure(px * 4));
+    if (want_unmasked) BSM_TRY(c->un_d.ensure(px * 4));
+    BSM_TRY(c->counters.ensure(64));
+    BSM_TRY(c->inv.ensure(px * 4));
+
+    BSM_TRY(field_device(c, dl, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
+    BSM_TRY(field_device(c, dr, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
+    BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(), W, rows, p->d_max,
+                       false, true, c->keys_l.as<uint32_t>(), T_WTA_L));
+    BSM_TRY(wta_device(c, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>(), c->fdl.as<uint32_t>(), W, rows, p->d_max,
+                       true, true, c->keys_r.as<uint32_t>(), T_WTA_R));
+    if (want_unmasked)
+        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), nullptr, c->fdr.as<uint32_t>(), W, rows, p->d_max, false, false,
+                           c->keys_u.as<uint32_t>(), T_WTA_U));
+    {
+        Scope s(c, T_LR);
+        BSM_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+        const int tb = 256;
+        k_lr_check_keys<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(
+            c->keys_l.as<uint32_t>(), c->keys_r.as<uint32_t>(), W, rows, p->lr_tolerance, c->chk_d.as<float>(),
+            c->chk_v.as<uint8_t>(), c->lw_d.as<float>(), c->rw_d.as<float>(), out0 - r0, out0 - r0 + out_rows,
+            c->counters.as<int>(), c->inv.as<int>());
+        BSM_TRY(check_launch(c, "lr_check"));
+        if (want_unmasked) {
+            k_keys_to_float<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->keys_u.as<uint32_t>(), px,
+                                                                              c->un_d.as<float>());
+            BSM_TRY(check_launch(c, "keys_to_float"));
+        }
+    }
+    {
+        Scope s(c, T_REFINE);
+        BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
+        BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
+        const int nbins = round_up(p->d_max, 32);
+        const int warps = 8;
+        const size_t sm = size_t(warps) * nbins * 8;
+        BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
+            c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, W, rows, p->vote_radius,
+            c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(),
+            nbins, c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+        BSM_TRY(check_launch(c, "vote_refine"));
+    }
+    c->last_W = W;
+    c->last_rows = rows;
+    c->last_r0 = r0;
+    c->last_out0 = out0;
+    c->last_out_rows = out_rows;
+    c->last_unmasked = want_unmasked ? 1 : 0;
+    return BSM_OK;
+}
+
+int fetch(bsm_ctx* c, bsm_maps* o) {
+    if (!o) return BSM_OK;
+    Scope s(c, T_D2H);
+    const int W = c->last_W;
+    const size_t all = size_t(c->last_rows) * W;
+    const size_t off = size_t(c->last_out0 - c->last_r0) * W;
+    const size_t outpx = size_t(c->last_out_rows) * W;
+    auto d2h = [&](void* dst, const DevBuf& b, size_t byte_off, size_t bytes) -> int {
+        if (!dst) return BSM_OK;
+        BSM_CUDA(cudaMemcpyAsync(dst, static_cast<const char*>(b.p) + byte_off, bytes, cudaMemcpyDeviceToHost, c->stream));
+        return BSM_OK;
+    };
+    BSM_TRY(d2h(o->refined_d, c->ref_d, off * 4, outpx * 4));
+    BSM_TRY(d2h(o->refined_v, c->ref_v, off, outpx));
+    BSM_TRY(d2h(o->left_d, c->lw_d, 0, all * 4));
+    BSM_TRY(d2h(o->right_d, c->rw_d, 0, all * 4));
+    BSM_TRY(d2h(o->checked_d, c->chk_d, 0, all * 4));
+    BSM_TRY(d2h(o->checked_v, c->chk_v, 0, all));
+    if (c->last_unmasked) BSM_TRY(d2h(o->unmasked_d, c->un_d, 0, all * 4));
+    return BSM_OK;
+}
+
+int begin_call(bsm_ctx* c) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    BSM_CUDA(cudaSetDevice(c->device));
+    c->launches = 0;
+    for (int t = 0; t < T_COUNT; ++t) c->ev_used[t] = false;
+    return BSM_OK;
+}
+
+int upload_views(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W, int H) {
+    Scope s(c, T_H2D);
+    const size_t n = size_t(W) * H;
+    BSM_TRY(c->img_l.ensure(n));
+    BSM_TRY(c->img_r.ensure(n));
+    BSM_CUDA(cudaMemcpyAsync(c->img_l.p, left, n, cudaMemcpyHostToDevice, c->stream));
+    if (right) BSM_CUDA(cudaMemcpyAsync(c->img_r.p, right, n, cudaMemcpyHostToDevice, c->stream));
+    return BSM_OK;
+}
+
+int sync(bsm_ctx* c) {
+    BSM_CUDA(cudaStreamSynchronize(c->stream));
+    return BSM_OK;
+}
+
+int check_dims(int W, int H) {
+    if (W < 1 || H < 1) return set_err(BSM_INVALID_ARGUMENT, "bsm: image dimensions must be >= 1");
+    if (int64_t(W) * H > (int64_t(1) << 31) - 1)
+        return set_err(BSM_UNSUPPORTED, "bsm: images above 2^31 pixels are outside this build's envelope");
+    return BSM_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+const char* bsm_last_error(void) { return g_err.c_str(); }
+const char* bsm_version(void) { return "bsm-b200 0.1 (sm_100a)"; }
+
+int bsm_ctx_create(int device, bsm_ctx** out) {
+    if (!out) return set_err(BSM_INVALID_ARGUMENT, "bsm: null output pointer");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return set_err(BSM_CUDA_ERROR, std::string("CUDA: no usable device (") + cudaGetErrorString(e) +
+                                           "); this library has no CPU fallback");
+    if (device < 0 || device >= ndev) return set_err(BSM_INVALID_ARGUMENT, "bsm: device index out of range");
+    BSM_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    BSM_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(BSM_CUDA_ERROR, std::string("CUDA: built for sm_100a, device is ") + prop.name);
+    bsm_ctx* c = new bsm_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return set_err(BSM_CUDA_ERROR, "CUDA: stream creation failed");
+    }
+    for (int t = 0; t < T_COUNT; ++t) {
+        cudaEventCreate(&c->ev[t][0]);
+        cudaEventCreate(&c->ev[t][1]);
+    }
+    bsmh::gray_lab_lut(c->gray_lut, c->lab_lut);
+    for (int v = 1; v < 256; ++v)
+        if (!(c->gray_lut[v] > c->gray_lut[v - 1])) {
+            bsm_ctx_destroy(c);
+            return set_err(BSM_UNSUPPORTED, "bsm: gray conversion table is not strictly increasing");
+        }
+    std::vector<uint8_t> rank(65536);
+    bsmh::sad_rank_table(c->lab_lut, rank.data());
+    int rc = c->d_rank.ensure(65536);
+    if (rc == BSM_OK && cudaMemcpy(c->d_rank.p, rank.data(), 65536, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = set_err(BSM_CUDA_ERROR, "CUDA: rank table upload failed");
+    if (rc != BSM_OK) {
+        bsm_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return BSM_OK;
+}
+
+int bsm_ctx_destroy(bsm_ctx* c) {
+    if (!c) return BSM_OK;
+    cudaSetDevice(c->device);
+    DevBuf* bufs[] = {&c->d_desc_off, &c->d_pq, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+                      &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
+                      &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
+                      &c->counters, &c->inv, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
+    for (DevBuf* b : bufs) b->release();
+    for (int t = 0; t < T_COUNT; ++t) {
+        if (c->ev[t][0]) cudaEventDestroy(c->ev[t][0]);
+        if (c->ev[t][1]) cudaEventDestroy(c->ev[t][1]);
+    }
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return BSM_OK;
+}
+
+int bsm_generate_pattern(int n, int window, double spread, uint64_t seed, int16_t* out) {
+    if (!out) return set_err(BSM_INVALID_ARGUMENT, "bsm: null output pointer");
+    std::string err;
+    if (!bsmh::generate_pattern(n, window, spread, seed, out, err)) return set_err(BSM_INVALID_ARGUMENT, err);
+    return BSM_OK;
+}
+
+int bsm_gray_lab_lut(float* gray256, float* lab768) {
+    if (!gray256 || !lab768) return set_err(BSM_INVALID_ARGUMENT, "bsm: null output pointer");
+    bsmh::gray_lab_lut(gray256, lab768);
+    return BSM_OK;
+}
+
+int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
+    if (!c || !pairs) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    if (n < 1) return set_err(BSM_INVALID_ARGUMENT, "pattern: n must be >= 1");
+    if (window < 2) return set_err(BSM_INVALID_ARGUMENT, "pattern: window must be >= 2");
+    if (n > kMaxPairs) return set_err(BSM_UNSUPPORTED, "bsm: n > 8192 is outside this build's envelope");
+    if (window > 128) return set_err(BSM_UNSUPPORTED, "bsm: window > 128 is outside this build's envelope");
+    const int half = window / 2, side = 2 * half + 1;
+    for (int i = 0; i < 4 * n; ++i)
+        if (pairs[i] < -half || pairs[i] > half)
+            return set_err(BSM_INVALID_ARGUMENT, "pattern: offset outside window");
+    BSM_CUDA(cudaSetDevice(c->device));
+    c->n = n;
+    c->window = window;
+    c->half = half;
+    c->NW = 2 * ((n + 63) / 64);
+    c->pairs.assign(pairs, pairs + 4 * size_t(n));
+    // Used window offsets (index into the (2h+1)^2 table, like
+    // build_table_indices, descriptor.hpp:157-168) and per-pair endpoint
+    // indices into that list.
+    std::vector<int> slot(size_t(side) * side, -1);
+    c->used.clear();
+    std::vector<uint32_t> pq(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        int idx[2];
+        for (int e = 0; e < 2; ++e) {
+            const int t = (pairs[4 * i + 2 * e + 1] + half) * side + (pairs[4 * i + 2 * e] + half);
+            if (slot[size_t(t)] < 0) {
+                slot[size_t(t)] = int(c->used.size());
+                c->used.push_back(int16_t(t));
+            }
+            idx[e] = slot[size_t(t)];
+        }
+        pq[size_t(i)] = uint32_t(idx[0]) | (uint32_t(idx[1]) << 16);
+    }
+    c->u = int(c->used.size());
+    c->upad = round_up(c->u, 16);
+    BSM_TRY(c->d_pq.ensure(pq.size() * 4));
+    BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
+    c->desc_off_tw = -1;
+    c->uoff_tw = -1;
+    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024)
+        return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
+    return BSM_OK;
+}
+
+int bsm_compute_field_u8(bsm_ctx* c, const uint8_t* img, int W, int H, uint64_t* desc, uint64_t* mask) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    if (!img) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    const int Wp = round_up(W, 128);
+    const size_t fbytes = size_t(H) * c->NW * Wp * 4;
+    BSM_TRY(upload_views(c, img, nullptr, W, H));
+    BSM_TRY(c->fdl.ensure(fbytes));
+    BSM_TRY(c->fml.ensure(fbytes));
+    BSM_TRY(field_device(c, c->img_l.as<uint8_t>(), W, H, 0, H, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
+    const size_t aos = size_t(H) * W * c->NW;
+    BSM_TRY(c->aux0.ensure(aos * 4));
+    const int tb = 256;
+    for (int which = 0; which < 2; ++which) {
+        uint64_t* dst = which == 0 ? desc : mask;
+        if (!dst) continue;
+        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(
+            which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H, c->NW, Wp, c->aux0.as<uint32_t>());
+        BSM_TRY(check_launch(c, "soa_to_aos"));
+        BSM_CUDA(cudaMemcpyAsync(dst, c->aux0.p, aos * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSM_TRY(sync(c));
+    }
+    return sync(c);
+}
+
+int bsm_wta(bsm_ctx* c, const uint64_t* desc_ref, const uint64_t* mask_ref, const uint64_t* desc_other, int W,
+            int H, int n, int d_max, int right_ref, int use_mask, float* out_d) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_dims(W, H));
+    if (!desc_ref || !desc_other || (use_mask && !mask_ref))
+        return set_err(BSM_INVALID_ARGUMENT, "bsm: null field");
+    if (d_max < 1) return set_err(BSM_INVALID_ARGUMENT, "wta: d_max must be >= 1");
+    if (d_max > 65535) return set_err(BSM_UNSUPPORTED, "bsm: d_max > 65535 is outside this build's envelope");
+    if (n < 1 || n > kMaxPairs) return set_err(BSM_UNSUPPORTED, "bsm: n outside [1, 8192]");
+    const int NW = 2 * ((n + 63) / 64);
+    const int savedNW = c->NW;
+    c->NW = NW;
+    const int Wp = round_up(W, 128);
+    const size_t aos = size_t(H) * W * NW, soa = size_t(H) * NW * Wp;
+    int rc = BSM_OK;
+    do {
+        if ((rc = c->aux0.ensure(aos * 4)) != BSM_OK) break;
+        if ((rc = c->fdl.ensure(soa * 4)) != BSM_OK) break;
+        if ((rc = c->fml.ensure(soa * 4)) != BSM_OK) break;
+        if ((rc = c->fdr.ensure(soa * 4)) != BSM_OK) break;
+        if ((rc = c->keys_l.ensure(size_t(H) * W * 4)) != BSM_OK) break;
+        if ((rc = c->lw_d.ensure(size_t(H) * W * 4)) != BSM_OK) break;
+        const int tb = 256;
+        const uint64_t* srcs[3] = {desc_ref, use_mask ? mask_ref : nullptr, desc_other};
+        DevBuf* dsts[3] = {&c->fdl, &c->fml, &c->fdr};
+        for (int k = 0; k < 3 && rc == BSM_OK; ++k) {
+            if (!srcs[k]) continue;
+            if (cudaMemcpyAsync(c->aux0.p, srcs[k], aos * 4, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+                rc = set_err(BSM_CUDA_ERROR, "CUDA: field upload failed");
+                break;
+            }
+            k_aos_to_soa<<<unsigned((soa + tb - 1) / tb), tb, 0, c->stream>>>(c->aux0.as<uint32_t>(), W, H, NW, Wp,
+                                                                            dsts[k]->as<uint32_t>());
+            rc = check_launch(c, "aos_to_soa");
+            if (rc == BSM_OK) rc = sync(c);  // aux0 is reused by the next upload
+        }
+        if (rc != BSM_OK) break;
+        rc = wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(), W, H, d_max,
+                        right_ref != 0, use_mask != 0, c->keys_l.as<uint32_t>(), right_ref ? T_WTA_R : T_WTA_L);
+        if (rc != BSM_OK) break;
+        const size_t px = size_t(H) * W;
+        k_keys_to_float<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->keys_l.as<uint32_t>(), px,
+                                                                          c->lw_d.as<float>());
+        if ((rc = check_launch(c, "keys_to_float")) != BSM_OK) break;
+        if (out_d && cudaMemcpyAsync(out_d, c->lw_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
+            rc = set_err(BSM_CUDA_ERROR, "CUDA: download failed");
+            break;
+        }
+        rc = sync(c);
+    } while (0);
+    c->NW = savedNW;
+    return rc;
+}
+
+int bsm_lr_check(bsm_ctx* c, const float* left_d, const float* right_d, int W, int H, double tol, float* out_d,
+                 uint8_t* out_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_dims(W, H));
+    if (!left_d || !right_d) return set_err(BSM_INVALID_ARGUMENT, "bsm: null map");
+    const size_t px = size_t(W) * H;
+    BSM_TRY(c->aux0.ensure(px * 4));
+    BSM_TRY(c->aux1.ensure(px * 4));
+    BSM_TRY(c->aux2.ensure(px * 4));
+    BSM_TRY(c->aux3.ensure(px));
+    BSM_CUDA(cudaMemcpyAsync(c->aux0.p, left_d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->aux1.p, right_d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    const int tb = 256;
+    k_lr_check_float<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->aux0.as<float>(), c->aux1.as<float>(), W,
+                                                                       H, tol, c->aux2.as<float>(),
+                                                                       c->aux3.as<uint8_t>());
+    BSM_TRY(check_launch(c, "lr_check_float"));
+    if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->aux2.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->aux3.p, px, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c);
+}
+
+int bsm_vote_refine_u8(bsm_ctx* c, const float* d, const uint8_t* v, const uint8_t* gray_img, int W, int H,
+                       double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_dims(W, H));
+    if (!d || !v || !gray_img) return set_err(BSM_INVALID_ARGUMENT, "bsm: null input");
+    if (!(lambda_c > 0)) return set_err(BSM_INVALID_ARGUMENT, "refine: lambda_c must be > 0");
+    if (!(lambda_e > 0)) return set_err(BSM_INVALID_ARGUMENT, "refine: lambda_e must be > 0");
+    if (vote_radius < 1) return set_err(BSM_INVALID_ARGUMENT, "refine: vote_radius must be >= 1");
+    if (vote_radius > 180) return set_err(BSM_UNSUPPORTED, "bsm: vote_radius > 180 is outside this build's envelope");
+    const size_t px = size_t(W) * H;
+    // Host pre-pass over the caller's map: max_bin (refine.hpp:68-72) and the
+    // invalid list.  Valid disparities must round to a bin >= 0.
+    int max_bin = 0;
+    std::vector<int> invalid;
+    for (size_t i = 0; i < px; ++i) {
+        if (v[i]) {
+            const double dv = double(d[i]);
+            if (!(dv > -0.5) || !(dv < 1e6)) return set_err(BSM_INVALID_ARGUMENT, "vote_refine: valid disparity out of range");
+            max_bin = std::max(max_bin, int(std::lround(dv)));
+        } else {
+            invalid.push_back(int(i));
+        }
+    }
+    if (max_bin + 1 > 12288) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too large for the refine bins");
+    BSM_TRY(ensure_weight_table(c, lambda_c, lambda_e, vote_radius));
+    BSM_TRY(c->img_l.ensure(px));
+    BSM_TRY(c->chk_d.ensure(px * 4));
+    BSM_TRY(c->chk_v.ensure(px));
+    BSM_TRY(c->ref_d.ensure(px * 4));
+    BSM_TRY(c->ref_v.ensure(px));
+    BSM_TRY(c->counters.ensure(64));
+    BSM_TRY(c->inv.ensure(std::max<size_t>(4, invalid.size() * 4)));
+    BSM_CUDA(cudaMemcpyAsync(c->img_l.p, gray_img, px, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->chk_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->chk_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
+    int cnt[2] = {max_bin, int(invalid.size())};
+    BSM_CUDA(cudaMemcpyAsync(c->counters.p, cnt, 8, cudaMemcpyHostToDevice, c->stream));
+    if (!invalid.empty())
+        BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_TRY(sync(c));  // host staging buffers (cnt, invalid) go out of scope
+    const int nbins = round_up(max_bin + 1, 32);
+    const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
+    const size_t sm = size_t(warps) * nbins * 8;
+    BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
+        c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), W, H, vote_radius,
+        c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins,
+        c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+    BSM_TRY(check_launch(c, "vote_refine"));
+    if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->ref_v.p, px, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c);
+}
+
+int bsm_pipeline_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W, int H, const bsm_params* params,
+                    int want_unmasked, bsm_maps* out) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    BSM_TRY(upload_views(c, left, right, W, H));
+    BSM_TRY(pipeline_device(c, c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>(), W, H, 0, H, params,
+                            want_unmasked != 0));
+    BSM_TRY(fetch(c, out));
+    return sync(c);
+}
+
+int bsm_pipeline_u8_device(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_right, int W, int H,
+                           const bsm_params* params, int want_unmasked) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    if (!d_left || !d_right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    return pipeline_device(c, d_left, d_right, W, H, 0, H, params, want_unmasked != 0);
+}
+
+int bsm_fetch_maps(bsm_ctx* c, bsm_maps* out) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    if (c->last_W == 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: no pipeline result to fetch");
+    BSM_TRY(fetch(c, out));
+    return sync(c);
+}
+
+int bsm_pipeline_band_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W, int H, int y0, int y1,
+                         const bsm_params* params, float* refined_d, uint8_t* refined_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    if (y0 < 0 || y1 > H || y0 >= y1) return set_err(BSM_INVALID_ARGUMENT, "bsm: band rows out of range");
+    BSM_TRY(upload_views(c, left, right, W, H));
+    BSM_TRY(pipeline_device(c, c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>(), W, H, y0, y1 - y0, params, false));
+    bsm_maps m = {};
+    m.refined_d = refined_d;
+    m.refined_v = refined_v;
+    BSM_TRY(fetch(c, &m));
+    return sync(c);
+}
+
+int bsm_stream(bsm_ctx* c, void** stream) {
+    if (!c || !stream) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    *stream = c->stream;
+    return BSM_OK;
+}
+
+int bsm_set_profiling(bsm_ctx* c, int enable) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    c->profiling = enable != 0;
+    return BSM_OK;
+}
+
+int bsm_last_timings(bsm_ctx* c, float* ms, int max, int* count) {
+    if (!c || !ms) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    BSM_CUDA(cudaStreamSynchronize(c->stream));
+    const int k = std::min(max, int(T_COUNT));
+    for (int t = 0; t < k; ++t) {
+        ms[t] = 0.0f;
+        if (c->profiling && c->ev_used[t]) cudaEventElapsedTime(&ms[t], c->ev[t][0], c->ev[t][1]);
+    }
+    if (count) *count = k;
+    return BSM_OK;
+}
+
+const char* bsm_timing_names(void) { return kTimingNames; }
+
+int bsm_last_launch_count(bsm_ctx* c, int* count) {
+    if (!c || !count) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    *count = c->launches;
+    return BSM_OK;
+}
+
+int bsm_measure_popc_peak(bsm_ctx* c, double* ops_per_s) {
+    if (!c || !ops_per_s) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    BSM_CUDA(cudaSetDevice(c->device));
+    const int blocks = c->sm_count * 4, threads = 512, iters = 8192;
+    BSM_TRY(c->popc_out.ensure(size_t(blocks) * threads * 4));
+    cudaEvent_t e0, e1;
+    BSM_CUDA(cudaEventCreate(&e0));
+    BSM_CUDA(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0, c->stream);
+        k_popc_peak<<<blocks, threads, 0, c->stream>>>(c->popc_out.as<uint32_t>(), 7u + r, iters);
+        cudaEventRecord(e1, c->stream);
+        BSM_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ops_per_s = double(blocks) * threads * iters * 8 / (double(best) * 1e-3);
+    return BSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    import oracle
+    return oracle.Reference()
+
+
+@pytest.fixture(scope="session")
+def orc():
+    import oracle
+    return oracle.Restatement()
+
+
+@pytest.fixture(scope="session")
+def default_pairs(ref):
+    return ref.generate_pattern(4096, 26, 4.0, 42)
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    import paper_1402_2020_b200 as bsm
+    return bsm.Context(0)
+
+
+def random_u8(h, w, seed):
+    return np.random.default_rng(seed).integers(0, 256, size=(h, w), dtype=np.uint8)
