@@ -241,6 +241,143 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
+// K2' -- mask for n <= 4096: one warp per CTA, 8 pixels per CTA, two pixels
+// per pass.  Same contract as k_mask; restructured for issue rate:
+//   * the warp's rank table rho[] sits at the start of dynamic shared memory
+//     (a constant base, so every gather is one LDS [R + imm]) and holds both
+//     pixels' ranks as one u32 (rhoA | rhoB << 16) per used offset: one
+//     gather serves two pixels and a = max(rhoP, rhoQ) of both is one
+//     VIMNMX.U16x2;
+//   * pair endpoints come pre-scaled (byte offsets 4P | 4Q << 16) from a
+//     4096-entry L1-resident table; pairs >= n point at a sentinel entry
+//     (a = 255), so the unrolled gather loop has no branches;
+//   * lane l keeps a of pair 32g+l for g = 0..127 as bytes
+//     [A(2j) B(2j) A(2j+1) B(2j+1)] in 64 registers;
+//   * selection: step 1 counts a > 127 (bit 7); each pixel then maps its bytes
+//     into a 0..128 window (low range: min(a,128); high range: a-128 or 0) so
+//     every later count is IADD + LOP3 + shift-add per 4 values:
+//     bit 7 of (a' + 127 - t) == (a' > t), per-byte thresholds, no carries;
+//   * output: one ballot per (group, pixel); lanes 0..3 store the four words
+//     of a register pair in one STS.
+constexpr int kM3Px = 8;
+
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_off) {
+    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + byte_off);
+}
+
+__global__ void __launch_bounds__(32, 16)
+    k_mask3(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint32_t* __restrict__ pqb,
+            int n, const int32_t* __restrict__ uoff, int u, int rho_words, const uint8_t* __restrict__ rank,
+            int half, int NW, int Wp, uint32_t* __restrict__ mask) {
+    constexpr int NREG = 64;  // 128 groups x 2 pixels, 4 bytes per register
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t* rho = dsm;                                   // rho_words (u + sentinel)
+    uint32_t* stage = dsm + rho_words;                     // G x kM3Px
+    const int G = (n + 31) >> 5;
+    uint8_t* tile = reinterpret_cast<uint8_t*>(stage + G * kM3Px);  // (2h+1) x (kM3Px + 2h)
+    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
+    const int lane = threadIdx.x;
+    const int x0 = blockIdx.x * kM3Px;
+    const int ly = blockIdx.y;
+    const int y = ybeg + ly;
+    for (int idx = lane; idx < TW * TH; idx += 32) {
+        const int r = idx / TW, c = idx - r * TW;
+        const int gx = min(max(x0 - half + c, 0), W - 1);
+        const int gy = min(max(y - half + r, 0), H - 1);
+        tile[idx] = __ldg(img + size_t(gy) * W + gx);
+    }
+    if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
+    __syncwarp();
+
+    const int k = max(1, n / 4);
+    const unsigned full = 0xFFFFFFFFu;
+    const int slots = 32 * 2 * NREG;  // per pixel, pads included (always "greater")
+#pragma unroll 1
+    for (int q = 0; q < kM3Px; q += 2) {
+        const int cia = half * TW + half + q, cib = cia + 1;
+        const uint8_t* ra = rank + 256 * int(tile[cia]);
+        const uint8_t* rb = rank + 256 * int(tile[cib]);
+        for (int j = lane; j < u; j += 32) {
+            const int o = __ldg(uoff + j);
+            rho[j] = uint32_t(__ldg(ra + tile[cia + o])) | (uint32_t(__ldg(rb + tile[cib + o])) << 16);
+        }
+        __syncwarp();
+
+        uint32_t R[NREG];
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) {
+            const uint32_t e0 = __ldg(pqb + 64 * j + lane);
+            const uint32_t e1 = __ldg(pqb + 64 * j + 32 + lane);
+            const uint32_t m0 = vmax_u16x2(lds_u32(rho, e0 & 0xFFFFu), lds_u32(rho, e0 >> 16));
+            const uint32_t m1 = vmax_u16x2(lds_u32(rho, e1 & 0xFFFFu), lds_u32(rho, e1 >> 16));
+            R[j] = __byte_perm(m0, m1, 0x6420);
+        }
+        __syncwarp();  // rho is rewritten by the next pass
+
+        // Step 1: #{a > 127} per pixel (bytes 0,2 -> A, 1,3 -> B).
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) acc += (R[j] & 0x80808080u) >> 7;
+        int gtA = __reduce_add_sync(full, (acc & 0xFFu) + ((acc >> 16) & 0xFFu));
+        int gtB = __reduce_add_sync(full, ((acc >> 8) & 0xFFu) + (acc >> 24));
+        const uint32_t Hm = (slots - gtA < k ? 0x00FF00FFu : 0u) | (slots - gtB < k ? 0xFF00FF00u : 0u);
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) {
+            const uint32_t b = R[j] & 0x80808080u;
+            const uint32_t S = b - (b >> 7);  // 0x7F where a >= 128
+            // high range: R & S (a - 128, or 0); low range: R & ~S (a, or 0x80 where a >= 128)
+            R[j] = R[j] & ((S & Hm) | (~S & ~Hm));
+        }
+        int loA = 0, hiA = 127, loB = 0, hiB = 127;
+#pragma unroll 1
+        for (int it = 0; it < 7; ++it) {
+            const int midA = (loA + hiA) >> 1, midB = (loB + hiB) >> 1;
+            const uint32_t K = uint32_t(127 - midA) * 0x00010001u + uint32_t(127 - midB) * 0x01000100u;
+            uint32_t c = 0;
+#pragma unroll
+            for (int j = 0; j < NREG; ++j) c += ((R[j] + K) & 0x80808080u) >> 7;
+            gtA = __reduce_add_sync(full, (c & 0xFFu) + ((c >> 16) & 0xFFu));
+            gtB = __reduce_add_sync(full, ((c >> 8) & 0xFFu) + (c >> 24));
+            if (slots - gtA >= k) hiA = midA; else loA = midA + 1;
+            if (slots - gtB >= k) hiB = midB; else loB = midB + 1;
+        }
+        // Output: bit = a <= T  <=>  not (a' > t).  Lane 0..3 store words
+        // (2j, A), (2j, B), (2j+1, A), (2j+1, B).
+        const uint32_t K = uint32_t(127 - loA) * 0x00010001u + uint32_t(127 - loB) * 0x01000100u;
+        const int sg = lane >> 1, sp = q + (lane & 1);
+#pragma unroll
+        for (int j = 0; j < NREG; ++j) {
+            const uint32_t f = (R[j] + K) & 0x80808080u;
+            const uint32_t wA0 = __ballot_sync(full, !(f & 0x80u));
+            const uint32_t wB0 = __ballot_sync(full, !(f & 0x8000u));
+            const uint32_t wA1 = __ballot_sync(full, !(f & 0x800000u));
+            const uint32_t wB1 = __ballot_sync(full, !(f & 0x80000000u));
+            const uint32_t wv = lane == 0 ? wA0 : lane == 1 ? wB0 : lane == 2 ? wA1 : wB1;
+            const int g = 2 * j + sg;
+            if (lane < 4 && g < G) stage[g * kM3Px + sp] = wv;
+        }
+    }
+    __syncwarp();
+    // Tail mask of the last partial word, then coalesced rows of 8 words.
+    const int rem = n & 31;
+    for (int idx = lane; idx < NW * kM3Px; idx += 32) {
+        const int w = idx / kM3Px, j = idx - w * kM3Px;
+        uint32_t v = 0;
+        if (w < G) {
+            v = stage[w * kM3Px + j];
+            if (rem && w == G - 1) v &= (1u << rem) - 1u;
+        }
+        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
 // (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
 // :68-75 (ties -> smaller d).  No cost volume is materialised.
@@ -606,7 +743,7 @@ struct bsm_ctx {
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
-    DevBuf d_desc_off, d_pq, d_uoff;
+    DevBuf d_desc_off, d_pq, d_pqb, d_uoff;
     int desc_off_tw = -1, uoff_tw = -1;
     // tables
     float gray_lut[256], lab_lut[768];
@@ -621,8 +758,9 @@ struct bsm_ctx {
     int last_W = 0, last_rows = 0, last_unmasked = 0, last_r0 = 0, last_out0 = 0, last_out_rows = 0;
     // instrumentation
     bool profiling = false;
-    cudaEvent_t ev[T_COUNT][2] = {};
-    bool ev_used[T_COUNT] = {};
+    static constexpr int kEvPerSlot = 4;  // a stage may run several times per call (two views)
+    cudaEvent_t ev[T_COUNT][kEvPerSlot][2] = {};
+    int ev_used[T_COUNT] = {};
     int launches = 0;
     DevBuf popc_out;
 };
@@ -632,14 +770,15 @@ namespace {
 struct Scope {  // brackets one pipeline stage with events when profiling
     bsm_ctx* c;
     int t;
+    int slot = -1;
     Scope(bsm_ctx* c_, int t_) : c(c_), t(t_) {
-        if (c->profiling) {
-            cudaEventRecord(c->ev[t][0], c->stream);
-            c->ev_used[t] = true;
+        if (c->profiling && c->ev_used[t] < bsm_ctx::kEvPerSlot) {
+            slot = c->ev_used[t]++;
+            cudaEventRecord(c->ev[t][slot][0], c->stream);
         }
     }
     ~Scope() {
-        if (c->profiling) cudaEventRecord(c->ev[t][1], c->stream);
+        if (slot >= 0) cudaEventRecord(c->ev[t][slot][1], c->stream);
     }
 };
 
@@ -671,8 +810,8 @@ int ensure_desc_offsets(bsm_ctx* c) {
     return BSM_OK;
 }
 
-int ensure_mask_offsets(bsm_ctx* c) {
-    const int TW = kMaskTile + 2 * c->half;
+int ensure_mask_offsets(bsm_ctx* c, int tile_px) {
+    const int TW = tile_px + 2 * c->half;
     if (c->uoff_tw == TW) return BSM_OK;
     const int side = 2 * c->half + 1;
     std::vector<int32_t> o(c->used.size());
@@ -720,11 +859,16 @@ size_t mask_smem(const bsm_ctx* c) {
            size_t(TW) * TH;
 }
 
+size_t mask3_smem(const bsm_ctx* c) {
+    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1, G = (c->n + 31) / 32;
+    return size_t(c->u + 1) * 4 + size_t(G) * kM3Px * 4 + size_t(TW) * TH;
+}
+
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
     const int Wp = round_up(W, 128);
     BSM_TRY(ensure_desc_offsets(c));
-    BSM_TRY(ensure_mask_offsets(c));
+    BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? kM3Px : kMaskTile));
     {
         Scope s(c, T_DESC);
         const size_t sm = desc_smem(c);
@@ -739,10 +883,12 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         const size_t sm = mask_smem(c);
         dim3 grid(Wp / kMaskTile, rows);
         if (c->n <= 4096) {
-            BSM_CUDA(cudaFuncSetAttribute(k_mask<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            k_mask<32><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
-                                                                 c->d_uoff.as<int32_t>(), c->u, c->upad,
-                                                                 c->d_rank.as<uint8_t>(), c->half, c->NW, Wp, mask);
+            const size_t sm3 = mask3_smem(c);
+            BSM_CUDA(cudaFuncSetAttribute(k_mask3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+            dim3 grid3(Wp / kM3Px, rows);
+            k_mask3<<<grid3, 32, sm3, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint32_t>(), c->n,
+                                                   c->d_uoff.as<int32_t>(), c->u, c->u + 1, c->d_rank.as<uint8_t>(),
+                                                   c->half, c->NW, Wp, mask);
         } else {
             BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             k_mask<64><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
@@ -888,7 +1034,7 @@ int begin_call(bsm_ctx* c) {
     if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
     BSM_CUDA(cudaSetDevice(c->device));
     c->launches = 0;
-    for (int t = 0; t < T_COUNT; ++t) c->ev_used[t] = false;
+    for (int t = 0; t < T_COUNT; ++t) c->ev_used[t] = 0;
     return BSM_OK;
 }
 
@@ -944,10 +1090,11 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
         delete c;
         return set_err(BSM_CUDA_ERROR, "CUDA: stream creation failed");
     }
-    for (int t = 0; t < T_COUNT; ++t) {
-        cudaEventCreate(&c->ev[t][0]);
-        cudaEventCreate(&c->ev[t][1]);
-    }
+    for (int t = 0; t < T_COUNT; ++t)
+        for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
+            cudaEventCreate(&c->ev[t][s][0]);
+            cudaEventCreate(&c->ev[t][s][1]);
+        }
     bsmh::gray_lab_lut(c->gray_lut, c->lab_lut);
     for (int v = 1; v < 256; ++v)
         if (!(c->gray_lut[v] > c->gray_lut[v - 1])) {
@@ -970,15 +1117,16 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_desc_off, &c->d_pq, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_desc_off, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
     for (DevBuf* b : bufs) b->release();
-    for (int t = 0; t < T_COUNT; ++t) {
-        if (c->ev[t][0]) cudaEventDestroy(c->ev[t][0]);
-        if (c->ev[t][1]) cudaEventDestroy(c->ev[t][1]);
-    }
+    for (int t = 0; t < T_COUNT; ++t)
+        for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
+            if (c->ev[t][s][0]) cudaEventDestroy(c->ev[t][s][0]);
+            if (c->ev[t][s][1]) cudaEventDestroy(c->ev[t][s][1]);
+        }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return BSM_OK;
@@ -1035,9 +1183,15 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     c->upad = round_up(c->u, 16);
     BSM_TRY(c->d_pq.ensure(pq.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
+    // k_mask3: byte offsets into its u32 rank table; pads -> sentinel slot u.
+    std::vector<uint32_t> pqb(4096, (uint32_t(4 * c->u) | (uint32_t(4 * c->u) << 16)));
+    for (int i = 0; i < std::min(n, 4096); ++i)
+        pqb[size_t(i)] = (4 * (pq[size_t(i)] & 0xFFFFu)) | ((4 * (pq[size_t(i)] >> 16)) << 16);
+    BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
+    BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
     c->desc_off_tw = -1;
     c->uoff_tw = -1;
-    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024)
+    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024 || mask3_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
 }
@@ -1265,7 +1419,11 @@ int bsm_last_timings(bsm_ctx* c, float* ms, int max, int* count) {
     const int k = std::min(max, int(T_COUNT));
     for (int t = 0; t < k; ++t) {
         ms[t] = 0.0f;
-        if (c->profiling && c->ev_used[t]) cudaEventElapsedTime(&ms[t], c->ev[t][0], c->ev[t][1]);
+        for (int s = 0; s < c->ev_used[t]; ++s) {
+            float v = 0.0f;
+            cudaEventElapsedTime(&v, c->ev[t][s][0], c->ev[t][s][1]);
+            ms[t] += v;
+        }
     }
     if (count) *count = k;
     return BSM_OK;
