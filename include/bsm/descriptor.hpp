@@ -1,0 +1,109 @@
+// bsm/descriptor.hpp -- DescriptorField and the descriptor/mask API
+// (reference descriptor.hpp:18-239).  compute_field runs on the GPU
+// (bsm_compute_field_u8: kernels k_descriptor + k_mask3); the single-pixel
+// compute_descriptor / compute_mask are answered from the same device field
+// so they agree with it by construction.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <span>
+#include <vector>
+
+#include "../bsm_cuda.h"
+#include "bsm/bitstring.hpp"
+#include "bsm/detail_cabi.hpp"
+#include "bsm/errors.hpp"
+#include "bsm/image.hpp"
+#include "bsm/pattern.hpp"
+
+namespace bsm {
+
+class DescriptorField {
+public:
+    DescriptorField() = default;
+    DescriptorField(int width, int height, int n_bits)
+        : width_(width), height_(height), n_(n_bits), words_(words_for_bits(n_bits)),
+          desc_(std::size_t(width) * height * std::size_t(words_), 0),
+          mask_(std::size_t(width) * height * std::size_t(words_), 0) {}
+
+    int width() const { return width_; }
+    int height() const { return height_; }
+    int bits() const { return n_; }
+    int words_per_string() const { return words_; }
+
+    std::span<const uint64_t> descriptor(int x, int y) const { return {&desc_[index(x, y)], std::size_t(words_)}; }
+    std::span<const uint64_t> mask(int x, int y) const { return {&mask_[index(x, y)], std::size_t(words_)}; }
+    std::span<uint64_t> descriptor(int x, int y) { return {&desc_[index(x, y)], std::size_t(words_)}; }
+    std::span<uint64_t> mask(int x, int y) { return {&mask_[index(x, y)], std::size_t(words_)}; }
+    BitString descriptor_at(int x, int y) const { return bits_of(descriptor(x, y)); }
+    BitString mask_at(int x, int y) const { return bits_of(mask(x, y)); }
+
+    // Flat AoS storage, index ((y*W + x) * words) -- the C ABI's layout.
+    uint64_t* descriptor_data() { return desc_.data(); }
+    uint64_t* mask_data() { return mask_.data(); }
+    const uint64_t* descriptor_data() const { return desc_.data(); }
+    const uint64_t* mask_data() const { return mask_.data(); }
+
+private:
+    std::size_t index(int x, int y) const { return (std::size_t(y) * width_ + x) * std::size_t(words_); }
+    BitString bits_of(std::span<const uint64_t> w) const {
+        BitString b(n_);
+        std::copy(w.begin(), w.end(), b.words().begin());
+        return b;
+    }
+    int width_ = 0, height_ = 0, n_ = 0, words_ = 0;
+    std::vector<uint64_t> desc_, mask_;
+};
+
+// The floor(n/4)-th smallest weight, rank from 1 (host scalar helper).
+inline float quarter_threshold(std::span<const float> weights, std::vector<float>& scratch) {
+    if (weights.empty()) throw InvalidArgument("quarter_threshold: empty weight sequence");
+    const std::size_t rank = std::max<std::size_t>(1, weights.size() / 4);
+    scratch.assign(weights.begin(), weights.end());
+    std::nth_element(scratch.begin(), scratch.begin() + std::ptrdiff_t(rank - 1), scratch.end());
+    return scratch[rank - 1];
+}
+
+inline float quarter_threshold(std::span<const float> weights) {
+    std::vector<float> s;
+    return quarter_threshold(weights, s);
+}
+
+namespace detail {
+inline DescriptorField field_u8(const std::vector<uint8_t>& img, int W, int H, const SamplingPattern& pat) {
+    Context& ctx = context();
+    ctx.use_pattern(flat_pairs(pat), pat.n, pat.window);
+    DescriptorField f(W, H, pat.n);
+    throw_status(bsm_compute_field_u8(ctx.get(), img.data(), W, H, f.descriptor_data(), f.mask_data()));
+    return f;
+}
+}  // namespace detail
+
+inline DescriptorField compute_field(const GrayImage& gray, const LabImage& lab, const SamplingPattern& pat,
+                                     int threads = 1) {
+    (void)threads;
+    if (gray.width != lab.width || gray.height != lab.height)
+        throw DimensionMismatch("compute_field: gray/lab dimensions differ");
+    const auto u8 = detail::u8_from_planes(&gray, &lab);
+    if (!u8) detail::colour_unsupported("compute_field");
+    return detail::field_u8(*u8, gray.width, gray.height, pat);
+}
+
+inline BitString compute_descriptor(const GrayImage& gray, const SamplingPattern& pat, int x, int y) {
+    if (x < 0 || x >= gray.width || y < 0 || y >= gray.height)
+        throw InvalidArgument("compute_descriptor: pixel outside image");
+    const auto u8 = detail::u8_from_planes(&gray, nullptr);
+    if (!u8) detail::colour_unsupported("compute_descriptor");
+    return detail::field_u8(*u8, gray.width, gray.height, pat).descriptor_at(x, y);
+}
+
+inline BitString compute_mask(const LabImage& lab, const SamplingPattern& pat, int x, int y) {
+    if (x < 0 || x >= lab.width || y < 0 || y >= lab.height)
+        throw InvalidArgument("compute_mask: pixel outside image");
+    const auto u8 = detail::u8_from_planes(nullptr, &lab);
+    if (!u8) detail::colour_unsupported("compute_mask");
+    return detail::field_u8(*u8, lab.width, lab.height, pat).mask_at(x, y);
+}
+
+}  // namespace bsm

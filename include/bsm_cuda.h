@@ -81,6 +81,10 @@ int bsm_set_pattern(bsm_ctx* ctx, const int16_t* pairs, int n, int window);
 /* to_gray / to_lab of the gray pixel (v,v,v), v = 0..255 (image.hpp:90-140). */
 int bsm_gray_lab_lut(float* gray256, float* lab768);
 
+/* to_gray / to_lab (image.hpp:90-140) of an interleaved RGB image, host-side
+ * (floating point compiled like the reference); gray / lab may be NULL. */
+int bsm_to_gray_lab(const uint8_t* rgb, int W, int H, float* gray, float* lab);
+
 /* compute_field (descriptor.hpp:200-239) of a grayscale view (r=g=b=img).
  * desc/mask: W*H*words64 uint64 each, AoS. */
 int bsm_compute_field_u8(bsm_ctx* ctx, const uint8_t* img, int W, int H, uint64_t* desc, uint64_t* mask);

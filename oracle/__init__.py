@@ -89,6 +89,14 @@ class Restatement(_Lib):
         self.f("gray_lab_lut", [_P, _P], None)(_p(g), _p(l))
         return g, l
 
+    def to_gray_lab(self, rgb):
+        rgb = np.ascontiguousarray(rgb, np.uint8)
+        H, W = rgb.shape[:2]
+        g = np.zeros((H, W), np.float32)
+        l = np.zeros((H, W, 3), np.float32)
+        self.f("to_gray_lab", [_P, _I, _I, _P, _P], None)(_p(rgb), W, H, _p(g), _p(l))
+        return g, l
+
     def compute_field_u8(self, img, pairs, window):
         img = np.ascontiguousarray(img, np.uint8)
         H, W = img.shape
@@ -173,6 +181,14 @@ class Reference(_Lib):
         g = np.zeros(256, np.float32)
         l = np.zeros((256, 3), np.float32)
         self.f("gray_lab_lut", [_P, _P], None)(_p(g), _p(l))
+        return g, l
+
+    def to_gray_lab(self, rgb):
+        rgb = np.ascontiguousarray(rgb, np.uint8)
+        H, W = rgb.shape[:2]
+        g = np.zeros((H, W), np.float32)
+        l = np.zeros((H, W, 3), np.float32)
+        self.f("to_gray_lab", [_P, _I, _I, _P, _P], None)(_p(rgb), W, H, _p(g), _p(l))
         return g, l
 
     def compute_field_u8(self, img, pairs, window, threads=1):

@@ -33,7 +33,7 @@ from ._lib import (
 
 __all__ = [
     "BsmConfig", "SamplingPattern", "DisparityMap", "PipelineResult", "Context",
-    "generate_pattern", "gray_lab_lut", "compute_field", "wta", "lr_check",
+    "generate_pattern", "gray_lab_lut", "to_gray_lab", "compute_field", "wta", "lr_check",
     "vote_refine", "run_pipeline", "run_pipeline_band", "default_context",
     "BsmError", "InvalidArgument", "DimensionMismatch", "CudaError", "Unsupported",
     "GENERATOR_NAME",
@@ -221,6 +221,18 @@ def gray_lab_lut():
     g = np.zeros(256, np.float32)
     l = np.zeros((256, 3), np.float32)
     check(lib().bsm_gray_lab_lut(_ptr(g), _ptr(l)))
+    return g, l
+
+
+def to_gray_lab(rgb):
+    """to_gray / to_lab (image.hpp:90-140) of an (H, W, 3) uint8 image, host-side."""
+    a = np.ascontiguousarray(rgb, dtype=np.uint8)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise InvalidArgument("bsm: to_gray_lab expects an (H, W, 3) uint8 image")
+    H, W = a.shape[:2]
+    g = np.zeros((H, W), np.float32)
+    l = np.zeros((H, W, 3), np.float32)
+    check(lib().bsm_to_gray_lab(_ptr(a), W, H, _ptr(g), _ptr(l)))
     return g, l
 
 

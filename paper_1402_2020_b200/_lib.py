@@ -83,6 +83,7 @@ _SIGS = {
     "bsm_generate_pattern": [_I, _I, _D, C.c_uint64, _P],
     "bsm_set_pattern": [_P, _P, _I, _I],
     "bsm_gray_lab_lut": [_P, _P],
+    "bsm_to_gray_lab": [_P, _I, _I, _P, _P],
     "bsm_compute_field_u8": [_P, _P, _I, _I, _P, _P],
     "bsm_wta": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P],
     "bsm_lr_check": [_P, _P, _P, _I, _I, _D, _P, _P],

@@ -69,20 +69,36 @@ double cie_f(double t) {
 }
 }  // namespace
 
+namespace {
+// BT.601 luma in float, same expression shape as image.hpp:95.
+float luma(uint8_t r, uint8_t g, uint8_t b) { return 0.299f * float(r) + 0.587f * float(g) + 0.114f * float(b); }
+
+void lab_of(uint8_t R, uint8_t G, uint8_t B, float* out) {
+    const double r = decode(R / 255.0), g = decode(G / 255.0), b = decode(B / 255.0);
+    // sRGB -> XYZ (D65) normalised by the matrix row sums (image.hpp:113-115).
+    const double X = (0.4124564 * r + 0.3575761 * g + 0.1804375 * b) / 0.9504700;
+    const double Y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
+    const double Z = (0.0193339 * r + 0.1191920 * g + 0.9503041 * b) / 1.0888300;
+    const double fx = cie_f(X), fy = cie_f(Y), fz = cie_f(Z);
+    out[0] = float(std::clamp(116.0 * fy - 16.0, 0.0, 100.0));
+    out[1] = float(500.0 * (fx - fy));
+    out[2] = float(200.0 * (fy - fz));
+}
+}  // namespace
+
 void gray_lab_lut(float* gray256, float* lab768) {
     for (int v = 0; v < 256; ++v) {
         const uint8_t c = uint8_t(v);
-        // BT.601 luma in float, same expression shape as image.hpp:95.
-        gray256[v] = 0.299f * float(c) + 0.587f * float(c) + 0.114f * float(c);
-        const double r = decode(c / 255.0), g = decode(c / 255.0), b = decode(c / 255.0);
-        // sRGB -> XYZ (D65) normalised by the matrix row sums (image.hpp:113-115).
-        const double X = (0.4124564 * r + 0.3575761 * g + 0.1804375 * b) / 0.9504700;
-        const double Y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
-        const double Z = (0.0193339 * r + 0.1191920 * g + 0.9503041 * b) / 1.0888300;
-        const double fx = cie_f(X), fy = cie_f(Y), fz = cie_f(Z);
-        lab768[3 * v + 0] = float(std::clamp(116.0 * fy - 16.0, 0.0, 100.0));
-        lab768[3 * v + 1] = float(500.0 * (fx - fy));
-        lab768[3 * v + 2] = float(200.0 * (fy - fz));
+        gray256[v] = luma(c, c, c);
+        lab_of(c, c, c, lab768 + 3 * v);
+    }
+}
+
+void to_gray_lab(const uint8_t* rgb, size_t npx, float* gray, float* lab) {
+    for (size_t i = 0; i < npx; ++i) {
+        const uint8_t* p = rgb + 3 * i;
+        if (gray) gray[i] = luma(p[0], p[1], p[2]);
+        if (lab) lab_of(p[0], p[1], p[2], lab + 3 * i);
     }
 }
 

@@ -5,6 +5,7 @@
 // FP contraction on (bsm_host.cpp), so its floating point matches the
 // reference's default -O3 -march=native build.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -16,6 +17,9 @@ bool generate_pattern(int n, int window, double spread, uint64_t seed, int16_t* 
 
 // image.hpp:90-140 for (v,v,v).
 void gray_lab_lut(float* gray256, float* lab768);
+
+// Per-pixel to_gray / to_lab of interleaved RGB (image.hpp:90-140).
+void to_gray_lab(const uint8_t* rgb, size_t npx, float* gray, float* lab);
 
 // rank[c*256 + v] = dense rank of lab_sad(Lab[c], Lab[v]) among the 256 values
 // of row c (equal values share a rank).  lab_sad: image.hpp:144-146.

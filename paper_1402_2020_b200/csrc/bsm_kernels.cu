@@ -1145,6 +1145,13 @@ int bsm_gray_lab_lut(float* gray256, float* lab768) {
     return BSM_OK;
 }
 
+int bsm_to_gray_lab(const uint8_t* rgb, int W, int H, float* gray, float* lab) {
+    if (!rgb) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    if (W < 1 || H < 1) return set_err(BSM_INVALID_ARGUMENT, "bsm: image dimensions must be >= 1");
+    bsmh::to_gray_lab(rgb, size_t(W) * size_t(H), gray, lab);
+    return BSM_OK;
+}
+
 int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     if (!c || !pairs) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
     if (n < 1) return set_err(BSM_INVALID_ARGUMENT, "pattern: n must be >= 1");
