@@ -128,8 +128,12 @@ int bsm_last_timings(bsm_ctx* ctx, float* ms, int max, int* count);
 const char* bsm_timing_names(void);
 /* Kernel launches issued by the last pipeline call. */
 int bsm_last_launch_count(bsm_ctx* ctx, int* count);
-/* Measured POPC word-op throughput of this device (ops/s), microbenchmark. */
+/* Measured masked-XOR-popcount word-op throughput of this device (words/s),
+ * register-only microbenchmarks of the cost kernel's two instruction mixes:
+ * direct (LOP3 + POPC + IADD per word) and carry-save (per two words:
+ * 4 LOP3 + POPC + IMAD).  Either pointer may be NULL. */
 int bsm_measure_popc_peak(bsm_ctx* ctx, double* ops_per_s);
+int bsm_measure_word_peaks(bsm_ctx* ctx, double* popc_words_per_s, double* csa_words_per_s);
 
 #ifdef __cplusplus
 }

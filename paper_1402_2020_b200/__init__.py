@@ -189,6 +189,12 @@ class Context:
         check(lib().bsm_measure_popc_peak(self.handle, C.byref(v)))
         return float(v.value)
 
+    def measure_word_peaks(self) -> tuple:
+        """(direct POPC mix, carry-save mix) word-op rates of this GPU, words/s."""
+        a, b = C.c_double(), C.c_double()
+        check(lib().bsm_measure_word_peaks(self.handle, C.byref(a), C.byref(b)))
+        return float(a.value), float(b.value)
+
 
 _tls = threading.local()
 

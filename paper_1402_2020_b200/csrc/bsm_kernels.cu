@@ -272,15 +272,17 @@ __device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_
 }
 
 __global__ void __launch_bounds__(32, 16)
-    k_mask3(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint32_t* __restrict__ pqb,
-            int n, const int32_t* __restrict__ uoff, int u, int rho_words, const uint8_t* __restrict__ rank,
-            int half, int NW, int Wp, uint32_t* __restrict__ mask) {
+    k_mask3(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
+            const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
+            const uint8_t* __restrict__ rank, int half, int NW, int Wp, uint32_t* __restrict__ mask) {
     constexpr int NREG = 64;  // 128 groups x 2 pixels, 4 bytes per register
+    constexpr int GMAX = 2 * NREG;
     extern __shared__ __align__(16) uint32_t dsm[];
-    uint32_t* rho = dsm;                                   // rho_words (u + sentinel)
-    uint32_t* stage = dsm + rho_words;                     // G x kM3Px
+    uint32_t* rho = dsm;                                               // rho_words (u + sentinel)
+    uint32_t* stage = dsm + rho_words;                                 // GMAX x kM3Px
+    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + GMAX * kM3Px);  // 2 x 256 rank rows
+    uint8_t* tile = rrows + 512;                                       // (2h+1) x (kM3Px + 2h)
     const int G = (n + 31) >> 5;
-    uint8_t* tile = reinterpret_cast<uint8_t*>(stage + G * kM3Px);  // (2h+1) x (kM3Px + 2h)
     const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
@@ -297,33 +299,39 @@ __global__ void __launch_bounds__(32, 16)
 
     const int k = max(1, n / 4);
     const unsigned full = 0xFFFFFFFFu;
-    const int slots = 32 * 2 * NREG;  // per pixel, pads included (always "greater")
+    const int slots = 32 * GMAX;  // per pixel, pads included (always "greater")
 #pragma unroll 1
     for (int q = 0; q < kM3Px; q += 2) {
         const int cia = half * TW + half + q, cib = cia + 1;
-        const uint8_t* ra = rank + 256 * int(tile[cia]);
-        const uint8_t* rb = rank + 256 * int(tile[cib]);
+        // the two centres' rank rows (rank[c][*], 256 B each) into shared memory
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(rank + 256 * int(lane < 16 ? tile[cia] : tile[cib]));
+            reinterpret_cast<uint4*>(rrows)[lane] = __ldg(src + (lane & 15));
+        }
+        __syncwarp();
         for (int j = lane; j < u; j += 32) {
             const int o = __ldg(uoff + j);
-            rho[j] = uint32_t(__ldg(ra + tile[cia + o])) | (uint32_t(__ldg(rb + tile[cib + o])) << 16);
+            rho[j] = uint32_t(rrows[tile[cia + o]]) | (uint32_t(rrows[256 + tile[cib + o]]) << 16);
         }
         __syncwarp();
 
         uint32_t R[NREG];
+        uint32_t acc = 0;  // step 1: #{a > 127}, bytes 0,2 -> A, 1,3 -> B
 #pragma unroll
-        for (int j = 0; j < NREG; ++j) {
-            const uint32_t e0 = __ldg(pqb + 64 * j + lane);
-            const uint32_t e1 = __ldg(pqb + 64 * j + 32 + lane);
-            const uint32_t m0 = vmax_u16x2(lds_u32(rho, e0 & 0xFFFFu), lds_u32(rho, e0 >> 16));
-            const uint32_t m1 = vmax_u16x2(lds_u32(rho, e1 & 0xFFFFu), lds_u32(rho, e1 >> 16));
-            R[j] = __byte_perm(m0, m1, 0x6420);
+        for (int jj = 0; jj < NREG / 2; ++jj) {
+            const uint4 P = __ldg(p4 + 32 * jj + lane);  // byte offsets of groups 4jj..4jj+3
+            const uint4 Q = __ldg(q4 + 32 * jj + lane);
+            const uint32_t m0 = vmax_u16x2(lds_u32(rho, P.x), lds_u32(rho, Q.x));
+            const uint32_t m1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
+            const uint32_t m2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
+            const uint32_t m3 = vmax_u16x2(lds_u32(rho, P.w), lds_u32(rho, Q.w));
+            R[2 * jj] = __byte_perm(m0, m1, 0x6420);
+            R[2 * jj + 1] = __byte_perm(m2, m3, 0x6420);
+            acc = __umulhi(R[2 * jj] & 0x80808080u, 1u << 25) + acc;
+            acc = __umulhi(R[2 * jj + 1] & 0x80808080u, 1u << 25) + acc;
         }
-        __syncwarp();  // rho is rewritten by the next pass
+        __syncwarp();  // rho and rrows are rewritten by the next pass
 
-        // Step 1: #{a > 127} per pixel (bytes 0,2 -> A, 1,3 -> B).
-        uint32_t acc = 0;
-#pragma unroll
-        for (int j = 0; j < NREG; ++j) acc += (R[j] & 0x80808080u) >> 7;
         int gtA = __reduce_add_sync(full, (acc & 0xFFu) + ((acc >> 16) & 0xFFu));
         int gtB = __reduce_add_sync(full, ((acc >> 8) & 0xFFu) + (acc >> 24));
         const uint32_t Hm = (slots - gtA < k ? 0x00FF00FFu : 0u) | (slots - gtB < k ? 0xFF00FF00u : 0u);
@@ -341,16 +349,18 @@ __global__ void __launch_bounds__(32, 16)
             const uint32_t K = uint32_t(127 - midA) * 0x00010001u + uint32_t(127 - midB) * 0x01000100u;
             uint32_t c = 0;
 #pragma unroll
-            for (int j = 0; j < NREG; ++j) c += ((R[j] + K) & 0x80808080u) >> 7;
+            for (int j = 0; j < NREG; ++j) c = __umulhi((R[j] + K) & 0x80808080u, 1u << 25) + c;
             gtA = __reduce_add_sync(full, (c & 0xFFu) + ((c >> 16) & 0xFFu));
             gtB = __reduce_add_sync(full, ((c >> 8) & 0xFFu) + (c >> 24));
             if (slots - gtA >= k) hiA = midA; else loA = midA + 1;
             if (slots - gtB >= k) hiB = midB; else loB = midB + 1;
         }
-        // Output: bit = a <= T  <=>  not (a' > t).  Lane 0..3 store words
-        // (2j, A), (2j, B), (2j+1, A), (2j+1, B).
+        // Output: bit = a <= T  <=>  not (a' > t).  Lanes 0..3 store words
+        // (2j, A), (2j, B), (2j+1, A), (2j+1, B); pad groups land in stage rows
+        // >= G and are never copied out.
         const uint32_t K = uint32_t(127 - loA) * 0x00010001u + uint32_t(127 - loB) * 0x01000100u;
-        const int sg = lane >> 1, sp = q + (lane & 1);
+        uint32_t* sdst = stage + (lane >> 1) * kM3Px + q + (lane & 1);
+        const bool writer = lane < 4;
 #pragma unroll
         for (int j = 0; j < NREG; ++j) {
             const uint32_t f = (R[j] + K) & 0x80808080u;
@@ -359,8 +369,7 @@ __global__ void __launch_bounds__(32, 16)
             const uint32_t wA1 = __ballot_sync(full, !(f & 0x800000u));
             const uint32_t wB1 = __ballot_sync(full, !(f & 0x80000000u));
             const uint32_t wv = lane == 0 ? wA0 : lane == 1 ? wB0 : lane == 2 ? wA1 : wB1;
-            const int g = 2 * j + sg;
-            if (lane < 4 && g < G) stage[g * kM3Px + sp] = wv;
+            if (writer) sdst[2 * j * kM3Px] = wv;
         }
     }
     __syncwarp();
@@ -371,6 +380,182 @@ __global__ void __launch_bounds__(32, 16)
         uint32_t v = 0;
         if (w < G) {
             v = stage[w * kM3Px + j];
+            if (rem && w == G - 1) v &= (1u << rem) - 1u;
+        }
+        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2'' -- mask for n <= 4096 on bit planes.  Lane l owns pairs
+// [128l, 128l + 128) in four chunks of 32; for two pixels per pass it
+//   1. gathers a = max(rhoP, rhoQ) of both pixels per pair (one u32 rank-table
+//      gather + VIMNMX.U16x2 serves both), packs each pixel's 32 chunk values
+//      into eight byte registers,
+//   2. transposes them into 8 bit planes (four 8x8 bit-matrix transposes and a
+//      4x4 byte transpose): plane j, word m of lane l holds bit j of a for
+//      pairs 128l + 32m + t at bit t -- exactly the layout of output word
+//      4l + m,
+//   3. selects the k-th smallest a MSB-first on the planes (per bit: LOP3 +
+//      POPC per word, one REDUX), and
+//   4. emits bit = a <= T with an 8-plane comparator, one word per (lane, m).
+// Small loop bodies (no 64-register arrays), so the code stays cache-resident.
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x = x ^ t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x = x ^ t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    return x ^ t ^ (t << 28);  // byte j, bit k  <-  byte k, bit j
+}
+
+// w[0..7]: 32 byte values (value t = byte t%4 of w[t/4]); planes[j] bit t = bit j of value t.
+__device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t (&pl)[8]) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint64_t y = transpose8x8(uint64_t(w[2 * b]) | (uint64_t(w[2 * b + 1]) << 32));
+        lo[b] = uint32_t(y);
+        hi[b] = uint32_t(y >> 32);
+    }
+    // 4x4 byte transposes: plane j = byte j of block 0..3
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t* s = h ? hi : lo;
+        const uint32_t t0 = __byte_perm(s[0], s[1], 0x5140), t1 = __byte_perm(s[0], s[1], 0x7362);
+        const uint32_t t2 = __byte_perm(s[2], s[3], 0x5140), t3 = __byte_perm(s[2], s[3], 0x7362);
+        pl[4 * h + 0] = __byte_perm(t0, t2, 0x5410);
+        pl[4 * h + 1] = __byte_perm(t0, t2, 0x7632);
+        pl[4 * h + 2] = __byte_perm(t1, t3, 0x5410);
+        pl[4 * h + 3] = __byte_perm(t1, t3, 0x7632);
+    }
+}
+
+constexpr int kM4Stage = 132;  // stage row stride (words): 16-B aligned, conflict-free read-out
+
+__global__ void __launch_bounds__(32, 16)
+    k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
+            const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
+            const uint8_t* __restrict__ rank, int half, int NW, int Wp, uint32_t* __restrict__ mask) {
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
+    uint32_t* planes = rho + rho_words;                   // [2 px][8 planes][4 chunks][32 lanes]
+    uint32_t* stage = planes + 2 * 8 * 4 * 32;            // [kM3Px][kM4Stage]
+    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * kM4Stage);  // 2 x 256
+    uint8_t* tile = rrows + 512;                                            // (2h+1) x (kM3Px + 2h)
+    const int G = (n + 31) >> 5;
+    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
+    const int lane = threadIdx.x;
+    const int x0 = blockIdx.x * kM3Px;
+    const int ly = blockIdx.y;
+    const int y = ybeg + ly;
+    for (int idx = lane; idx < TW * TH; idx += 32) {
+        const int r = idx / TW, c = idx - r * TW;
+        const int gx = min(max(x0 - half + c, 0), W - 1);
+        const int gy = min(max(y - half + r, 0), H - 1);
+        tile[idx] = __ldg(img + size_t(gy) * W + gx);
+    }
+    if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
+    __syncwarp();
+
+    const int k = max(1, n / 4);
+    const unsigned full = 0xFFFFFFFFu;
+#pragma unroll 1
+    for (int q = 0; q < kM3Px; q += 2) {
+        const int cia = half * TW + half + q, cib = cia + 1;
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(rank + 256 * int(lane < 16 ? tile[cia] : tile[cib]));
+            reinterpret_cast<uint4*>(rrows)[lane] = __ldg(src + (lane & 15));
+        }
+        __syncwarp();
+        for (int j = lane; j < u; j += 32) {
+            const int o = __ldg(uoff + j);
+            rho[j] = uint32_t(rrows[tile[cia + o]]) | (uint32_t(rrows[256 + tile[cib + o]]) << 16);
+        }
+        __syncwarp();
+
+#pragma unroll 1
+        for (int m = 0; m < 4; ++m) {
+            uint32_t wa[8], wb[8];
+#pragma unroll
+            for (int t4 = 0; t4 < 8; ++t4) {
+                const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                const uint32_t v0 = vmax_u16x2(lds_u32(rho, P.x), lds_u32(rho, Q.x));
+                const uint32_t v1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
+                const uint32_t v2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
+                const uint32_t v3 = vmax_u16x2(lds_u32(rho, P.w), lds_u32(rho, Q.w));
+                const uint32_t x01 = __byte_perm(v0, v1, 0x6240);  // [A0 A1 B0 B1]
+                const uint32_t x23 = __byte_perm(v2, v3, 0x6240);  // [A2 A3 B2 B3]
+                wa[t4] = __byte_perm(x01, x23, 0x5410);
+                wb[t4] = __byte_perm(x01, x23, 0x7632);
+            }
+            uint32_t pa[8], pb[8];
+            bytes_to_planes(wa, pa);
+            bytes_to_planes(wb, pb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                planes[((0 * 8 + j) * 4 + m) * 32 + lane] = pa[j];
+                planes[((1 * 8 + j) * 4 + m) * 32 + lane] = pb[j];
+            }
+        }
+        __syncwarp();  // rho / rrows are rewritten by the next pass
+
+#pragma unroll 1
+        for (int px = 0; px < 2; ++px) {
+            uint32_t P[8][4];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) P[j][m] = planes[((px * 8 + j) * 4 + m) * 32 + lane];
+            // MSB-first selection of the k-th smallest a (pads are 255: never below a real k-th).
+            uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u};
+            int kk = k, T = 0;
+#pragma unroll
+            for (int j = 7; j >= 0; --j) {
+                const int zl = __popc(eq[0] & ~P[j][0]) + __popc(eq[1] & ~P[j][1]) + __popc(eq[2] & ~P[j][2]) +
+                               __popc(eq[3] & ~P[j][3]);
+                const int zeros = int(__reduce_add_sync(full, uint32_t(zl)));
+                if (zeros >= kk) {
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) eq[m] &= ~P[j][m];
+                } else {
+                    kk -= zeros;
+                    T |= 1 << j;
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) eq[m] &= P[j][m];
+                }
+            }
+            // bit = a <= T: (a < T) | (a == T); eq already holds a == T.
+            uint32_t lt[4] = {0u, 0u, 0u, 0u}, e2[4] = {~0u, ~0u, ~0u, ~0u};
+#pragma unroll
+            for (int j = 7; j >= 0; --j) {
+                if ((T >> j) & 1) {
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        lt[m] |= e2[m] & ~P[j][m];
+                        e2[m] &= P[j][m];
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) e2[m] &= ~P[j][m];
+                }
+            }
+            uint4 o;
+            o.x = lt[0] | e2[0];
+            o.y = lt[1] | e2[1];
+            o.z = lt[2] | e2[2];
+            o.w = lt[3] | e2[3];
+            *reinterpret_cast<uint4*>(stage + (q + px) * kM4Stage + 4 * lane) = o;
+        }
+    }
+    __syncwarp();
+    const int rem = n & 31;
+    for (int idx = lane; idx < NW * kM3Px; idx += 32) {
+        const int w = idx / kM3Px, j = idx - w * kM3Px;
+        uint32_t v = 0;
+        if (w < G) {
+            v = stage[j * kM4Stage + w];
             if (rem && w == G - 1) v &= (1u << rem) - 1u;
         }
         mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
@@ -404,7 +589,9 @@ template <bool RIGHT, bool MASKED>
 __global__ void __launch_bounds__(256, 2)
     k_cost_wta(const uint32_t* __restrict__ dref, const uint32_t* __restrict__ mref,
                const uint32_t* __restrict__ doth, int W, int rows, int NW, int Wp, int D,
-               uint32_t* __restrict__ keys) {
+               uint32_t* __restrict__ keys, uint32_t two) {
+    // `two` == 2 at run time: a register multiplier keeps the carry-save
+    // accumulate an IMAD (FMA pipe) instead of an IADD3 (ALU pipe).
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
     __shared__ __align__(16) uint32_t sa[ST][K][T];
     __shared__ __align__(16) uint32_t sm[MASKED ? ST : 1][K][MASKED ? T : 4];
@@ -442,11 +629,14 @@ __global__ void __launch_bounds__(256, 2)
         cp_async_commit();
     }
 
-    uint32_t acc[4][8];
+    uint32_t acc[4][8], ones[4][8];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int s = 0; s < 8; ++s) acc[j][s] = 0;
+        for (int s = 0; s < 8; ++s) {
+            acc[j][s] = 0;
+            ones[j][s] = 0;
+        }
 
     const int xs = lane * 4;
     const int ds = wi * 8;
@@ -459,29 +649,50 @@ __global__ void __launch_bounds__(256, 2)
         if (c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
         cp_async_commit();
         const int st = c % ST;
-#pragma unroll 2
-        for (int w = 0; w < K; ++w) {
-            const uint4 a4 = *reinterpret_cast<const uint4*>(&sa[st][w][xs]);
-            uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-            if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(&sm[st][w][xs]);
-            const uint4 b0 = *reinterpret_cast<const uint4*>(&sb[st][w][c0]);
-            const uint4 b1 = *reinterpret_cast<const uint4*>(&sb[st][w][c0 + 4]);
-            const uint4 b2 = *reinterpret_cast<const uint4*>(&sb[st][w][c0 + 8]);
-            const uint32_t a[4] = {a4.x, a4.y, a4.z, a4.w};
-            const uint32_t m[4] = {m4.x, m4.y, m4.z, m4.w};
-            const uint32_t b[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+        // Two words per step through a carry-save accumulator (Harley-Seal
+        // with one level): ones' = ones ^ x0 ^ x1, twos = maj(ones, x0, x1),
+        // acc += 2 * popc(twos).  One POPC per two words instead of two; the
+        // LOP3s and the IMAD accumulate run on the ALU and FMA pipes beside it.
+#pragma unroll 1
+        for (int w = 0; w < K; w += 2) {
+            uint32_t a[2][4], m[2][4], b[2][12];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 a4 = *reinterpret_cast<const uint4*>(&sa[st][w + h][xs]);
+                uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(&sm[st][w + h][xs]);
+                const uint4 b0 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0]);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0 + 4]);
+                const uint4 b2 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0 + 8]);
+                a[h][0] = a4.x; a[h][1] = a4.y; a[h][2] = a4.z; a[h][3] = a4.w;
+                m[h][0] = m4.x; m[h][1] = m4.y; m[h][2] = m4.z; m[h][3] = m4.w;
+                b[h][0] = b0.x; b[h][1] = b0.y; b[h][2] = b0.z; b[h][3] = b0.w;
+                b[h][4] = b1.x; b[h][5] = b1.y; b[h][6] = b1.z; b[h][7] = b1.w;
+                b[h][8] = b2.x; b[h][9] = b2.y; b[h][10] = b2.z; b[h][11] = b2.w;
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int s = 0; s < 8; ++s) {
                     const int e = RIGHT ? j + s : j - s + 8;
-                    uint32_t v = a[j] ^ b[e];
-                    if constexpr (MASKED) v &= m[j];
-                    acc[j][s] += __popc(v);
+                    uint32_t x0 = a[0][j] ^ b[0][e];
+                    uint32_t x1 = a[1][j] ^ b[1][e];
+                    if constexpr (MASKED) {
+                        x0 &= m[0][j];
+                        x1 &= m[1][j];
+                    }
+                    const uint32_t o = ones[j][s];
+                    const uint32_t twos = (o & x0) | (o & x1) | (x0 & x1);
+                    ones[j][s] = o ^ x0 ^ x1;
+                    acc[j][s] = __popc(twos) * two + acc[j][s];
                 }
         }
     }
     cp_async_wait<0>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[j][s] += __popc(ones[j][s]);
 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -681,7 +892,11 @@ __global__ void k_keys_to_float(const uint32_t* __restrict__ keys, size_t n, flo
     if (i < n) out[i] = float(keys[i] & 0xFFFFu);
 }
 
-// POPC-bound microbenchmark of the cost kernel's word-op (LOP3 + POPC + IADD).
+// Roofline microbenchmarks of the cost kernel's inner loop (register-only,
+// 8 independent chains per thread, 2048 threads per SM):
+//   k_popc_peak: one word per LOP3 + POPC + IADD (the direct mix);
+//   k_csa_peak:  two words per 4 LOP3 + POPC + IMAD (the carry-save mix the
+//                kernel uses; balances the ALU and POPC pipes).
 __global__ void __launch_bounds__(512) k_popc_peak(uint32_t* out, uint32_t seed, int iters) {
     uint32_t a[8], b[8], m[8], s[8];
 #pragma unroll
@@ -702,6 +917,32 @@ __global__ void __launch_bounds__(512) k_popc_peak(uint32_t* out, uint32_t seed,
     uint32_t r = 0;
 #pragma unroll
     for (int i = 0; i < 8; i++) r += s[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(512) k_csa_peak(uint32_t* out, uint32_t seed, int iters, uint32_t two) {
+    uint32_t a[8], b[8], m[8], o[8], s[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        a[i] = seed * (threadIdx.x + i + 1);
+        b[i] = (seed + 0x9e3779b9u) * (threadIdx.x * 7u + i + 3u);
+        m[i] = ~a[i] + i;
+        o[i] = 0;
+        s[i] = 0;
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t x0 = (a[i] ^ s[i]) & m[i];
+            const uint32_t x1 = (b[i] ^ o[i]) & m[i];
+            const uint32_t t = (o[i] & x0) | (o[i] & x1) | (x0 & x1);
+            o[i] = o[i] ^ x0 ^ x1;
+            s[i] = __popc(t) * two + s[i];
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r += s[i] + o[i];
     out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }
 
@@ -859,9 +1100,15 @@ size_t mask_smem(const bsm_ctx* c) {
            size_t(TW) * TH;
 }
 
+size_t mask4_smem(const bsm_ctx* c) {
+    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
+    return size_t(round_up(c->u + 1, 4)) * 4 + 2 * 8 * 4 * 32 * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
+           size_t(TW) * TH;
+}
+
 size_t mask3_smem(const bsm_ctx* c) {
-    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1, G = (c->n + 31) / 32;
-    return size_t(c->u + 1) * 4 + size_t(G) * kM3Px * 4 + size_t(TW) * TH;
+    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
+    return size_t(round_up(c->u + 1, 4)) * 4 + size_t(128) * kM3Px * 4 + 512 + size_t(TW) * TH;
 }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
@@ -883,11 +1130,12 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         const size_t sm = mask_smem(c);
         dim3 grid(Wp / kMaskTile, rows);
         if (c->n <= 4096) {
-            const size_t sm3 = mask3_smem(c);
-            BSM_CUDA(cudaFuncSetAttribute(k_mask3, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm3)));
+            const size_t sm4 = mask4_smem(c);
+            BSM_CUDA(cudaFuncSetAttribute(k_mask4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
             dim3 grid3(Wp / kM3Px, rows);
-            k_mask3<<<grid3, 32, sm3, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint32_t>(), c->n,
-                                                   c->d_uoff.as<int32_t>(), c->u, c->u + 1, c->d_rank.as<uint8_t>(),
+            k_mask4<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
+                                                   c->d_pqb.as<uint4>() + 3 * 1024, c->n,
+                                                   c->d_uoff.as<int32_t>(), c->u, round_up(c->u + 1, 4), c->d_rank.as<uint8_t>(),
                                                    c->half, c->NW, Wp, mask);
         } else {
             BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
@@ -909,11 +1157,11 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
     dim3 grid(Wp / kCostTile, rows, dz);
     if (right) {
-        if (masked) k_cost_wta<true, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
-        else k_cost_wta<true, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+        if (masked) k_cost_wta<true, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
+        else k_cost_wta<true, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
     } else {
-        if (masked) k_cost_wta<false, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
-        else k_cost_wta<false, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys);
+        if (masked) k_cost_wta<false, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
+        else k_cost_wta<false, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
     }
     return check_launch(c, "cost_wta");
 }
@@ -1190,15 +1438,30 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     c->upad = round_up(c->u, 16);
     BSM_TRY(c->d_pq.ensure(pq.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
-    // k_mask3: byte offsets into its u32 rank table; pads -> sentinel slot u.
-    std::vector<uint32_t> pqb(4096, (uint32_t(4 * c->u) | (uint32_t(4 * c->u) << 16)));
-    for (int i = 0; i < std::min(n, 4096); ++i)
-        pqb[size_t(i)] = (4 * (pq[size_t(i)] & 0xFFFFu)) | ((4 * (pq[size_t(i)] >> 16)) << 16);
+    // k_mask3: byte offsets into its u32 rank table, P and Q as two tables of
+    // uint4 [jj][lane] = groups 4jj..4jj+3 of pair 32g + lane; pads -> the
+    // sentinel slot u.
+    std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->u));
+    for (int i = 0; i < std::min(n, 4096); ++i) {
+        const int g = i >> 5, l = i & 31;
+        const size_t at = (size_t(g >> 2) * 32 + l) * 4 + (g & 3);
+        pqb[at] = 4 * (pq[size_t(i)] & 0xFFFFu);
+        pqb[4096 + at] = 4 * (pq[size_t(i)] >> 16);
+    }
+    // k_mask4: lane-block order -- lane l, chunk m, t: pair 128l + 32m + t at
+    // uint4 [(m*8 + t/4)*32 + l], component t%4.
+    pqb.resize(4 * 4096, uint32_t(4 * c->u));
+    for (int i = 0; i < std::min(n, 4096); ++i) {
+        const int l = i >> 7, m = (i >> 5) & 3, t = i & 31;
+        const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
+        pqb[2 * 4096 + at] = 4 * (pq[size_t(i)] & 0xFFFFu);
+        pqb[3 * 4096 + at] = 4 * (pq[size_t(i)] >> 16);
+    }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
     c->desc_off_tw = -1;
     c->uoff_tw = -1;
-    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024 || mask3_smem(c) > 200 * 1024)
+    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
 }
@@ -1445,26 +1708,36 @@ int bsm_last_launch_count(bsm_ctx* c, int* count) {
 }
 
 int bsm_measure_popc_peak(bsm_ctx* c, double* ops_per_s) {
-    if (!c || !ops_per_s) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    return bsm_measure_word_peaks(c, ops_per_s, nullptr);
+}
+
+int bsm_measure_word_peaks(bsm_ctx* c, double* popc_words_per_s, double* csa_words_per_s) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
     BSM_CUDA(cudaSetDevice(c->device));
     const int blocks = c->sm_count * 4, threads = 512, iters = 8192;
     BSM_TRY(c->popc_out.ensure(size_t(blocks) * threads * 4));
     cudaEvent_t e0, e1;
     BSM_CUDA(cudaEventCreate(&e0));
     BSM_CUDA(cudaEventCreate(&e1));
-    float best = 1e30f;
-    for (int r = 0; r < 4; ++r) {
-        cudaEventRecord(e0, c->stream);
-        k_popc_peak<<<blocks, threads, 0, c->stream>>>(c->popc_out.as<uint32_t>(), 7u + r, iters);
-        cudaEventRecord(e1, c->stream);
-        BSM_CUDA(cudaEventSynchronize(e1));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        if (r > 0) best = std::min(best, ms);
+    for (int kind = 0; kind < 2; ++kind) {
+        double* dst = kind == 0 ? popc_words_per_s : csa_words_per_s;
+        if (!dst) continue;
+        float best = 1e30f;
+        for (int r = 0; r < 4; ++r) {
+            cudaEventRecord(e0, c->stream);
+            if (kind == 0) k_popc_peak<<<blocks, threads, 0, c->stream>>>(c->popc_out.as<uint32_t>(), 7u + r, iters);
+            else k_csa_peak<<<blocks, threads, 0, c->stream>>>(c->popc_out.as<uint32_t>(), 7u + r, iters, 2u);
+            cudaEventRecord(e1, c->stream);
+            BSM_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r > 0) best = std::min(best, ms);
+        }
+        const double words = double(blocks) * threads * iters * 8 * (kind == 0 ? 1 : 2);
+        *dst = words / (double(best) * 1e-3);
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    *ops_per_s = double(blocks) * threads * iters * 8 / (double(best) * 1e-3);
     return BSM_OK;
 }
 
