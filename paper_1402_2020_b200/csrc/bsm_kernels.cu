@@ -121,6 +121,108 @@ __global__ void __launch_bounds__(kDescTX* kDescTY)
 }
 
 // ---------------------------------------------------------------------------
+// K1' -- descriptor, four pixels per thread.  Same contract as k_descriptor.
+// A thread owns pixels x..x+3 (x % 4 == 0) of two rows; per pair it reads the
+// 4 p-samples and the 4 q-samples as two aligned words each plus one PRMT
+// (the byte alignment is the same for every thread, so the selector is
+// warp-uniform), compares the 4 unsigned bytes with a borrow-free SWAR test,
+// and deposits the 4 result bits into byte lanes; every 32 pairs a 4x4 byte
+// transpose turns them into the 4 pixels' words, stored as one 16-B store.
+constexpr int kD2TX = 32, kD2TY = 8, kD2Rows = 2;  // CTA: 128 px x 16 rows
+
+__device__ __forceinline__ uint32_t bytes_gt(uint32_t p, uint32_t q) {
+    // bit 7 of each byte: p_b > q_b (unsigned).  d = (q|0x80) - (p&0x7F) has no
+    // inter-byte borrow; bit 7 of d is [q_lo >= p_lo]; then q >= p <=>
+    // (q7 & ~p7) | (~(q7 ^ p7) & d7), and p > q is its complement.
+    const uint32_t d = (q | 0x80808080u) - (p & 0x7F7F7F7Fu);
+    const uint32_t ge = (q & ~p) | (~(q ^ p) & d);
+    return ~ge & 0x80808080u;
+}
+
+__global__ void __launch_bounds__(kD2TX* kD2TY)
+    k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
+                  const uint4* __restrict__ ptab, int n, int half, int TWs, int NW, int Wp,
+                  uint32_t* __restrict__ desc) {
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint8_t* tile = reinterpret_cast<uint8_t*>(dsm);
+    const int TH = kD2TY * kD2Rows + 2 * half;
+    const int tid = threadIdx.y * kD2TX + threadIdx.x;
+    const int gx0 = blockIdx.x * (kD2TX * 4) - half;
+    const int ly0 = blockIdx.y * kD2TY * kD2Rows;
+    const int gy0 = ybeg + ly0 - half;
+    for (int idx = tid; idx < TWs * TH; idx += kD2TX * kD2TY) {
+        const int r = idx / TWs, c = idx - r * TWs;
+        const int gx = min(max(gx0 + c, 0), W - 1);
+        const int gy = min(max(gy0 + r, 0), H - 1);
+        tile[idx] = __ldg(img + size_t(gy) * W + gx);
+    }
+    __syncthreads();
+    const int xq = blockIdx.x * (kD2TX * 4) + 4 * threadIdx.x;
+    // byte address of the thread's first pixel (row 0) inside the tile; the
+    // per-pair table holds word offsets relative to (base & ~3) for this
+    // block's alignment class
+    const int base = (threadIdx.y * kD2Rows + half) * TWs + 4 * threadIdx.x + half;
+    const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile) + (base >> 2);
+    const int rowW = TWs >> 2;
+    const int full = n >> 5;
+    for (int w = 0; w < NW; ++w) {
+        uint32_t acc[kD2Rows][4];
+#pragma unroll
+        for (int r = 0; r < kD2Rows; ++r)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[r][b] = 0;
+        const int cnt = w < full ? 32 : (w == full ? (n & 31) : 0);
+        if (cnt == 32) {
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) {
+                const uint4 e = __ldg(ptab + 32 * w + k);  // {p word off, q word off, p sel, q sel}
+#pragma unroll
+                for (int r = 0; r < kD2Rows; ++r) {
+                    const uint32_t* t = tw + r * rowW;
+                    const uint32_t p = __byte_perm(t[int(e.x)], t[int(e.x) + 1], e.z);
+                    const uint32_t q = __byte_perm(t[int(e.y)], t[int(e.y) + 1], e.w);
+                    const uint32_t f = bytes_gt(p, q);  // bit 7 of byte j: pixel j
+                    // pair k -> bit (k & 7) of byte lane j of acc[k >> 3]
+                    const int sh = 7 - (k & 7);
+                    acc[r][k >> 3] |= (f >> sh);
+                }
+            }
+        } else {
+            for (int k = 0; k < cnt; ++k) {
+                const uint4 e = __ldg(ptab + 32 * w + k);
+#pragma unroll
+                for (int r = 0; r < kD2Rows; ++r) {
+                    const uint32_t* t = tw + r * rowW;
+                    const uint32_t p = __byte_perm(t[int(e.x)], t[int(e.x) + 1], e.z);
+                    const uint32_t q = __byte_perm(t[int(e.y)], t[int(e.y) + 1], e.w);
+                    const uint32_t f = bytes_gt(p, q);
+                    const uint32_t v = f >> (7 - (k & 7));
+                    switch (k >> 3) {
+                        case 0: acc[r][0] |= v; break;
+                        case 1: acc[r][1] |= v; break;
+                        case 2: acc[r][2] |= v; break;
+                        default: acc[r][3] |= v; break;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kD2Rows; ++r) {
+            // acc[b] byte j = bits 8b..8b+7 of pixel j  ->  4x4 byte transpose
+            const uint32_t t0 = __byte_perm(acc[r][0], acc[r][1], 0x5140), t1 = __byte_perm(acc[r][0], acc[r][1], 0x7362);
+            const uint32_t t2 = __byte_perm(acc[r][2], acc[r][3], 0x5140), t3 = __byte_perm(acc[r][2], acc[r][3], 0x7362);
+            uint4 o;
+            o.x = __byte_perm(t0, t2, 0x5410);
+            o.y = __byte_perm(t0, t2, 0x7632);
+            o.z = __byte_perm(t1, t3, 0x5410);
+            o.w = __byte_perm(t1, t3, 0x7632);
+            const int ly = ly0 + threadIdx.y * kD2Rows + r;
+            if (ly < rows) *reinterpret_cast<uint4*>(desc + (size_t(ly) * NW + w) * Wp + xq) = o;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K2 -- mask.  descriptor.hpp:118-154 (mask_at_pixel), quarter_threshold
 // :64-76.  Warp per pixel.
 //   1. rho[k] = dense rank of lab_sad(centre, window pixel k) for the u window
@@ -984,8 +1086,8 @@ struct bsm_ctx {
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
-    DevBuf d_desc_off, d_pq, d_pqb, d_uoff;
-    int desc_off_tw = -1, uoff_tw = -1;
+    DevBuf d_desc_off, d_desc4, d_pq, d_pqb, d_uoff;
+    int desc_off_tw = -1, desc4_tw = -1, uoff_tw = -1;
     // tables
     float gray_lut[256], lab_lut[768];
     DevBuf d_rank;
@@ -1037,6 +1139,28 @@ int check_launch(bsm_ctx* c, const char* what) {
     } while (0)
 
 // Tile-relative offset tables depend on the staged tile width.
+int desc4_tile_width(int half) { return round_up(kD2TX * 4 + 2 * half + 8, 16); }
+
+// k_descriptor4's per-pair table: word offsets (relative to the thread's
+// aligned base word) and PRMT selectors of both endpoints.
+int ensure_desc4_table(bsm_ctx* c) {
+    const int TWs = desc4_tile_width(c->half);
+    if (c->desc4_tw == TWs) return BSM_OK;
+    const int G = (c->n + 31) / 32;
+    std::vector<uint4> t(size_t(G) * 32, make_uint4(0, 0, 0, 0));
+    const int a0 = c->half & 3;  // every thread's base byte is congruent to half (mod 4)
+    for (int i = 0; i < c->n; ++i) {
+        const int16_t* p = &c->pairs[4 * size_t(i)];
+        const int op = a0 + p[1] * TWs + p[0], oq = a0 + p[3] * TWs + p[2];
+        auto sel = [](int r) { return uint32_t(r | ((r + 1) << 4) | ((r + 2) << 8) | ((r + 3) << 12)); };
+        t[size_t(i)] = make_uint4(uint32_t(op >> 2), uint32_t(oq >> 2), sel(op & 3), sel(oq & 3));
+    }
+    BSM_TRY(c->d_desc4.ensure(t.size() * sizeof(uint4)));
+    BSM_CUDA(cudaMemcpy(c->d_desc4.p, t.data(), t.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+    c->desc4_tw = TWs;
+    return BSM_OK;
+}
+
 int ensure_desc_offsets(bsm_ctx* c) {
     const int TW = kDescTX + 2 * c->half;
     if (c->desc_off_tw == TW) return BSM_OK;
@@ -1118,11 +1242,13 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
     BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? kM3Px : kMaskTile));
     {
         Scope s(c, T_DESC);
-        const size_t sm = desc_smem(c);
-        dim3 grid(Wp / kDescTX, (rows + kDescTY * kDescPY - 1) / (kDescTY * kDescPY));
-        BSM_CUDA(cudaFuncSetAttribute(k_descriptor, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        k_descriptor<<<grid, dim3(kDescTX, kDescTY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc_off.as<int2>(),
-                                                                       c->n, c->half, c->NW, Wp, desc);
+        BSM_TRY(ensure_desc4_table(c));
+        const int TWs = desc4_tile_width(c->half);
+        const size_t sm = size_t(TWs) * (kD2TY * kD2Rows + 2 * c->half);
+        dim3 grid(Wp / (kD2TX * 4), (rows + kD2TY * kD2Rows - 1) / (kD2TY * kD2Rows));
+        BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<uint4>(),
+                                                                    c->n, c->half, TWs, c->NW, Wp, desc);
         BSM_TRY(check_launch(c, "descriptor"));
     }
     {
@@ -1365,7 +1491,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_desc_off, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_desc_off, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
@@ -1460,6 +1586,7 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
     c->desc_off_tw = -1;
+    c->desc4_tw = -1;
     c->uoff_tw = -1;
     if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
