@@ -966,6 +966,78 @@ __global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __res
 }
 
 // ---------------------------------------------------------------------------
+// K6' -- voting refinement, thread per invalid pixel (refine.hpp:62-111).
+// Each thread walks its clipped (2r+1)^2 window in row-major order and adds
+// every valid voter's exact weight to its own column of double bins in
+// shared memory ([bin][thread]: a lane always hits its own bank pair, so any
+// mix of bins is conflict-free).  Per bin the additions happen in the
+// reference's voter order, so the sums are bit-identical.  Voter data comes
+// pre-packed (k_make_vmap: bin | gray << 16 | valid << 24); the window offset
+// (dy, dx) is warp-uniform, so the distance column of the weight table is a
+// broadcast.  Used when the bins fit (nbins * 8 B * 32 threads); otherwise
+// the warp-per-pixel k_vote_refine runs.
+__global__ void k_make_vmap(const float* __restrict__ cd, const uint8_t* __restrict__ cv,
+                            const uint8_t* __restrict__ gray, size_t n, uint32_t* __restrict__ vmap) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t g = uint32_t(gray[i]) << 16;
+    vmap[i] = cv[i] ? (g | (1u << 24) | uint32_t(llround(double(cd[i])))) : g;
+}
+
+__global__ void k_vote_refine_tpp(const uint32_t* __restrict__ vmap, int W, int rows, int radius,
+                                  const double* __restrict__ wtab, int ncol, const int16_t* __restrict__ s2col,
+                                  const int* __restrict__ counters, const int* __restrict__ inv,
+                                  float* __restrict__ od, uint8_t* __restrict__ ov) {
+    extern __shared__ __align__(16) double bins[];  // [nbins][blockDim.x]
+    const int NT = blockDim.x, t = threadIdx.x;
+    const int max_bin = counters[0];
+    const int n_inv = counters[1];
+    for (int idx = blockIdx.x * NT + t; idx < n_inv; idx += gridDim.x * NT) {
+        const int p = inv[idx];
+        const int y = p / W, x = p - y * W;
+        const int u = int((vmap[p] >> 16) & 0xFFu);
+        for (int b = 0; b <= max_bin; ++b) bins[b * NT + t] = 0.0;
+        const int tu = u * (u + 1) / 2;
+        bool any = false;
+        for (int dy = -radius; dy <= radius; ++dy) {
+            const int py = y + dy;
+            if (py < 0 || py >= rows) continue;
+            const uint32_t* row = vmap + size_t(py) * W;
+            const int dy2 = dy * dy;
+            const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
+#pragma unroll 4
+            for (int dx = dx0; dx <= dx1; ++dx) {
+                const uint32_t e = __ldg(row + x + dx);
+                if (e & (1u << 24)) {
+                    const int v = int((e >> 16) & 0xFFu);
+                    const int tri = v >= u ? (v * (v + 1) / 2 + u) : (tu + v);
+                    const double w = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
+                    double* bp = bins + int(e & 0xFFFFu) * NT + t;
+                    *bp += w;
+                    any = true;
+                }
+            }
+        }
+        if (!any) {
+            od[p] = 0.0f;
+            ov[p] = 0;
+            continue;
+        }
+        int best = 0;
+        double bv = bins[t];
+        for (int b = 1; b <= max_bin; ++b) {
+            const double v = bins[b * NT + t];
+            if (v > bv) {
+                bv = v;
+                best = b;
+            }
+        }
+        od[p] = float(best);
+        ov[p] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Layout converters for the per-stage API (reference AoS u64 <-> device SoA).
 __global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
                              uint32_t* __restrict__ dst) {
@@ -1096,7 +1168,7 @@ struct bsm_ctx {
     int wt_radius = -1, wt_ncol = 0;
     // scratch
     DevBuf img_l, img_r, fdl, fml, fdr, fmr, keys_l, keys_r, keys_u;
-    DevBuf chk_d, chk_v, ref_d, ref_v, lw_d, rw_d, un_d, counters, inv;
+    DevBuf chk_d, chk_v, ref_d, ref_v, lw_d, rw_d, un_d, counters, inv, vmap;
     DevBuf aux0, aux1, aux2, aux3;
     int last_W = 0, last_rows = 0, last_unmasked = 0, last_r0 = 0, last_out0 = 0, last_out_rows = 0;
     // instrumentation
@@ -1292,6 +1364,40 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     return check_launch(c, "cost_wta");
 }
 
+// Refinement of the invalid pixels listed in c->inv (count in counters[1],
+// max_bin in counters[0]) into c->ref_d / c->ref_v (pre-filled with the input
+// map).  nbins_max bounds max_bin + 1.
+int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t* gray, int W, int rows, int radius,
+                  int nbins_max) {
+    const size_t px = size_t(rows) * W;
+    const int nbins = round_up(std::max(nbins_max, 1), 32);
+    // The thread-per-pixel variant is latency-bound on the weight-table
+    // gathers unless ~8+ warps fit per SM, i.e. for short disparity ranges.
+    int nt = int((200 * 1024) / (size_t(nbins) * 8)) / 32 * 32;
+    if (nt >= 256) {
+        nt = 256;
+        BSM_TRY(c->vmap.ensure(px * 4));
+        const int tb = 256;
+        k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
+        BSM_TRY(check_launch(c, "make_vmap"));
+        const size_t sm = size_t(nbins) * nt * 8;
+        BSM_CUDA(cudaFuncSetAttribute(k_vote_refine_tpp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_vote_refine_tpp<<<c->sm_count, nt, sm, c->stream>>>(c->vmap.as<uint32_t>(), W, rows, radius,
+                                                              c->d_wtab.as<double>(), c->wt_ncol,
+                                                              c->d_s2col.as<int16_t>(), c->counters.as<int>(),
+                                                              c->inv.as<int>(), c->ref_d.as<float>(),
+                                                              c->ref_v.as<uint8_t>());
+        return check_launch(c, "vote_refine_tpp");
+    }
+    const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
+    const size_t sm = size_t(warps) * nbins * 8;
+    BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
+        cd, cv, gray, W, rows, radius, c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(),
+        c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+    return check_launch(c, "vote_refine");
+}
+
 int validate_params(const bsm_params* p) {
     if (!p) return set_err(BSM_INVALID_ARGUMENT, "bsm: null params");
     if (p->d_max < 1) return set_err(BSM_INVALID_ARGUMENT, "config: d_max must be set (>= 1)");
@@ -1363,15 +1469,8 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
         Scope s(c, T_REFINE);
         BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
         BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
-        const int nbins = round_up(p->d_max, 32);
-        const int warps = 8;
-        const size_t sm = size_t(warps) * nbins * 8;
-        BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
-            c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, W, rows, p->vote_radius,
-            c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(),
-            nbins, c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
-        BSM_TRY(check_launch(c, "vote_refine"));
+        BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, W, rows,
+                              p->vote_radius, p->d_max));
     }
     c->last_W = W;
     c->last_rows = rows;
@@ -1494,7 +1593,7 @@ int bsm_ctx_destroy(bsm_ctx* c) {
     DevBuf* bufs[] = {&c->d_desc_off, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
-                      &c->counters, &c->inv, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
+                      &c->counters, &c->inv, &c->vmap, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
     for (DevBuf* b : bufs) b->release();
     for (int t = 0; t < T_COUNT; ++t)
         for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
@@ -1737,15 +1836,8 @@ int bsm_vote_refine_u8(bsm_ctx* c, const float* d, const uint8_t* v, const uint8
     if (!invalid.empty())
         BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_TRY(sync(c));  // host staging buffers (cnt, invalid) go out of scope
-    const int nbins = round_up(max_bin + 1, 32);
-    const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
-    const size_t sm = size_t(warps) * nbins * 8;
-    BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-    k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
-        c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), W, H, vote_radius,
-        c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins,
-        c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
-    BSM_TRY(check_launch(c, "vote_refine"));
+    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), W, H,
+                          vote_radius, max_bin + 1));
     if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
     if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->ref_v.p, px, cudaMemcpyDeviceToHost, c->stream));
     return sync(c);
