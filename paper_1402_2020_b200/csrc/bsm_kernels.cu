@@ -42,7 +42,7 @@ int set_err(int code, const std::string& msg) {
 constexpr int kMaxPairs = 8192;      // mask kernel keeps 2*ceil(n/128) regs/lane of ranks
 constexpr int kCostTile = 128;       // pixels per cost CTA
 constexpr int kCostDisp = 64;        // disparities per cost CTA
-constexpr int kCostK = 8;            // u32 words per pipeline stage
+constexpr int kCostK = 16;           // u32 words per pipeline stage
 constexpr int kCostStages = 3;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -695,33 +695,54 @@ __global__ void __launch_bounds__(256, 2)
     // `two` == 2 at run time: a register multiplier keeps the carry-save
     // accumulate an IMAD (FMA pipe) instead of an IADD3 (ALU pipe).
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
-    __shared__ __align__(16) uint32_t sa[ST][K][T];
-    __shared__ __align__(16) uint32_t sm[MASKED ? ST : 1][K][MASKED ? T : 4];
-    __shared__ __align__(16) uint32_t sb[ST][K][BW];
-    __shared__ uint32_t red[8][T];
+    constexpr int SA = K * T, SB = K * BW;                 // words per stage
+    constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
+    extern __shared__ __align__(16) uint32_t csm[];       // ST x {a, m, b} + red
+    uint32_t* red = csm + ST * STAGE;                      // [8][T]
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const int x0 = blockIdx.x * T;
     const int y = blockIdx.y;
     const int d0 = blockIdx.z * DC;
     const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
-    const size_t rowbase = size_t(y) * NW;
     const int nchunks = (NW + K - 1) / K;
+
+    // Per-thread copy assignments, fixed for all stages: a/m rows (tid>>5) and
+    // (tid>>5)+8, column 4*(tid&31); three 16-B chunks of the other-view span.
+    constexpr int NB = (SB / 4 + 255) / 256;
+    const int aw = tid >> 5, acol = (tid & 31) * 4;
+    const uint32_t* ga = dref + (size_t(y) * NW + aw) * Wp + x0 + acol;
+    const uint32_t* gm = MASKED ? mref + (size_t(y) * NW + aw) * Wp + x0 + acol : nullptr;
+    int bw[NB], bcol[NB];
+    bool bok[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const int t = tid + 256 * i;
+        bw[i] = t / (BW / 4);
+        bcol[i] = (t - bw[i] * (BW / 4)) * 4;
+        const int gcol = bbase + bcol[i];
+        bok[i] = t < SB / 4 && gcol >= 0 && gcol < Wp;
+    }
+    const uint32_t* gb = doth + size_t(y) * NW * Wp + bbase;
 
     auto load_stage = [&](int c, int st) {
         const int w0 = c * K;
-        {
-            const int w = tid >> 5, col = (tid & 31) * 4;
+        uint32_t* s = csm + st * STAGE;
+#pragma unroll
+        for (int h = 0; h < K / 8; ++h) {
+            const int w = aw + 8 * h;
             const bool ok = w0 + w < NW;
-            const size_t off = (rowbase + w0 + w) * Wp + x0 + col;
-            cp_async16(&sa[st][w][col], ok ? dref + off : dref, ok);
-            if constexpr (MASKED) cp_async16(&sm[st][w][col], ok ? mref + off : mref, ok);
+            const size_t off = size_t(w0 + 8 * h) * Wp;
+            cp_async16(s + w * T + acol, ok ? ga + off : dref, ok);
+            if constexpr (MASKED) cp_async16(s + SA + w * T + acol, ok ? gm + off : mref, ok);
         }
-        for (int t = tid; t < K * (BW / 4); t += 256) {
-            const int w = t / (BW / 4), col = (t - w * (BW / 4)) * 4;
-            const int gcol = bbase + col;
-            const bool ok = (w0 + w < NW) && gcol >= 0 && gcol < Wp;
-            cp_async16(&sb[st][w][col], ok ? doth + (rowbase + w0 + w) * Wp + gcol : doth, ok);
+        uint32_t* sb = s + (MASKED ? 2 * SA : SA);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (tid + 256 * i < SB / 4) {
+                const bool ok = bok[i] && w0 + bw[i] < NW;
+                cp_async16(sb + bw[i] * BW + bcol[i], ok ? gb + size_t(w0 + bw[i]) * Wp + bcol[i] : doth, ok);
+            }
         }
     };
 
@@ -750,22 +771,24 @@ __global__ void __launch_bounds__(256, 2)
         __syncthreads();
         if (c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
         cp_async_commit();
-        const int st = c % ST;
+        const uint32_t* sa = csm + (c % ST) * STAGE;
+        const uint32_t* sm = sa + SA;
+        const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
         // Two words per step through a carry-save accumulator (Harley-Seal
         // with one level): ones' = ones ^ x0 ^ x1, twos = maj(ones, x0, x1),
         // acc += 2 * popc(twos).  One POPC per two words instead of two; the
         // LOP3s and the IMAD accumulate run on the ALU and FMA pipes beside it.
-#pragma unroll 1
+#pragma unroll 2
         for (int w = 0; w < K; w += 2) {
             uint32_t a[2][4], m[2][4], b[2][12];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const uint4 a4 = *reinterpret_cast<const uint4*>(&sa[st][w + h][xs]);
+                const uint4 a4 = *reinterpret_cast<const uint4*>(sa + (w + h) * T + xs);
                 uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(&sm[st][w + h][xs]);
-                const uint4 b0 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0]);
-                const uint4 b1 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0 + 4]);
-                const uint4 b2 = *reinterpret_cast<const uint4*>(&sb[st][w + h][c0 + 8]);
+                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(sm + (w + h) * T + xs);
+                const uint4 b0 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 4);
+                const uint4 b2 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 8);
                 a[h][0] = a4.x; a[h][1] = a4.y; a[h][2] = a4.z; a[h][3] = a4.w;
                 m[h][0] = m4.x; m[h][1] = m4.y; m[h][2] = m4.z; m[h][3] = m4.w;
                 b[h][0] = b0.x; b[h][1] = b0.y; b[h][2] = b0.z; b[h][3] = b0.w;
@@ -808,13 +831,13 @@ __global__ void __launch_bounds__(256, 2)
             const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
             if (ok && key < best) best = key;
         }
-        red[wi][xs + j] = best;
+        red[wi * T + xs + j] = best;
     }
     __syncthreads();
     if (tid < T) {
-        uint32_t best = red[0][tid];
+        uint32_t best = red[tid];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) best = min(best, red[w][tid]);
+        for (int w = 1; w < 8; ++w) best = min(best, red[w * T + tid]);
         const int x = x0 + tid;
         if (x < W && best != 0xFFFFFFFFu) {
             if (gridDim.z == 1) keys[size_t(y) * W + x] = best;
@@ -1354,13 +1377,15 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     const int dz = (d_max + kCostDisp - 1) / kCostDisp;
     if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
     dim3 grid(Wp / kCostTile, rows, dz);
-    if (right) {
-        if (masked) k_cost_wta<true, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
-        else k_cost_wta<true, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
-    } else {
-        if (masked) k_cost_wta<false, true><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
-        else k_cost_wta<false, false><<<grid, 256, 0, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
-    }
+    const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
+    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4;
+    auto launch = [&](auto kern) -> int {
+        BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        kern<<<grid, 256, sm, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
+        return BSM_OK;
+    };
+    if (right) BSM_TRY(masked ? launch(k_cost_wta<true, true>) : launch(k_cost_wta<true, false>));
+    else BSM_TRY(masked ? launch(k_cost_wta<false, true>) : launch(k_cost_wta<false, false>));
     return check_launch(c, "cost_wta");
 }
 
