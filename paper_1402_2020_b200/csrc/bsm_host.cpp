@@ -163,3 +163,110 @@ void vote_weight_table(const float* lab, double lc, double le, int radius, std::
 }
 
 }  // namespace bsmh
+
+namespace bsmh {
+
+namespace {
+// Wavefronts of one 32-lane gather of the given slots: the largest number of
+// distinct slots requested from one bank (a slot requested twice is one word).
+int gather_cost(const int* s) {
+    int cnt[32] = {0};
+    uint32_t seen_lo[32] = {0};  // per bank: slots (>> 5) already counted, small tables only
+    int mx = 0;
+    for (int l = 0; l < 32; ++l) {
+        const int b = s[l] & 31, row = s[l] >> 5;
+        bool dup;
+        if (row < 32) {
+            dup = (seen_lo[b] >> row) & 1u;
+            seen_lo[b] |= 1u << row;
+        } else {
+            dup = false;
+            for (int k = 0; k < l; ++k)
+                if (s[k] == s[l]) dup = true;
+        }
+        if (!dup) mx = std::max(mx, ++cnt[b]);
+    }
+    return mx;
+}
+}  // namespace
+
+void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<int>& slot, double* cost_before,
+                      double* cost_after) {
+    // gathers: 2 endpoints x 128 steps, 32 lanes each (pairs >= n: sentinel, excluded)
+    const int nsteps = 128;
+    std::vector<int> gpair(size_t(2) * nsteps * 32, -1);  // offset index per (gather, lane), -1 = sentinel
+    for (int e = 0; e < 2; ++e)
+        for (int st = 0; st < nsteps; ++st)
+            for (int l = 0; l < 32; ++l) {
+                const int i = 128 * l + st;  // st = 32m + t
+                if (i < n) gpair[(size_t(e) * nsteps + st) * 32 + l] = int(e ? (pq[i] >> 16) : (pq[i] & 0xFFFFu));
+            }
+    const int ng = 2 * nsteps;
+    // offset -> gathers it appears in
+    std::vector<std::vector<int>> uses(static_cast<size_t>(u));
+    for (int g = 0; g < ng; ++g)
+        for (int l = 0; l < 32; ++l) {
+            const int o = gpair[size_t(g) * 32 + l];
+            if (o >= 0 && (uses[size_t(o)].empty() || uses[size_t(o)].back() != g)) uses[size_t(o)].push_back(g);
+        }
+    // slot_owner[s] = offset in slot s or -1; the sentinel is handled by the kernel at slot u
+    slot.resize(size_t(u));
+    std::vector<int> owner(size_t(nslots), -1);
+    for (int o = 0; o < u; ++o) {
+        slot[size_t(o)] = o;
+        owner[size_t(o)] = o;
+    }
+    const int sentinel_slot = nslots;  // distinct bank pattern irrelevant (pads are rare)
+    auto eval = [&](int g) {
+        int s[32];
+        for (int l = 0; l < 32; ++l) {
+            const int o = gpair[size_t(g) * 32 + l];
+            s[l] = o >= 0 ? slot[size_t(o)] : sentinel_slot;
+        }
+        return gather_cost(s);
+    };
+    std::vector<int> gcost(static_cast<size_t>(ng));
+    long total = 0;
+    for (int g = 0; g < ng; ++g) total += (gcost[size_t(g)] = eval(g));
+    if (cost_before) *cost_before = double(total) / ng;
+    std::mt19937_64 rng(12345);
+    std::vector<int> touched;
+    std::vector<char> mark(static_cast<size_t>(ng), 0);
+    const int iters = 40000;
+    for (int it = 0; it < iters; ++it) {
+        const int o1 = int(rng() % uint64_t(u));
+        const int s2 = int(rng() % uint64_t(nslots));
+        const int o2 = owner[size_t(s2)];
+        if (o2 == o1) continue;
+        const int s1 = slot[size_t(o1)];
+        touched.clear();
+        for (int g : uses[size_t(o1)])
+            if (!mark[size_t(g)]) mark[size_t(g)] = 1, touched.push_back(g);
+        if (o2 >= 0)
+            for (int g : uses[size_t(o2)])
+                if (!mark[size_t(g)]) mark[size_t(g)] = 1, touched.push_back(g);
+        long before = 0;
+        for (int g : touched) before += gcost[size_t(g)];
+        // apply
+        slot[size_t(o1)] = s2;
+        owner[size_t(s2)] = o1;
+        owner[size_t(s1)] = o2;
+        if (o2 >= 0) slot[size_t(o2)] = s1;
+        long after = 0;
+        std::vector<int> nc(touched.size());
+        for (size_t k = 0; k < touched.size(); ++k) after += (nc[k] = eval(touched[k]));
+        if (after <= before) {
+            for (size_t k = 0; k < touched.size(); ++k) gcost[size_t(touched[k])] = nc[k];
+            total += after - before;
+        } else {  // revert
+            slot[size_t(o1)] = s1;
+            owner[size_t(s1)] = o1;
+            owner[size_t(s2)] = o2;
+            if (o2 >= 0) slot[size_t(o2)] = s2;
+        }
+        for (int g : touched) mark[size_t(g)] = 0;
+    }
+    if (cost_after) *cost_after = double(total) / ng;
+}
+
+}  // namespace bsmh

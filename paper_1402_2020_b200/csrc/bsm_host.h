@@ -34,3 +34,18 @@ void vote_weight_table(const float* lab768, double lc, double le, int radius, st
                        std::vector<int16_t>& s2col, int& ncol);
 
 }  // namespace bsmh
+
+namespace bsmh {
+
+// Shared-memory bank placement for the mask kernel's per-warp rank table.
+// Pair i's endpoints are used-offset indices P[i], Q[i] (< u).  In k_mask4 lane
+// l reads pair 128l + 32m + t at step (m, t); a 32-lane gather costs as many
+// shared-memory wavefronts as the largest number of distinct 4-byte slots
+// requested from one bank.  Returns slot[o] for every used offset o (slots are
+// a permutation of [0, nslots) restricted to u entries, nslots >= u) chosen by
+// a deterministic local search that minimises the total wavefront count.
+// `cost_before` / `cost_after` receive the average wavefronts per gather.
+void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<int>& slot, double* cost_before,
+                      double* cost_after);
+
+}  // namespace bsmh

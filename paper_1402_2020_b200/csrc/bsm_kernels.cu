@@ -1178,6 +1178,9 @@ struct bsm_ctx {
     int sm_count = 0;
     // pattern
     int n = 0, window = 0, half = 0, NW = 0, u = 0, upad = 0;
+    int mslots = 0;                 // rank-table slots used by the mask kernels
+    std::vector<int> slot_used;     // slot -> used-offset index (-1: empty)
+    double slot_cost[2] = {0, 0};   // avg wavefronts per gather before/after placement
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
@@ -1274,10 +1277,12 @@ int ensure_mask_offsets(bsm_ctx* c, int tile_px) {
     const int TW = tile_px + 2 * c->half;
     if (c->uoff_tw == TW) return BSM_OK;
     const int side = 2 * c->half + 1;
-    std::vector<int32_t> o(c->used.size());
-    for (size_t k = 0; k < c->used.size(); ++k) {
-        const int dy = c->used[k] / side - c->half, dx = c->used[k] % side - c->half;
-        o[k] = dy * TW + dx;
+    std::vector<int32_t> o(size_t(c->mslots), 0);  // empty slots read the centre (harmless)
+    for (int k = 0; k < c->mslots; ++k) {
+        const int ui = c->slot_used[size_t(k)];
+        if (ui < 0) continue;
+        const int dy = c->used[size_t(ui)] / side - c->half, dx = c->used[size_t(ui)] % side - c->half;
+        o[size_t(k)] = dy * TW + dx;
     }
     BSM_TRY(c->d_uoff.ensure(std::max<size_t>(4, o.size() * 4)));
     BSM_CUDA(cudaMemcpy(c->d_uoff.p, o.data(), o.size() * 4, cudaMemcpyHostToDevice));
@@ -1321,7 +1326,7 @@ size_t mask_smem(const bsm_ctx* c) {
 
 size_t mask4_smem(const bsm_ctx* c) {
     const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
-    return size_t(round_up(c->u + 1, 4)) * 4 + 2 * 8 * 4 * 32 * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
+    return size_t(round_up(c->mslots + 1, 4)) * 4 + 2 * 8 * 4 * 32 * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
            size_t(TW) * TH;
 }
 
@@ -1356,7 +1361,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
             dim3 grid3(Wp / kM3Px, rows);
             k_mask4<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
                                                    c->d_pqb.as<uint4>() + 3 * 1024, c->n,
-                                                   c->d_uoff.as<int32_t>(), c->u, round_up(c->u + 1, 4), c->d_rank.as<uint8_t>(),
+                                                   c->d_uoff.as<int32_t>(), c->mslots, round_up(c->mslots + 1, 4),
+                                                   c->d_rank.as<uint8_t>(),
                                                    c->half, c->NW, Wp, mask);
         } else {
             BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
@@ -1688,6 +1694,18 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     c->upad = round_up(c->u, 16);
     BSM_TRY(c->d_pq.ensure(pq.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
+    // Rank-table slot placement (k_mask4): minimise shared-memory bank
+    // conflicts of the per-pair gathers; identity for the n > 4096 kernel.
+    std::vector<int> rslot(size_t(c->u));
+    if (n <= 4096) {
+        c->mslots = round_up(c->u, 32) + 32;
+        bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, rslot, &c->slot_cost[0], &c->slot_cost[1]);
+    } else {
+        c->mslots = c->u;
+        for (int o = 0; o < c->u; ++o) rslot[size_t(o)] = o;
+    }
+    c->slot_used.assign(size_t(c->mslots), -1);
+    for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
     // k_mask3: byte offsets into its u32 rank table, P and Q as two tables of
     // uint4 [jj][lane] = groups 4jj..4jj+3 of pair 32g + lane; pads -> the
     // sentinel slot u.
@@ -1700,12 +1718,12 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     }
     // k_mask4: lane-block order -- lane l, chunk m, t: pair 128l + 32m + t at
     // uint4 [(m*8 + t/4)*32 + l], component t%4.
-    pqb.resize(4 * 4096, uint32_t(4 * c->u));
+    pqb.resize(4 * 4096, uint32_t(4 * c->mslots));  // pads -> sentinel slot mslots
     for (int i = 0; i < std::min(n, 4096); ++i) {
         const int l = i >> 7, m = (i >> 5) & 3, t = i & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
-        pqb[2 * 4096 + at] = 4 * (pq[size_t(i)] & 0xFFFFu);
-        pqb[3 * 4096 + at] = 4 * (pq[size_t(i)] >> 16);
+        pqb[2 * 4096 + at] = uint32_t(4 * rslot[size_t(pq[size_t(i)] & 0xFFFFu)]);
+        pqb[3 * 4096 + at] = uint32_t(4 * rslot[size_t(pq[size_t(i)] >> 16)]);
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
