@@ -102,6 +102,11 @@ int bsm_lr_check(bsm_ctx* ctx, const float* left_d, const float* right_d, int W,
 int bsm_vote_refine_u8(bsm_ctx* ctx, const float* d, const uint8_t* v, const uint8_t* gray_img, int W, int H,
                        double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v);
 
+/* vote_refine (refine.hpp:62-111) with an arbitrary float Lab plane
+ * (W*H*3 floats, e.g. from bsm_to_gray_lab of a colour image). */
+int bsm_vote_refine_lab(bsm_ctx* ctx, const float* d, const uint8_t* v, const float* lab, int W, int H,
+                        double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v);
+
 /* run_pipeline (pipeline.hpp:25-56) of a grayscale pair (r=g=b), host buffers. */
 int bsm_pipeline_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H,
                     const bsm_params* params, int want_unmasked, bsm_maps* out);
@@ -134,6 +139,13 @@ int bsm_last_launch_count(bsm_ctx* ctx, int* count);
  * 4 LOP3 + POPC + IMAD).  Either pointer may be NULL. */
 int bsm_measure_popc_peak(bsm_ctx* ctx, double* ops_per_s);
 int bsm_measure_word_peaks(bsm_ctx* ctx, double* popc_words_per_s, double* csa_words_per_s);
+/* The device restatement of libm's exp used for refine weights, evaluated on
+ * n arguments (validation / tests). */
+int bsm_device_exp(bsm_ctx* ctx, const double* x, int n, double* out);
+/* Refinement kernel choice (all bit-identical): 0 = per-bin window scans with
+ * device exp (default), 1 = shared-memory bins with device exp, 2 = exact host
+ * weight table (grayscale only). */
+int bsm_set_refine_mode(bsm_ctx* ctx, int mode);
 
 #ifdef __cplusplus
 }

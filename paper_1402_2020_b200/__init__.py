@@ -189,6 +189,17 @@ class Context:
         check(lib().bsm_measure_popc_peak(self.handle, C.byref(v)))
         return float(v.value)
 
+    def set_refine_mode(self, mode: int) -> None:
+        """0: per-bin window scans (default), 1: shared-memory bins, 2: host weight table."""
+        check(lib().bsm_set_refine_mode(self.handle, int(mode)))
+
+    def device_exp(self, x) -> np.ndarray:
+        """The device restatement of libm's exp (refine weights) on `x`."""
+        xs = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(xs)
+        check(lib().bsm_device_exp(self.handle, _ptr(xs), int(xs.size), _ptr(out)))
+        return out
+
     def measure_word_peaks(self) -> tuple:
         """(direct POPC mix, carry-save mix) word-op rates of this GPU, words/s."""
         a, b = C.c_double(), C.c_double()
@@ -307,11 +318,24 @@ def lr_check(left: DisparityMap, right: DisparityMap, tol: float, ctx: Optional[
     return DisparityMap(od, ov)
 
 
-def vote_refine(m: DisparityMap, gray_img, lambda_c: float = 9.0, lambda_e: float = 16.0,
+def vote_refine(m: DisparityMap, image, lambda_c: float = 9.0, lambda_e: float = 16.0,
                 vote_radius: int = 20, threads: int = 1, ctx: Optional[Context] = None) -> DisparityMap:
-    """vote_refine (refine.hpp:62-111); the Lab image is that of the grayscale view."""
-    g = _u8(gray_img)
-    if g.shape != m.disparity.shape:
+    """vote_refine (refine.hpp:62-111).
+
+    `image` is the grayscale uint8 view (its Lab is the conversion of (v,v,v))
+    or an (H, W, 3) float32 Lab plane (e.g. from to_gray_lab of a colour view).
+    """
+    lab = None
+    a = np.asarray(image)
+    if a.ndim == 3:
+        lab = np.ascontiguousarray(a, dtype=np.float32)
+        if lab.shape[2] != 3:
+            raise InvalidArgument("bsm: Lab planes must be (H, W, 3)")
+        shape = lab.shape[:2]
+    else:
+        g = _u8(a)
+        shape = g.shape
+    if shape != m.disparity.shape:
         raise DimensionMismatch("vote_refine: map/image dimensions differ")
     if not lambda_c > 0: raise InvalidArgument("refine: lambda_c must be > 0")
     if not lambda_e > 0: raise InvalidArgument("refine: lambda_e must be > 0")
@@ -322,8 +346,12 @@ def vote_refine(m: DisparityMap, gray_img, lambda_c: float = 9.0, lambda_e: floa
     H, W = d.shape
     od = np.zeros((H, W), np.float32)
     ov = np.zeros((H, W), np.uint8)
-    check(lib().bsm_vote_refine_u8(ctx.handle, _ptr(d), _ptr(v), _ptr(g), W, H, float(lambda_c),
-                                   float(lambda_e), int(vote_radius), _ptr(od), _ptr(ov)))
+    if lab is not None:
+        check(lib().bsm_vote_refine_lab(ctx.handle, _ptr(d), _ptr(v), _ptr(lab), W, H, float(lambda_c),
+                                        float(lambda_e), int(vote_radius), _ptr(od), _ptr(ov)))
+    else:
+        check(lib().bsm_vote_refine_u8(ctx.handle, _ptr(d), _ptr(v), _ptr(g), W, H, float(lambda_c),
+                                       float(lambda_e), int(vote_radius), _ptr(od), _ptr(ov)))
     return DisparityMap(od, ov)
 
 

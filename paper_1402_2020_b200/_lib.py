@@ -88,6 +88,9 @@ _SIGS = {
     "bsm_wta": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P],
     "bsm_lr_check": [_P, _P, _P, _I, _I, _D, _P, _P],
     "bsm_vote_refine_u8": [_P, _P, _P, _P, _I, _I, _D, _D, _I, _P, _P],
+    "bsm_vote_refine_lab": [_P, _P, _P, _P, _I, _I, _D, _D, _I, _P, _P],
+    "bsm_device_exp": [_P, _P, _I, _P],
+    "bsm_set_refine_mode": [_P, _I],
     "bsm_pipeline_u8": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I, C.POINTER(bsm_maps)],
     "bsm_pipeline_u8_device": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I],
     "bsm_fetch_maps": [_P, C.POINTER(bsm_maps)],

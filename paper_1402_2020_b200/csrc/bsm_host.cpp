@@ -270,3 +270,107 @@ void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<
 }
 
 }  // namespace bsmh
+
+#include <dlfcn.h>
+
+#include <cstring>
+#include <fstream>
+
+namespace bsmh {
+
+double exp_restated(double x, const ExpParams& p) {
+    // e_exp.c with the contraction of the FMA build (see the device copy,
+    // exp_glibc in bsm_kernels.cu):
+    //   kd = fma(x, InvLn2N, Shift); ki = bits(kd); kd -= Shift;
+    //   r = fma(kd, NegLn2loN, fma(kd, NegLn2hiN, x));
+    //   tmp = fma(r2*r2, fma(r, C5, C4), fma(fma(r, C3, C2), r2, tail + r));
+    //   exp = fma(scale, tmp, scale), or specialcase() for 512 <= |x| < 1024.
+    uint64_t xb;
+    std::memcpy(&xb, &x, 8);
+    const uint32_t abstop = uint32_t(xb >> 52) & 0x7ffu;
+    bool special = false;
+    if (abstop - 0x3c9u >= 0x3fu) {
+        if (int(abstop) - 0x3c9 < 0) return 1.0 + x;
+        if (abstop >= 0x409u) return (xb >> 63) ? 0.0 : HUGE_VAL;
+        special = true;
+    }
+    double kd = std::fma(x, p.invln2N, p.shift);
+    uint64_t ki;
+    std::memcpy(&ki, &kd, 8);
+    kd -= p.shift;
+    const double r = std::fma(kd, p.negln2loN, std::fma(kd, p.negln2hiN, x));
+    const uint64_t idx = 2 * (ki & 127);
+    const uint64_t top = ki << 45;
+    double tail;
+    std::memcpy(&tail, &p.tab[idx], 8);
+    uint64_t sbits = p.tab[idx + 1] + top;
+    const double r2 = r * r;
+    const double tmp = std::fma(r2 * r2, std::fma(r, p.c5, p.c4), std::fma(std::fma(r, p.c3, p.c2), r2, tail + r));
+    double scale;
+    if (!special) {
+        std::memcpy(&scale, &sbits, 8);
+        return std::fma(scale, tmp, scale);
+    }
+    if (!(ki & 0x80000000ull)) {
+        sbits -= 1009ull << 52;
+        std::memcpy(&scale, &sbits, 8);
+        volatile double st = scale * tmp;
+        return 0x1p1009 * (scale + st);
+    }
+    sbits += 1022ull << 52;
+    std::memcpy(&scale, &sbits, 8);
+    volatile double st = scale * tmp;  // not contracted in the library either
+    double y = scale + st;
+    if (y < 1.0) {
+        volatile double hi = y + 1.0;
+        volatile double lo = (scale - y) + st;
+        volatile double l2 = ((1.0 - hi) + y) + lo;
+        y = (l2 + hi) - 1.0;
+        if (y == 0.0) y = 0.0;
+    }
+    return y * 0x1p-1022;
+}
+
+bool glibc_exp_params(ExpParams& p, std::string& why) {
+    if (!__builtin_cpu_supports("fma") || !__builtin_cpu_supports("avx2")) {
+        why = "host CPU lacks FMA/AVX2: libm uses its non-FMA exp";
+        return false;
+    }
+    Dl_info info;
+    double (*fexp)(double) = &::exp;
+    if (!dladdr(reinterpret_cast<void*>(fexp), &info) || !info.dli_fname) {
+        why = "cannot locate libm";
+        return false;
+    }
+    std::ifstream f(info.dli_fname, std::ios::binary);
+    std::string bytes((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    // __exp_data starts with InvLn2N = 0x1.71547652b82fep7, Shift = 0x1.8p52.
+    const uint64_t sig[2] = {0x40671547652b82feull, 0x4338000000000000ull};
+    size_t at = std::string::npos;
+    for (size_t i = 0; i + 0xb0 + 2048 <= bytes.size(); i += 8)
+        if (std::memcmp(bytes.data() + i, sig, 16) == 0) {
+            at = i;
+            break;
+        }
+    if (at == std::string::npos) {
+        why = "exp table not found in " + std::string(info.dli_fname);
+        return false;
+    }
+    std::memcpy(&p.invln2N, bytes.data() + at, 8 * 8);
+    std::memcpy(p.tab, bytes.data() + at + 0xb0, sizeof p.tab);
+    // Validate against the libm this process calls.
+    std::mt19937_64 rng(7);
+    for (int i = 0; i < 400000; ++i) {
+        // mostly the refine range, plus the underflow/special ranges
+        const double span = (i & 7) == 0 ? 1100.0 : 40.0;
+        const double x = -span * double(rng() >> 11) * 0x1.0p-53 - 0x1.0p-20;
+        const double a = std::exp(x), b = exp_restated(x, p);
+        if (std::memcmp(&a, &b, 8) != 0) {
+            why = "restated exp differs from libm";
+            return false;
+        }
+    }
+    return true;
+}
+
+}  // namespace bsmh

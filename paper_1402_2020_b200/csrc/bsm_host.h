@@ -49,3 +49,22 @@ void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<
                       double* cost_after);
 
 }  // namespace bsmh
+
+namespace bsmh {
+
+// glibc's exp (sysdeps/ieee754/dbl-64/e_exp.c, FMA variant selected on
+// x86-64 CPUs with FMA+AVX2), restated so the device can reproduce
+// vote_weight's std::exp (refine.hpp:34) bit for bit.  The table and
+// constants are read from the libm the process runs with and the restatement
+// is validated against that libm's exp before use.
+struct ExpParams {
+    double invln2N, shift, negln2hiN, negln2loN, c2, c3, c4, c5;
+    uint64_t tab[256];
+};
+// True when the parameters were found and the restatement matched libm's exp
+// on every validation argument; `why` explains a false return.
+bool glibc_exp_params(ExpParams& p, std::string& why);
+// Host restatement (for tests / validation).
+double exp_restated(double x, const ExpParams& p);
+
+}  // namespace bsmh

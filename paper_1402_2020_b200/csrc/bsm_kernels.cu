@@ -1061,6 +1061,249 @@ __global__ void k_vote_refine_tpp(const uint32_t* __restrict__ vmap, int W, int 
 }
 
 // ---------------------------------------------------------------------------
+// K6'' -- voting refinement with device-computed weights.  vote_weight
+// (refine.hpp:30-35) = exp(-(double(lab_sad)/lc + sqrt(dx^2+dy^2)/le)):
+// lab_sad in float (same association), the divisions and the sum in IEEE
+// double, and exp by a restatement of glibc's e_exp.c (FMA build) whose
+// table and constants come from the host's libm and were validated bit for
+// bit against it (bsmh::glibc_exp_params).  sqrt(s)/le depends only on the
+// warp-uniform window offset and comes from a small host table.  Thread per
+// invalid pixel, own column of double bins in shared memory; per bin the adds
+// follow the reference's row-major voter order.
+struct ExpDev {
+    double invln2N, shift, negln2hiN, negln2loN, c2, c3, c4, c5;
+};
+
+__device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const unsigned long long* tab) {
+    // e_exp.c: |x| < 2^-54 -> 1 + x;  |x| >= 1024 -> 0 / inf;  512 <= |x| < 1024
+    // -> specialcase (the scale is built with a biased exponent).
+    const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned abstop = unsigned(xb >> 52) & 0x7ffu;
+    bool special = false;
+    if (abstop - 0x3c9u >= 0x3fu) {
+        if (int(abstop) - 0x3c9 < 0) return 1.0 + x;
+        if (abstop >= 0x409u) return (xb >> 63) ? 0.0 : __longlong_as_double(0x7ff0000000000000ll);
+        special = true;
+    }
+    double kd = fma(x, p.invln2N, p.shift);
+    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
+    kd -= p.shift;
+    const double r = fma(kd, p.negln2loN, fma(kd, p.negln2hiN, x));
+    const unsigned idx = 2u * unsigned(ki & 127ull);
+    const unsigned long long top = ki << 45;
+    const double tail = __longlong_as_double(static_cast<long long>(tab[idx]));
+    unsigned long long sbits = tab[idx + 1] + top;
+    const double r2 = r * r;
+    const double tmp = fma(r2 * r2, fma(r, p.c5, p.c4), fma(fma(r, p.c3, p.c2), r2, tail + r));
+    if (!special) {
+        const double scale = __longlong_as_double(static_cast<long long>(sbits));
+        return fma(scale, tmp, scale);
+    }
+    if (!(ki & 0x80000000ull)) {  // k > 0 (x >= 512): overflow range
+        sbits -= 1009ull << 52;
+        const double scale = __longlong_as_double(static_cast<long long>(sbits));
+        return 0x1p1009 * __dadd_rn(scale, __dmul_rn(scale, tmp));
+    }
+    sbits += 1022ull << 52;  // k < 0: subnormal range, rounded once
+    const double scale = __longlong_as_double(static_cast<long long>(sbits));
+    const double st = __dmul_rn(scale, tmp);
+    double y = __dadd_rn(scale, st);
+    if (y < 1.0) {
+        const double hi = __dadd_rn(y, 1.0);
+        const double lo = __dadd_rn(__dsub_rn(scale, y), st);
+        const double l2 = __dadd_rn(__dadd_rn(__dsub_rn(1.0, hi), y), lo);
+        y = __dsub_rn(__dadd_rn(l2, hi), 1.0);
+        if (y == 0.0) y = 0.0;
+    }
+    return __dmul_rn(y, 0x1p-1022);
+}
+
+// lab: per-pixel float Lab plane (3 floats / px), or nullptr to use lab256 of
+// the gray value carried in the voter map.
+__global__ void k_vote_refine_exp(const uint32_t* __restrict__ vmap, const float* __restrict__ lab,
+                                  const float* __restrict__ lab256, int W, int rows, int radius, double lc,
+                                  const double* __restrict__ e_over_le, ExpDev ep,
+                                  const unsigned long long* __restrict__ etab, const int* __restrict__ counters,
+                                  const int* __restrict__ inv, float* __restrict__ od, uint8_t* __restrict__ ov) {
+    extern __shared__ __align__(16) double dyn[];
+    unsigned long long* stab = reinterpret_cast<unsigned long long*>(dyn);  // 256
+    float* slab = reinterpret_cast<float*>(stab + 256);                     // 768
+    double* bins = reinterpret_cast<double*>(slab + 768);                   // [nbins][NT]
+    const int NT = blockDim.x, t = threadIdx.x;
+    for (int i = t; i < 256; i += NT) stab[i] = etab[i];
+    if (!lab)
+        for (int i = t; i < 768; i += NT) slab[i] = lab256[i];
+    __syncthreads();
+    const int max_bin = counters[0];
+    const int n_inv = counters[1];
+    for (int idx = blockIdx.x * NT + t; idx < n_inv; idx += gridDim.x * NT) {
+        const int p = inv[idx];
+        const int y = p / W, x = p - y * W;
+        float lx0, lx1, lx2;
+        if (lab) {
+            lx0 = lab[3 * size_t(p)];
+            lx1 = lab[3 * size_t(p) + 1];
+            lx2 = lab[3 * size_t(p) + 2];
+        } else {
+            const int u = int((vmap[p] >> 16) & 0xFFu);
+            lx0 = slab[3 * u];
+            lx1 = slab[3 * u + 1];
+            lx2 = slab[3 * u + 2];
+        }
+        for (int b = 0; b <= max_bin; ++b) bins[b * NT + t] = 0.0;
+        bool any = false;
+        for (int dy = -radius; dy <= radius; ++dy) {
+            const int py = y + dy;
+            if (py < 0 || py >= rows) continue;
+            const uint32_t* row = vmap + size_t(py) * W;
+            const int dy2 = dy * dy;
+            const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
+#pragma unroll 2
+            for (int dx = dx0; dx <= dx1; ++dx) {
+                const uint32_t e = __ldg(row + x + dx);
+                if (e & (1u << 24)) {
+                    float l0, l1, l2;
+                    if (lab) {
+                        const size_t q = 3 * (size_t(py) * W + x + dx);
+                        l0 = __ldg(lab + q);
+                        l1 = __ldg(lab + q + 1);
+                        l2 = __ldg(lab + q + 2);
+                    } else {
+                        const int v = int((e >> 16) & 0xFFu);
+                        l0 = slab[3 * v];
+                        l1 = slab[3 * v + 1];
+                        l2 = slab[3 * v + 2];
+                    }
+                    // lab_sad(at_x, at_p), image.hpp:144-146: (|dL| + |da|) + |db| in float
+                    const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
+                                                fabsf(__fsub_rn(lx2, l2)));
+                    const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
+                    double* bp = bins + int(e & 0xFFFFu) * NT + t;
+                    *bp += exp_glibc(arg, ep, stab);
+                    any = true;
+                }
+            }
+        }
+        if (!any) {
+            od[p] = 0.0f;
+            ov[p] = 0;
+            continue;
+        }
+        int best = 0;
+        double bv = bins[t];
+        for (int b = 1; b <= max_bin; ++b) {
+            const double v = bins[b * NT + t];
+            if (v > bv) {
+                bv = v;
+                best = b;
+            }
+        }
+        od[p] = float(best);
+        ov[p] = 1;
+    }
+}
+
+// K6c -- the same refinement without bin storage: bins are visited in
+// ascending order, one window scan per distinct voter bin; each scan adds the
+// weights of that bin's voters in row-major order (the reference's order) and
+// finds the next larger bin.  Argmax: best starts at bin 0 with its sum (0.0
+// if it has no voter) and moves only on a strictly larger sum -- exactly the
+// reference's loop over all bins 0..max_bin (unvisited bins hold 0.0).
+// Registers only, so occupancy is full; work = (#distinct bins) window scans
+// of 4-byte voter words + one weight per voter.
+__global__ void __launch_bounds__(256) k_vote_refine_scan(
+    const uint32_t* __restrict__ vmap, const float* __restrict__ lab, const float* __restrict__ lab256, int W,
+    int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
+    const unsigned long long* __restrict__ etab, const int* __restrict__ counters, const int* __restrict__ inv,
+    float* __restrict__ od, uint8_t* __restrict__ ov) {
+    __shared__ unsigned long long stab[256];
+    __shared__ float slab[768];
+    const int t = threadIdx.x;
+    for (int i = t; i < 256; i += blockDim.x) stab[i] = etab[i];
+    if (!lab)
+        for (int i = t; i < 768; i += blockDim.x) slab[i] = lab256[i];
+    __syncthreads();
+    const int n_inv = counters[1];
+    for (int idx = blockIdx.x * blockDim.x + t; idx < n_inv; idx += gridDim.x * blockDim.x) {
+        const int p = inv[idx];
+        const int y = p / W, x = p - y * W;
+        float lx0, lx1, lx2;
+        if (lab) {
+            lx0 = lab[3 * size_t(p)];
+            lx1 = lab[3 * size_t(p) + 1];
+            lx2 = lab[3 * size_t(p) + 2];
+        } else {
+            const int u = int((vmap[p] >> 16) & 0xFFu);
+            lx0 = slab[3 * u];
+            lx1 = slab[3 * u + 1];
+            lx2 = slab[3 * u + 2];
+        }
+        const int ya = max(0, y - radius), yb = min(rows - 1, y + radius);
+        const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
+        int cur = -1;          // bin accumulated by this scan (-1: discovery only)
+        int best = 0;
+        double bv = 0.0;       // bins[best]
+        bool any = false;
+        while (true) {
+            int next = 0x7FFFFFFF;
+            double sum = 0.0;
+            for (int py = ya; py <= yb; ++py) {
+                const uint32_t* row = vmap + size_t(py) * W + x;
+                const int dy2 = (py - y) * (py - y);
+                for (int dx = dx0; dx <= dx1; ++dx) {
+                    const uint32_t e = __ldg(row + dx);
+                    if (!(e & (1u << 24))) continue;
+                    const int b = int(e & 0xFFFFu);
+                    if (b > cur) {
+                        next = min(next, b);
+                    } else if (b == cur) {
+                        float l0, l1, l2;
+                        if (lab) {
+                            const size_t q = 3 * (size_t(py) * W + x + dx);
+                            l0 = __ldg(lab + q);
+                            l1 = __ldg(lab + q + 1);
+                            l2 = __ldg(lab + q + 2);
+                        } else {
+                            const int v = int((e >> 16) & 0xFFu);
+                            l0 = slab[3 * v];
+                            l1 = slab[3 * v + 1];
+                            l2 = slab[3 * v + 2];
+                        }
+                        const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
+                                                    fabsf(__fsub_rn(lx2, l2)));
+                        const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
+                        sum += exp_glibc(arg, ep, stab);
+                    }
+                }
+            }
+            if (cur >= 0) {
+                any = true;
+                if (cur == 0) bv = sum;
+                else if (sum > bv) {
+                    bv = sum;
+                    best = cur;
+                }
+            }
+            if (next == 0x7FFFFFFF) break;
+            cur = next;
+        }
+        if (!any) {
+            od[p] = 0.0f;
+            ov[p] = 0;
+        } else {
+            od[p] = float(best);
+            ov[p] = 1;
+        }
+    }
+}
+
+__global__ void k_exp_eval(const double* __restrict__ x, int n, ExpDev ep, const unsigned long long* __restrict__ tab,
+                           double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = exp_glibc(x[i], ep, tab);
+}
+
+// ---------------------------------------------------------------------------
 // Layout converters for the per-stage API (reference AoS u64 <-> device SoA).
 __global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
                              uint32_t* __restrict__ dst) {
@@ -1190,6 +1433,13 @@ struct bsm_ctx {
     float gray_lut[256], lab_lut[768];
     DevBuf d_rank;
     DevBuf d_wtab, d_s2col;
+    bool exp_ok = false;            // device exp restatement validated against host libm
+    int refine_mode = -1;           // -1: auto, 0: scan kernel, 1: smem bins, 2: weight table
+    std::string exp_why;
+    ExpDev exp_dev{};
+    DevBuf d_etab, d_elam, d_lab256;
+    double elam_le = 0;
+    int elam_radius = -1;
     double wt_lc = 0, wt_le = 0;
     int wt_radius = -1, wt_ncol = 0;
     // scratch
@@ -1395,31 +1645,59 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     return check_launch(c, "cost_wta");
 }
 
+int ensure_elam(bsm_ctx* c, double le, int radius) {
+    if (c->elam_le == le && c->elam_radius == radius) return BSM_OK;
+    std::vector<double> t(size_t(2 * radius * radius) + 1);
+    for (size_t k = 0; k < t.size(); ++k) t[k] = std::sqrt(double(k)) / le;  // sqrt(dx*dx + dy*dy) / lambda_e
+    BSM_TRY(c->d_elam.ensure(t.size() * 8));
+    BSM_CUDA(cudaMemcpy(c->d_elam.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+    c->elam_le = le;
+    c->elam_radius = radius;
+    return BSM_OK;
+}
+
 // Refinement of the invalid pixels listed in c->inv (count in counters[1],
 // max_bin in counters[0]) into c->ref_d / c->ref_v (pre-filled with the input
-// map).  nbins_max bounds max_bin + 1.
-int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t* gray, int W, int rows, int radius,
-                  int nbins_max) {
+// map).  nbins_max bounds max_bin + 1.  lab: per-pixel Lab plane or nullptr
+// (grayscale: the gray value indexes the Lab table).
+int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t* gray, const float* lab, int W,
+                  int rows, int radius, int nbins_max, double lc, double le) {
     const size_t px = size_t(rows) * W;
     const int nbins = round_up(std::max(nbins_max, 1), 32);
-    // The thread-per-pixel variant is latency-bound on the weight-table
-    // gathers unless ~8+ warps fit per SM, i.e. for short disparity ranges.
-    int nt = int((200 * 1024) / (size_t(nbins) * 8)) / 32 * 32;
-    if (nt >= 256) {
-        nt = 256;
+    const int tb = 256;
+    const int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 0 : 2);
+    if (c->exp_ok && mode == 0) {
+        BSM_TRY(ensure_elam(c, le, radius));
         BSM_TRY(c->vmap.ensure(px * 4));
-        const int tb = 256;
         k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
         BSM_TRY(check_launch(c, "make_vmap"));
-        const size_t sm = size_t(nbins) * nt * 8;
-        BSM_CUDA(cudaFuncSetAttribute(k_vote_refine_tpp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        k_vote_refine_tpp<<<c->sm_count, nt, sm, c->stream>>>(c->vmap.as<uint32_t>(), W, rows, radius,
-                                                              c->d_wtab.as<double>(), c->wt_ncol,
-                                                              c->d_s2col.as<int16_t>(), c->counters.as<int>(),
-                                                              c->inv.as<int>(), c->ref_d.as<float>(),
-                                                              c->ref_v.as<uint8_t>());
-        return check_launch(c, "vote_refine_tpp");
+        k_vote_refine_scan<<<c->sm_count * 8, 256, 0, c->stream>>>(
+            c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
+            c->exp_dev, c->d_etab.as<unsigned long long>(), c->counters.as<int>(), c->inv.as<int>(),
+            c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+        return check_launch(c, "vote_refine_scan");
     }
+    if (c->exp_ok && mode == 1) {
+        const size_t fixed = 256 * 8 + 768 * 4;
+        int nt = int((200 * 1024 - fixed) / (size_t(nbins) * 8)) / 32 * 32;
+        if (nt >= 32) {
+            nt = std::min(nt, 256);
+            BSM_TRY(ensure_elam(c, le, radius));
+            BSM_TRY(c->vmap.ensure(px * 4));
+            k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
+            BSM_TRY(check_launch(c, "make_vmap"));
+            const size_t sm = fixed + size_t(nbins) * nt * 8;
+            BSM_CUDA(cudaFuncSetAttribute(k_vote_refine_exp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            const int per_sm = std::max(1, int((220 * 1024) / sm));
+            k_vote_refine_exp<<<c->sm_count * per_sm, nt, sm, c->stream>>>(
+                c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
+                c->exp_dev, c->d_etab.as<unsigned long long>(), c->counters.as<int>(), c->inv.as<int>(),
+                c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+            return check_launch(c, "vote_refine_exp");
+        }
+    }
+    if (lab) return set_err(BSM_UNSUPPORTED, "bsm: colour refine needs the device exp (" + c->exp_why + ")");
+    BSM_TRY(ensure_weight_table(c, lc, le, radius));
     const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
     const size_t sm = size_t(warps) * nbins * 8;
     BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
@@ -1448,7 +1726,6 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
                     const bsm_params* p, bool want_unmasked) {
     BSM_TRY(check_pattern(c));
     BSM_TRY(validate_params(p));
-    BSM_TRY(ensure_weight_table(c, p->lambda_c, p->lambda_e, p->vote_radius));
     const int r0 = std::max(0, out0 - p->vote_radius);
     const int r1 = std::min(H, out0 + out_rows + p->vote_radius);
     const int rows = r1 - r0;
@@ -1500,8 +1777,8 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
         Scope s(c, T_REFINE);
         BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
         BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
-        BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, W, rows,
-                              p->vote_radius, p->d_max));
+        BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, nullptr, W, rows,
+                              p->vote_radius, p->d_max, p->lambda_c, p->lambda_e));
     }
     c->last_W = W;
     c->last_rows = rows;
@@ -1605,6 +1882,21 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
             bsm_ctx_destroy(c);
             return set_err(BSM_UNSUPPORTED, "bsm: gray conversion table is not strictly increasing");
         }
+    {
+        bsmh::ExpParams ep;
+        c->exp_ok = bsmh::glibc_exp_params(ep, c->exp_why);
+        if (c->exp_ok) {
+            c->exp_dev = ExpDev{ep.invln2N, ep.shift, ep.negln2hiN, ep.negln2loN, ep.c2, ep.c3, ep.c4, ep.c5};
+            if (c->d_etab.ensure(sizeof ep.tab) != BSM_OK ||
+                cudaMemcpy(c->d_etab.p, ep.tab, sizeof ep.tab, cudaMemcpyHostToDevice) != cudaSuccess)
+                c->exp_ok = false;
+        }
+        if (c->d_lab256.ensure(sizeof c->lab_lut) != BSM_OK ||
+            cudaMemcpy(c->d_lab256.p, c->lab_lut, sizeof c->lab_lut, cudaMemcpyHostToDevice) != cudaSuccess) {
+            bsm_ctx_destroy(c);
+            return set_err(BSM_CUDA_ERROR, "CUDA: Lab table upload failed");
+        }
+    }
     std::vector<uint8_t> rank(65536);
     bsmh::sad_rank_table(c->lab_lut, rank.data());
     int rc = c->d_rank.ensure(65536);
@@ -1624,7 +1916,7 @@ int bsm_ctx_destroy(bsm_ctx* c) {
     DevBuf* bufs[] = {&c->d_desc_off, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
-                      &c->counters, &c->inv, &c->vmap, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
+                      &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
     for (DevBuf* b : bufs) b->release();
     for (int t = 0; t < T_COUNT; ++t)
         for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
@@ -1861,7 +2153,6 @@ int bsm_vote_refine_u8(bsm_ctx* c, const float* d, const uint8_t* v, const uint8
         }
     }
     if (max_bin + 1 > 12288) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too large for the refine bins");
-    BSM_TRY(ensure_weight_table(c, lambda_c, lambda_e, vote_radius));
     BSM_TRY(c->img_l.ensure(px));
     BSM_TRY(c->chk_d.ensure(px * 4));
     BSM_TRY(c->chk_v.ensure(px));
@@ -1879,8 +2170,8 @@ int bsm_vote_refine_u8(bsm_ctx* c, const float* d, const uint8_t* v, const uint8
     if (!invalid.empty())
         BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_TRY(sync(c));  // host staging buffers (cnt, invalid) go out of scope
-    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), W, H,
-                          vote_radius, max_bin + 1));
+    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), nullptr, W, H,
+                          vote_radius, max_bin + 1, lambda_c, lambda_e));
     if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
     if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->ref_v.p, px, cudaMemcpyDeviceToHost, c->stream));
     return sync(c);
@@ -1931,6 +2222,75 @@ int bsm_pipeline_band_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, 
     m.refined_v = refined_v;
     BSM_TRY(fetch(c, &m));
     return sync(c);
+}
+
+int bsm_device_exp(bsm_ctx* c, const double* x, int n, double* out) {
+    BSM_TRY(begin_call(c));
+    if (!x || !out || n < 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad arguments");
+    if (!c->exp_ok) return set_err(BSM_UNSUPPORTED, "bsm: device exp unavailable (" + c->exp_why + ")");
+    if (n == 0) return BSM_OK;
+    BSM_TRY(c->aux0.ensure(size_t(n) * 8));
+    BSM_TRY(c->aux1.ensure(size_t(n) * 8));
+    BSM_CUDA(cudaMemcpyAsync(c->aux0.p, x, size_t(n) * 8, cudaMemcpyHostToDevice, c->stream));
+    k_exp_eval<<<(n + 255) / 256, 256, 0, c->stream>>>(c->aux0.as<double>(), n, c->exp_dev,
+                                                       c->d_etab.as<unsigned long long>(), c->aux1.as<double>());
+    BSM_TRY(check_launch(c, "exp_eval"));
+    BSM_CUDA(cudaMemcpyAsync(out, c->aux1.p, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c);
+}
+
+int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const float* lab, int W, int H,
+                        double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_dims(W, H));
+    if (!d || !v || !lab) return set_err(BSM_INVALID_ARGUMENT, "bsm: null input");
+    if (!(lambda_c > 0)) return set_err(BSM_INVALID_ARGUMENT, "refine: lambda_c must be > 0");
+    if (!(lambda_e > 0)) return set_err(BSM_INVALID_ARGUMENT, "refine: lambda_e must be > 0");
+    if (vote_radius < 1) return set_err(BSM_INVALID_ARGUMENT, "refine: vote_radius must be >= 1");
+    if (vote_radius > 180) return set_err(BSM_UNSUPPORTED, "bsm: vote_radius > 180 is outside this build's envelope");
+    const size_t px = size_t(W) * H;
+    int max_bin = 0;
+    std::vector<int> invalid;
+    for (size_t i = 0; i < px; ++i) {
+        if (v[i]) {
+            const double dv = double(d[i]);
+            if (!(dv > -0.5) || !(dv < 65535.0))
+                return set_err(BSM_INVALID_ARGUMENT, "vote_refine: valid disparity out of range");
+            max_bin = std::max(max_bin, int(std::lround(dv)));
+        } else {
+            invalid.push_back(int(i));
+        }
+    }
+    BSM_TRY(c->img_l.ensure(px));
+    BSM_TRY(c->aux2.ensure(px * 12));
+    BSM_TRY(c->chk_d.ensure(px * 4));
+    BSM_TRY(c->chk_v.ensure(px));
+    BSM_TRY(c->ref_d.ensure(px * 4));
+    BSM_TRY(c->ref_v.ensure(px));
+    BSM_TRY(c->counters.ensure(64));
+    BSM_TRY(c->inv.ensure(std::max<size_t>(4, invalid.size() * 4)));
+    BSM_CUDA(cudaMemsetAsync(c->img_l.p, 0, px, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->aux2.p, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->chk_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->chk_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
+    int cnt[2] = {max_bin, int(invalid.size())};
+    BSM_CUDA(cudaMemcpyAsync(c->counters.p, cnt, 8, cudaMemcpyHostToDevice, c->stream));
+    if (!invalid.empty())
+        BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_TRY(sync(c));
+    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), c->aux2.as<float>(),
+                          W, H, vote_radius, max_bin + 1, lambda_c, lambda_e));
+    if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->ref_v.p, px, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c);
+}
+
+int bsm_set_refine_mode(bsm_ctx* c, int mode) {
+    if (!c || mode < -1 || mode > 2) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad refine mode");
+    c->refine_mode = mode;
+    return BSM_OK;
 }
 
 int bsm_stream(bsm_ctx* c, void** stream) {
