@@ -1297,6 +1297,152 @@ __global__ void __launch_bounds__(256) k_vote_refine_scan(
     }
 }
 
+// K6d -- voting refinement, NP invalid pixels per warp (LPP = 32/NP lanes
+// each).  Per window row the LPP lanes of a pixel form the bins and weights of
+// LPP consecutive voters in parallel (weight from the exact host table, or
+// the device exp for Lab planes), stage them, then fold them in voter order:
+// lane sl owns the bins b with (b % LPP) == sl and walks the staged entries in
+// order, keeping its current bin's running sum in a register.  Per bin the
+// additions are therefore the reference's row-major sequence; the NP pixels
+// fold side by side, so one warp step advances NP voters.
+template <int NP, bool DEVEXP>
+__global__ void __launch_bounds__(256) k_vote_refine_fold(
+    const uint32_t* __restrict__ vmap, const float* __restrict__ lab, const float* __restrict__ lab256, int W,
+    int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
+    const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
+    const int16_t* __restrict__ s2col, const int* __restrict__ counters, const int* __restrict__ inv, int nbins_cap,
+    float* __restrict__ od, uint8_t* __restrict__ ov) {
+    constexpr int LPP = 32 / NP;
+    extern __shared__ __align__(16) double fsm[];
+    unsigned long long* stab = reinterpret_cast<unsigned long long*>(fsm);  // 256 (DEVEXP)
+    float* slab = reinterpret_cast<float*>(stab + 256);                     // 768 (DEVEXP, gray)
+    const int nwarps = blockDim.x >> 5;
+    double* sw_all = reinterpret_cast<double*>(slab + 768);                 // [warps][32] staged weights
+    int* sb_all = reinterpret_cast<int*>(sw_all + nwarps * 32);             // [warps][32] staged bins
+    double* bins_all = reinterpret_cast<double*>(sb_all + nwarps * 32);     // [warps][NP][nbins_cap]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / LPP, sl = lane % LPP;
+    if (DEVEXP) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) stab[i] = etab[i];
+        if (!lab)
+            for (int i = threadIdx.x; i < 768; i += blockDim.x) slab[i] = lab256[i];
+    }
+    __syncthreads();
+    double* sw = sw_all + warp * 32;
+    int* sbn = sb_all + warp * 32;
+    double* bins = bins_all + size_t(warp * NP + sub) * nbins_cap;
+    const unsigned full = 0xFFFFFFFFu;
+    const unsigned submask = (LPP == 32) ? full : (((1u << LPP) - 1u) << (sub * LPP));
+    const int max_bin = counters[0];
+    const int n_inv = counters[1];
+    const int gw = blockIdx.x * nwarps + warp, nw = gridDim.x * nwarps;
+    for (int base = gw * NP; base < n_inv; base += nw * NP) {  // warp-uniform loop
+        const int idx = base + sub;
+        const bool live = idx < n_inv;
+        const int p = live ? inv[idx] : 0;
+        const int y = p / W, x = p - y * W;
+        const uint32_t e0 = vmap[p];
+        const int u = int((e0 >> 16) & 0xFFu);
+        float lx0 = 0.f, lx1 = 0.f, lx2 = 0.f;
+        if (DEVEXP) {
+            if (lab) {
+                lx0 = lab[3 * size_t(p)];
+                lx1 = lab[3 * size_t(p) + 1];
+                lx2 = lab[3 * size_t(p) + 2];
+            } else {
+                lx0 = slab[3 * u];
+                lx1 = slab[3 * u + 1];
+                lx2 = slab[3 * u + 2];
+            }
+        }
+        for (int b = sl; b <= max_bin; b += LPP) bins[b] = 0.0;
+        int cur = -1;
+        double acc = 0.0;
+        bool any = false;
+        const int tu = u * (u + 1) / 2;
+        for (int dy = -radius; dy <= radius; ++dy) {
+            const int py = y + dy;
+            const bool rowok = live && py >= 0 && py < rows;
+            const uint32_t* row = vmap + size_t(rowok ? py : 0) * W;
+            const int dy2 = dy * dy;
+            for (int dx0 = -radius; dx0 <= radius; dx0 += LPP) {
+                const int dx = dx0 + sl;
+                const int px = x + dx;
+                int bin = -1;
+                double w = 0.0;
+                if (rowok && dx <= radius && px >= 0 && px < W) {
+                    const uint32_t e = __ldg(row + px);
+                    if (e & (1u << 24)) {
+                        bin = int(e & 0xFFFFu);
+                        const int v = int((e >> 16) & 0xFFu);
+                        if (DEVEXP) {
+                            float l0, l1, l2;
+                            if (lab) {
+                                const size_t q = 3 * (size_t(py) * W + px);
+                                l0 = __ldg(lab + q);
+                                l1 = __ldg(lab + q + 1);
+                                l2 = __ldg(lab + q + 2);
+                            } else {
+                                l0 = slab[3 * v];
+                                l1 = slab[3 * v + 1];
+                                l2 = slab[3 * v + 2];
+                            }
+                            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
+                                                        fabsf(__fsub_rn(lx2, l2)));
+                            const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
+                            w = exp_glibc(arg, ep, stab);
+                        } else {
+                            const int tri = v >= u ? (v * (v + 1) / 2 + u) : (tu + v);
+                            w = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
+                        }
+                    }
+                }
+                any |= (__ballot_sync(full, bin >= 0) & submask) != 0u;
+                sbn[lane] = bin;
+                sw[lane] = w;
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < LPP; ++j) {
+                    const int b = sbn[sub * LPP + j];
+                    if (b >= 0 && (b % LPP) == sl) {
+                        if (b != cur) {
+                            if (cur >= 0) bins[cur] = acc;
+                            cur = b;
+                            acc = bins[b];
+                        }
+                        acc += sw[sub * LPP + j];
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (cur >= 0) bins[cur] = acc;
+        __syncwarp();
+        // argmax: strict '>' from bin 0 == first bin holding the maximum
+        double bv = -1.0;
+        int bb = 0x7FFFFFFF;
+        for (int b = sl; b <= max_bin; b += LPP)
+            if (bins[b] > bv) {
+                bv = bins[b];
+                bb = b;
+            }
+#pragma unroll
+        for (int o = LPP / 2; o > 0; o >>= 1) {
+            const double ov2 = __shfl_xor_sync(full, bv, o);
+            const int ob = __shfl_xor_sync(full, bb, o);
+            if (ov2 > bv || (ov2 == bv && ob < bb)) {
+                bv = ov2;
+                bb = ob;
+            }
+        }
+        if (live && sl == 0) {
+            od[p] = any ? float(bb) : 0.0f;
+            ov[p] = any ? 1 : 0;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_exp_eval(const double* __restrict__ x, int n, ExpDev ep, const unsigned long long* __restrict__ tab,
                            double* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1665,7 +1811,27 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
     const size_t px = size_t(rows) * W;
     const int nbins = round_up(std::max(nbins_max, 1), 32);
     const int tb = 256;
-    const int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 0 : 2);
+    const int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 4 : 3);
+    if (mode == 3 || (mode == 4 && c->exp_ok)) {
+        constexpr int NPX = 4;
+        const bool devexp = mode == 4;
+        if (devexp) BSM_TRY(ensure_elam(c, le, radius));
+        else BSM_TRY(ensure_weight_table(c, lc, le, radius));
+        BSM_TRY(c->vmap.ensure(px * 4));
+        k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
+        BSM_TRY(check_launch(c, "make_vmap"));
+        const int warps = 8;
+        const size_t sm = 256 * 8 + 768 * 4 + size_t(warps) * 32 * 12 + size_t(warps) * NPX * nbins * 8;
+        auto kern = devexp ? k_vote_refine_fold<NPX, true> : k_vote_refine_fold<NPX, false>;
+        BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
+        kern<<<c->sm_count * per_sm, warps * 32, sm, c->stream>>>(
+            c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
+            c->exp_dev, c->d_etab.as<unsigned long long>(), c->d_wtab.as<double>(), c->wt_ncol,
+            c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(),
+            c->ref_v.as<uint8_t>());
+        return check_launch(c, "vote_refine_fold");
+    }
     if (c->exp_ok && mode == 0) {
         BSM_TRY(ensure_elam(c, le, radius));
         BSM_TRY(c->vmap.ensure(px * 4));
@@ -2288,7 +2454,7 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
 }
 
 int bsm_set_refine_mode(bsm_ctx* c, int mode) {
-    if (!c || mode < -1 || mode > 2) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad refine mode");
+    if (!c || mode < -1 || mode > 4) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad refine mode");
     c->refine_mode = mode;
     return BSM_OK;
 }

@@ -23,6 +23,8 @@ def main():
     import torch
     ctx = bsm.Context(0)
     ctx.set_pattern(bsm.generate_pattern())
+    if len(sys.argv) > 3:
+        ctx.set_refine_mode(int(sys.argv[3]))
     left, right = workload_pair(key)
     dl = torch.from_numpy(left).cuda()
     dr = torch.from_numpy(right).cuda()
