@@ -343,24 +343,8 @@ __global__ void __launch_bounds__(kMaskWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
-// K2' -- mask for n <= 4096: one warp per CTA, 8 pixels per CTA, two pixels
-// per pass.  Same contract as k_mask; restructured for issue rate:
-//   * the warp's rank table rho[] sits at the start of dynamic shared memory
-//     (a constant base, so every gather is one LDS [R + imm]) and holds both
-//     pixels' ranks as one u32 (rhoA | rhoB << 16) per used offset: one
-//     gather serves two pixels and a = max(rhoP, rhoQ) of both is one
-//     VIMNMX.U16x2;
-//   * pair endpoints come pre-scaled (byte offsets 4P | 4Q << 16) from a
-//     4096-entry L1-resident table; pairs >= n point at a sentinel entry
-//     (a = 255), so the unrolled gather loop has no branches;
-//   * lane l keeps a of pair 32g+l for g = 0..127 as bytes
-//     [A(2j) B(2j) A(2j+1) B(2j+1)] in 64 registers;
-//   * selection: step 1 counts a > 127 (bit 7); each pixel then maps its bytes
-//     into a 0..128 window (low range: min(a,128); high range: a-128 or 0) so
-//     every later count is IADD + LOP3 + shift-add per 4 values:
-//     bit 7 of (a' + 127 - t) == (a' > t), per-byte thresholds, no carries;
-//   * output: one ballot per (group, pixel); lanes 0..3 store the four words
-//     of a register pair in one STS.
+// Shared helpers of the n <= 4096 mask kernel (k_mask4): one warp per CTA,
+// kM3Px pixels per CTA, two pixels per pass.
 constexpr int kM3Px = 8;
 
 __device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
@@ -371,121 +355,6 @@ __device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
 
 __device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_off) {
     return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + byte_off);
-}
-
-__global__ void __launch_bounds__(32, 16)
-    k_mask3(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
-            const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
-            const uint8_t* __restrict__ rank, int half, int NW, int Wp, uint32_t* __restrict__ mask) {
-    constexpr int NREG = 64;  // 128 groups x 2 pixels, 4 bytes per register
-    constexpr int GMAX = 2 * NREG;
-    extern __shared__ __align__(16) uint32_t dsm[];
-    uint32_t* rho = dsm;                                               // rho_words (u + sentinel)
-    uint32_t* stage = dsm + rho_words;                                 // GMAX x kM3Px
-    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + GMAX * kM3Px);  // 2 x 256 rank rows
-    uint8_t* tile = rrows + 512;                                       // (2h+1) x (kM3Px + 2h)
-    const int G = (n + 31) >> 5;
-    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
-    const int lane = threadIdx.x;
-    const int x0 = blockIdx.x * kM3Px;
-    const int ly = blockIdx.y;
-    const int y = ybeg + ly;
-    for (int idx = lane; idx < TW * TH; idx += 32) {
-        const int r = idx / TW, c = idx - r * TW;
-        const int gx = min(max(x0 - half + c, 0), W - 1);
-        const int gy = min(max(y - half + r, 0), H - 1);
-        tile[idx] = __ldg(img + size_t(gy) * W + gx);
-    }
-    if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
-    __syncwarp();
-
-    const int k = max(1, n / 4);
-    const unsigned full = 0xFFFFFFFFu;
-    const int slots = 32 * GMAX;  // per pixel, pads included (always "greater")
-#pragma unroll 1
-    for (int q = 0; q < kM3Px; q += 2) {
-        const int cia = half * TW + half + q, cib = cia + 1;
-        // the two centres' rank rows (rank[c][*], 256 B each) into shared memory
-        {
-            const uint4* src = reinterpret_cast<const uint4*>(rank + 256 * int(lane < 16 ? tile[cia] : tile[cib]));
-            reinterpret_cast<uint4*>(rrows)[lane] = __ldg(src + (lane & 15));
-        }
-        __syncwarp();
-        for (int j = lane; j < u; j += 32) {
-            const int o = __ldg(uoff + j);
-            rho[j] = uint32_t(rrows[tile[cia + o]]) | (uint32_t(rrows[256 + tile[cib + o]]) << 16);
-        }
-        __syncwarp();
-
-        uint32_t R[NREG];
-        uint32_t acc = 0;  // step 1: #{a > 127}, bytes 0,2 -> A, 1,3 -> B
-#pragma unroll
-        for (int jj = 0; jj < NREG / 2; ++jj) {
-            const uint4 P = __ldg(p4 + 32 * jj + lane);  // byte offsets of groups 4jj..4jj+3
-            const uint4 Q = __ldg(q4 + 32 * jj + lane);
-            const uint32_t m0 = vmax_u16x2(lds_u32(rho, P.x), lds_u32(rho, Q.x));
-            const uint32_t m1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
-            const uint32_t m2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
-            const uint32_t m3 = vmax_u16x2(lds_u32(rho, P.w), lds_u32(rho, Q.w));
-            R[2 * jj] = __byte_perm(m0, m1, 0x6420);
-            R[2 * jj + 1] = __byte_perm(m2, m3, 0x6420);
-            acc = __umulhi(R[2 * jj] & 0x80808080u, 1u << 25) + acc;
-            acc = __umulhi(R[2 * jj + 1] & 0x80808080u, 1u << 25) + acc;
-        }
-        __syncwarp();  // rho and rrows are rewritten by the next pass
-
-        int gtA = __reduce_add_sync(full, (acc & 0xFFu) + ((acc >> 16) & 0xFFu));
-        int gtB = __reduce_add_sync(full, ((acc >> 8) & 0xFFu) + (acc >> 24));
-        const uint32_t Hm = (slots - gtA < k ? 0x00FF00FFu : 0u) | (slots - gtB < k ? 0xFF00FF00u : 0u);
-#pragma unroll
-        for (int j = 0; j < NREG; ++j) {
-            const uint32_t b = R[j] & 0x80808080u;
-            const uint32_t S = b - (b >> 7);  // 0x7F where a >= 128
-            // high range: R & S (a - 128, or 0); low range: R & ~S (a, or 0x80 where a >= 128)
-            R[j] = R[j] & ((S & Hm) | (~S & ~Hm));
-        }
-        int loA = 0, hiA = 127, loB = 0, hiB = 127;
-#pragma unroll 1
-        for (int it = 0; it < 7; ++it) {
-            const int midA = (loA + hiA) >> 1, midB = (loB + hiB) >> 1;
-            const uint32_t K = uint32_t(127 - midA) * 0x00010001u + uint32_t(127 - midB) * 0x01000100u;
-            uint32_t c = 0;
-#pragma unroll
-            for (int j = 0; j < NREG; ++j) c = __umulhi((R[j] + K) & 0x80808080u, 1u << 25) + c;
-            gtA = __reduce_add_sync(full, (c & 0xFFu) + ((c >> 16) & 0xFFu));
-            gtB = __reduce_add_sync(full, ((c >> 8) & 0xFFu) + (c >> 24));
-            if (slots - gtA >= k) hiA = midA; else loA = midA + 1;
-            if (slots - gtB >= k) hiB = midB; else loB = midB + 1;
-        }
-        // Output: bit = a <= T  <=>  not (a' > t).  Lanes 0..3 store words
-        // (2j, A), (2j, B), (2j+1, A), (2j+1, B); pad groups land in stage rows
-        // >= G and are never copied out.
-        const uint32_t K = uint32_t(127 - loA) * 0x00010001u + uint32_t(127 - loB) * 0x01000100u;
-        uint32_t* sdst = stage + (lane >> 1) * kM3Px + q + (lane & 1);
-        const bool writer = lane < 4;
-#pragma unroll
-        for (int j = 0; j < NREG; ++j) {
-            const uint32_t f = (R[j] + K) & 0x80808080u;
-            const uint32_t wA0 = __ballot_sync(full, !(f & 0x80u));
-            const uint32_t wB0 = __ballot_sync(full, !(f & 0x8000u));
-            const uint32_t wA1 = __ballot_sync(full, !(f & 0x800000u));
-            const uint32_t wB1 = __ballot_sync(full, !(f & 0x80000000u));
-            const uint32_t wv = lane == 0 ? wA0 : lane == 1 ? wB0 : lane == 2 ? wA1 : wB1;
-            if (writer) sdst[2 * j * kM3Px] = wv;
-        }
-    }
-    __syncwarp();
-    // Tail mask of the last partial word, then coalesced rows of 8 words.
-    const int rem = n & 31;
-    for (int idx = lane; idx < NW * kM3Px; idx += 32) {
-        const int w = idx / kM3Px, j = idx - w * kM3Px;
-        uint32_t v = 0;
-        if (w < G) {
-            v = stage[w * kM3Px + j];
-            if (rem && w == G - 1) v &= (1u << rem) - 1u;
-        }
-        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1726,10 +1595,6 @@ size_t mask4_smem(const bsm_ctx* c) {
            size_t(TW) * TH;
 }
 
-size_t mask3_smem(const bsm_ctx* c) {
-    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
-    return size_t(round_up(c->u + 1, 4)) * 4 + size_t(128) * kM3Px * 4 + 512 + size_t(TW) * TH;
-}
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
@@ -2164,9 +2029,8 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     }
     c->slot_used.assign(size_t(c->mslots), -1);
     for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
-    // k_mask3: byte offsets into its u32 rank table, P and Q as two tables of
-    // uint4 [jj][lane] = groups 4jj..4jj+3 of pair 32g + lane; pads -> the
-    // sentinel slot u.
+    // Byte offsets into the u32 rank table (tables 0/1: group-major order,
+    // kept for layout compatibility; tables 2/3 below are k_mask4's).
     std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->u));
     for (int i = 0; i < std::min(n, 4096); ++i) {
         const int g = i >> 5, l = i & 31;
