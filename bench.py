@@ -181,8 +181,12 @@ def main():
     cfg = bsm.BsmConfig(d_max=D)
     pattern = bsm.generate_pattern(cfg=cfg)
     ctx.set_pattern(pattern)
-    # weak scaling: rank r matches pair index r of the workload's seed sequence
-    left, right = workload_pair(args.workload, index=rank)
+    # Partition: configs[4] (c5, one frame) -> contiguous row
+    # bands with a vote-radius halo + one NCCL all-gather of the refined bands
+    # (strong scaling); every other workload -> rank r matches pair index r of
+    # the workload's seed sequence (independent units, weak scaling).
+    bands = args.workload == "c5" and world > 1
+    left, right = workload_pair(args.workload, index=0 if bands else rank)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     d_left = torch.from_numpy(left).to(dev)
@@ -194,9 +198,26 @@ def main():
     import ctypes as C
     p = bsm_params(D, cfg.lambda_c, cfg.lambda_e, cfg.lr_tolerance, cfg.vote_radius)
 
+    if bands:
+        from paper_1402_2020_b200.dist import band_rows
+        y0, y1 = band_rows(H, world, rank)
+        rows_max = -(-H // world)
+        band_d = torch.zeros((rows_max, W), dtype=torch.float32, device=dev)
+        band_v = torch.zeros((rows_max, W), dtype=torch.uint8, device=dev)
+        all_d = [torch.empty_like(band_d) for _ in range(world)]
+        all_v = [torch.empty_like(band_v) for _ in range(world)]
+
     def step_device():
-        check(lib().bsm_pipeline_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
-                                           C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
+        if not bands:
+            check(lib().bsm_pipeline_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
+                                               C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
+            return
+        check(lib().bsm_pipeline_band_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
+                                                C.c_void_p(d_right.data_ptr()), W, H, y0, y1, C.byref(p)))
+        check(lib().bsm_copy_result_device(ctx.handle, C.c_void_p(band_d.data_ptr()), C.c_void_p(band_v.data_ptr())))
+        with torch.cuda.stream(stream):  # stream-ordered after the band kernels
+            dist.all_gather(all_d, band_d)
+            dist.all_gather(all_v, band_v)
 
     def barrier():
         torch.cuda.synchronize()
@@ -229,7 +250,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    units = W * H * D * world * args.steps
+    units = W * H * D * (1 if bands else world) * args.steps
     value = units / (total_ms * 1e-3) / 1e6
 
     # ---- e2e through the public C ABI with pinned host buffers ----
@@ -239,9 +260,23 @@ def main():
     h_rv = torch.empty((H, W), dtype=torch.uint8).pin_memory()
     maps = bsm._lib.bsm_maps(h_rd.data_ptr(), h_rv.data_ptr(), None, None, None, None, None)
 
+    if bands:
+        h_all_d = torch.empty((world * rows_max, W), dtype=torch.float32).pin_memory()
+        h_all_v = torch.empty((world * rows_max, W), dtype=torch.uint8).pin_memory()
+
     def step_e2e():
-        check(lib().bsm_pipeline_u8(ctx.handle, C.c_void_p(h_left.data_ptr()), C.c_void_p(h_right.data_ptr()),
-                                    W, H, C.byref(p), 0, C.byref(maps)))
+        if not bands:
+            check(lib().bsm_pipeline_u8(ctx.handle, C.c_void_p(h_left.data_ptr()), C.c_void_p(h_right.data_ptr()),
+                                        W, H, C.byref(p), 0, C.byref(maps)))
+            return
+        with torch.cuda.stream(stream):
+            d_left.copy_(h_left, non_blocking=True)
+            d_right.copy_(h_right, non_blocking=True)
+        step_device()
+        with torch.cuda.stream(stream):
+            h_all_d.copy_(torch.cat(all_d), non_blocking=True)
+            h_all_v.copy_(torch.cat(all_v), non_blocking=True)
+        stream.synchronize()
 
     step_e2e()
     barrier()
@@ -276,12 +311,16 @@ def main():
     prof_ms = {k: float(np.mean(v)) for k, v in prof.items() if np.mean(v) > 0}
     popc_peak, csa_peak = ctx.measure_word_peaks()  # word-ops/s, this GPU, live
 
-    evals_dir = in_bounds_evals(W, H, D)
+    if bands:  # fields / WTA / check cover the band plus the vote-radius halo
+        hr = min(H, y1 + cfg.vote_radius) - max(0, y0 - cfg.vote_radius)
+        evals_dir = in_bounds_evals(W, hr, D)
+    else:
+        evals_dir = in_bounds_evals(W, H, D)
     wta_ms = (prof_ms.get("wta_left", 0) + prof_ms.get("wta_right", 0)) / 2
     achieved = evals_dir * (4096 // 32) / (wta_ms * 1e-3)  # u32 masked-xor-popcount word-ops / s
     peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
     hbm_peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-    alg_bytes = W * H * (3 * 4096 // 8 + 4)  # ref desc + ref mask + other desc, + key out
+    alg_bytes = W * (hr if bands else H) * (3 * 4096 // 8 + 4)  # ref desc + ref mask + other desc, + key
     hbm_ach = alg_bytes / (wta_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -291,13 +330,16 @@ def main():
     line = {
         "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if bands else "weak", "vs_baseline": None,
         "dtype": "u32 popcount / f64 votes", "data": "synthetic (BASELINE.json generator, SURVEY.md 8(d))",
-        "config": {"workload": w.name, "width": W, "height": H, "d_max": D, "n": 4096, "pairs_per_step": world,
-                   "parallelism": f"pairs x{world}" if world > 1 else "1 pair",
+        "config": {"workload": w.name, "width": W, "height": H, "d_max": D, "n": 4096,
+                   "pairs_per_step": 1 if bands else world,
+                   "parallelism": (f"row bands x{world} + NCCL all-gather" if bands
+                                   else (f"pairs x{world}" if world > 1 else "1 pair")),
                    "l2": "256 MiB flush before every step (outside events); working set 3.2 GB >> L2"},
         "e2e": {"value": e2e_value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 2 * W * H,
-                "d2h_bytes_per_step": 5 * W * H, "ms_per_step": float(te.item()) / args.steps},
+                "d2h_bytes_per_step": 5 * (world * rows_max if bands else H) * W,
+                "ms_per_step": float(te.item()) / args.steps},
         "gpu_launches": launches * args.steps,
         "roofline": {"bound": "int-pipes (LOP3+POPC)",
                      "kernel": "k_cost_wta (fused masked Hamming + WTA, per direction)",

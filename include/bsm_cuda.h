@@ -124,6 +124,16 @@ int bsm_fetch_maps(bsm_ctx* ctx, bsm_maps* out);
 int bsm_pipeline_band_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H, int y0, int y1,
                          const bsm_params* params, float* refined_d, uint8_t* refined_v);
 
+/* Device-resident band: views on the device; read the result with
+ * bsm_fetch_maps (refined_d/v only) or bsm_result_device. */
+int bsm_pipeline_band_u8_device(bsm_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int W, int H, int y0,
+                                int y1, const bsm_params* params);
+/* Device pointers to the refined rows of the last pipeline/band call (valid
+ * until the next call on the context): [row0, row0 + nrows) x W. */
+int bsm_result_device(bsm_ctx* ctx, const float** refined_d, const uint8_t** refined_v, int* row0, int* nrows);
+/* Stream-ordered device-to-device copy of those rows into caller buffers. */
+int bsm_copy_result_device(bsm_ctx* ctx, float* dst_d, uint8_t* dst_v);
+
 /* Instrumentation.  bsm_stream returns the cudaStream_t the context launches
  * on.  When profiling is enabled, bsm_last_timings reports the device time (ms)
  * of the last pipeline's kernels, in the order of bsm_timing_names. */

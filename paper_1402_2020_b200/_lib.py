@@ -95,6 +95,9 @@ _SIGS = {
     "bsm_pipeline_u8_device": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I],
     "bsm_fetch_maps": [_P, C.POINTER(bsm_maps)],
     "bsm_pipeline_band_u8": [_P, _P, _P, _I, _I, _I, _I, C.POINTER(bsm_params), _P, _P],
+    "bsm_pipeline_band_u8_device": [_P, _P, _P, _I, _I, _I, _I, C.POINTER(bsm_params)],
+    "bsm_result_device": [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "bsm_copy_result_device": [_P, _P, _P],
     "bsm_stream": [_P, C.POINTER(C.c_void_p)],
     "bsm_set_profiling": [_P, _I],
     "bsm_last_timings": [_P, _P, _I, C.POINTER(C.c_int)],

@@ -2323,6 +2323,38 @@ int bsm_set_refine_mode(bsm_ctx* c, int mode) {
     return BSM_OK;
 }
 
+int bsm_pipeline_band_u8_device(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_right, int W, int H, int y0,
+                                 int y1, const bsm_params* params) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    if (!d_left || !d_right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    if (y0 < 0 || y1 > H || y0 >= y1) return set_err(BSM_INVALID_ARGUMENT, "bsm: band rows out of range");
+    return pipeline_device(c, d_left, d_right, W, H, y0, y1 - y0, params, false);
+}
+
+int bsm_result_device(bsm_ctx* c, const float** refined_d, const uint8_t** refined_v, int* row0, int* nrows) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    if (c->last_W == 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: no pipeline result");
+    const size_t off = size_t(c->last_out0 - c->last_r0) * c->last_W;
+    if (refined_d) *refined_d = c->ref_d.as<float>() + off;
+    if (refined_v) *refined_v = c->ref_v.as<uint8_t>() + off;
+    if (row0) *row0 = c->last_out0;
+    if (nrows) *nrows = c->last_out_rows;
+    return BSM_OK;
+}
+
+int bsm_copy_result_device(bsm_ctx* c, float* dst_d, uint8_t* dst_v) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    if (c->last_W == 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: no pipeline result");
+    const size_t off = size_t(c->last_out0 - c->last_r0) * c->last_W;
+    const size_t n = size_t(c->last_out_rows) * c->last_W;
+    if (dst_d) BSM_CUDA(cudaMemcpyAsync(dst_d, c->ref_d.as<float>() + off, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    if (dst_v) BSM_CUDA(cudaMemcpyAsync(dst_v, c->ref_v.as<uint8_t>() + off, n, cudaMemcpyDeviceToDevice, c->stream));
+    return BSM_OK;
+}
+
 int bsm_stream(bsm_ctx* c, void** stream) {
     if (!c || !stream) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
     *stream = c->stream;
