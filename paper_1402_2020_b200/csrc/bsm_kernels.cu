@@ -570,9 +570,11 @@ __global__ void __launch_bounds__(256, 2)
     uint32_t* red = csm + ST * STAGE;                      // [8][T]
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    const int x0 = blockIdx.x * T;
-    const int y = blockIdx.y;
-    const int d0 = blockIdx.z * DC;
+    // grid = (d-chunks, x-tiles, rows): the CTAs sharing a tile's reference
+    // words (same x-tile, different d) run back to back and hit in L2.
+    const int x0 = blockIdx.y * T;
+    const int y = blockIdx.z;
+    const int d0 = blockIdx.x * DC;
     const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
     const int nchunks = (NW + K - 1) / K;
 
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(256, 2)
         for (int w = 1; w < 8; ++w) best = min(best, red[w * T + tid]);
         const int x = x0 + tid;
         if (x < W && best != 0xFFFFFFFFu) {
-            if (gridDim.z == 1) keys[size_t(y) * W + x] = best;
+            if (gridDim.x == 1) keys[size_t(y) * W + x] = best;
             else atomicMin(&keys[size_t(y) * W + x], best);
         }
     }
@@ -1643,7 +1645,7 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     const int Wp = round_up(W, 128);
     const int dz = (d_max + kCostDisp - 1) / kCostDisp;
     if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
-    dim3 grid(Wp / kCostTile, rows, dz);
+    dim3 grid(dz, Wp / kCostTile, rows);
     const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
     const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4;
     auto launch = [&](auto kern) -> int {
