@@ -141,28 +141,36 @@ __device__ __forceinline__ uint32_t bytes_gt(uint32_t p, uint32_t q) {
 
 __global__ void __launch_bounds__(kD2TX* kD2TY)
     k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
-                  const uint4* __restrict__ ptab, int n, int half, int TWs, int NW, int Wp,
+                  const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wp,
                   uint32_t* __restrict__ desc) {
+    // tile: clamped bytes; t4[i] = bytes i..i+3 of the tile, so the 4 samples
+    // of a thread's 4 pixels at any offset are one aligned 32-bit load.
     extern __shared__ __align__(16) uint32_t dsm[];
-    uint8_t* tile = reinterpret_cast<uint8_t*>(dsm);
     const int TH = kD2TY * kD2Rows + 2 * half;
+    const int NT = TWs * TH;
+    uint32_t* t4 = dsm;
+    uint8_t* tile = reinterpret_cast<uint8_t*>(dsm + NT);
     const int tid = threadIdx.y * kD2TX + threadIdx.x;
     const int gx0 = blockIdx.x * (kD2TX * 4) - half;
     const int ly0 = blockIdx.y * kD2TY * kD2Rows;
     const int gy0 = ybeg + ly0 - half;
-    for (int idx = tid; idx < TWs * TH; idx += kD2TX * kD2TY) {
+    for (int idx = tid; idx < NT; idx += kD2TX * kD2TY) {
         const int r = idx / TWs, c = idx - r * TWs;
         const int gx = min(max(gx0 + c, 0), W - 1);
         const int gy = min(max(gy0 + r, 0), H - 1);
         tile[idx] = __ldg(img + size_t(gy) * W + gx);
     }
+    tile[NT] = tile[NT + 1] = tile[NT + 2] = 0;  // t4 tail (never sampled)
+    __syncthreads();
+    // phased layout: t4[ph * S4 + k] = bytes 4k+ph .. 4k+ph+3, so the windows a
+    // warp reads for one pair offset are 32 consecutive words (no conflicts)
+    const int S4 = NT >> 2;
+    for (int idx = tid; idx < NT; idx += kD2TX * kD2TY)
+        t4[(idx & 3) * S4 + (idx >> 2)] = uint32_t(tile[idx]) | (uint32_t(tile[idx + 1]) << 8) |
+                                          (uint32_t(tile[idx + 2]) << 16) | (uint32_t(tile[idx + 3]) << 24);
     __syncthreads();
     const int xq = blockIdx.x * (kD2TX * 4) + 4 * threadIdx.x;
-    // byte address of the thread's first pixel (row 0) inside the tile; the
-    // per-pair table holds word offsets relative to (base & ~3) for this
-    // block's alignment class
-    const int base = (threadIdx.y * kD2Rows + half) * TWs + 4 * threadIdx.x + half;
-    const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile) + (base >> 2);
+    const uint32_t* tb = t4 + ((threadIdx.y * kD2Rows + half) * TWs >> 2) + threadIdx.x;
     const int rowW = TWs >> 2;
     const int full = n >> 5;
     for (int w = 0; w < NW; ++w) {
@@ -175,28 +183,20 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
         if (cnt == 32) {
 #pragma unroll 8
             for (int k = 0; k < 32; ++k) {
-                const uint4 e = __ldg(ptab + 32 * w + k);  // {p word off, q word off, p sel, q sel}
+                const int2 e = __ldg(ptab + 32 * w + k);  // tile-relative offsets of p and q
 #pragma unroll
                 for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t* t = tw + r * rowW;
-                    const uint32_t p = __byte_perm(t[int(e.x)], t[int(e.x) + 1], e.z);
-                    const uint32_t q = __byte_perm(t[int(e.y)], t[int(e.y) + 1], e.w);
-                    const uint32_t f = bytes_gt(p, q);  // bit 7 of byte j: pixel j
+                    const uint32_t f = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]);  // bit 7 of byte j: pixel j
                     // pair k -> bit (k & 7) of byte lane j of acc[k >> 3]
-                    const int sh = 7 - (k & 7);
-                    acc[r][k >> 3] |= (f >> sh);
+                    acc[r][k >> 3] |= (f >> (7 - (k & 7)));
                 }
             }
         } else {
             for (int k = 0; k < cnt; ++k) {
-                const uint4 e = __ldg(ptab + 32 * w + k);
+                const int2 e = __ldg(ptab + 32 * w + k);
 #pragma unroll
                 for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t* t = tw + r * rowW;
-                    const uint32_t p = __byte_perm(t[int(e.x)], t[int(e.x) + 1], e.z);
-                    const uint32_t q = __byte_perm(t[int(e.y)], t[int(e.y) + 1], e.w);
-                    const uint32_t f = bytes_gt(p, q);
-                    const uint32_t v = f >> (7 - (k & 7));
+                    const uint32_t v = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]) >> (7 - (k & 7));
                     switch (k >> 3) {
                         case 0: acc[r][0] |= v; break;
                         case 1: acc[r][1] |= v; break;
@@ -1506,22 +1506,22 @@ int check_launch(bsm_ctx* c, const char* what) {
 // Tile-relative offset tables depend on the staged tile width.
 int desc4_tile_width(int half) { return round_up(kD2TX * 4 + 2 * half + 8, 16); }
 
-// k_descriptor4's per-pair table: word offsets (relative to the thread's
-// aligned base word) and PRMT selectors of both endpoints.
+// k_descriptor4's per-pair table: word offsets of both endpoints in its
+// phased 4-byte-window tile, relative to the thread's base word:
+// (half + px) % 4 selects the phase plane, py*TWs/4 + (half + px)/4 the word.
 int ensure_desc4_table(bsm_ctx* c) {
     const int TWs = desc4_tile_width(c->half);
     if (c->desc4_tw == TWs) return BSM_OK;
     const int G = (c->n + 31) / 32;
-    std::vector<uint4> t(size_t(G) * 32, make_uint4(0, 0, 0, 0));
-    const int a0 = c->half & 3;  // every thread's base byte is congruent to half (mod 4)
+    std::vector<int2> t(size_t(G) * 32, make_int2(0, 0));
     for (int i = 0; i < c->n; ++i) {
         const int16_t* p = &c->pairs[4 * size_t(i)];
-        const int op = a0 + p[1] * TWs + p[0], oq = a0 + p[3] * TWs + p[2];
-        auto sel = [](int r) { return uint32_t(r | ((r + 1) << 4) | ((r + 2) << 8) | ((r + 3) << 12)); };
-        t[size_t(i)] = make_uint4(uint32_t(op >> 2), uint32_t(oq >> 2), sel(op & 3), sel(oq & 3));
+        const int TH = kD2TY * kD2Rows + 2 * c->half, S4 = TWs * TH / 4;
+        auto woff = [&](int px, int py) { return ((c->half + px) & 3) * S4 + py * (TWs / 4) + ((c->half + px) >> 2); };
+        t[size_t(i)] = make_int2(woff(p[0], p[1]), woff(p[2], p[3]));
     }
-    BSM_TRY(c->d_desc4.ensure(t.size() * sizeof(uint4)));
-    BSM_CUDA(cudaMemcpy(c->d_desc4.p, t.data(), t.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+    BSM_TRY(c->d_desc4.ensure(t.size() * sizeof(int2)));
+    BSM_CUDA(cudaMemcpy(c->d_desc4.p, t.data(), t.size() * sizeof(int2), cudaMemcpyHostToDevice));
     c->desc4_tw = TWs;
     return BSM_OK;
 }
@@ -1607,10 +1607,10 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         Scope s(c, T_DESC);
         BSM_TRY(ensure_desc4_table(c));
         const int TWs = desc4_tile_width(c->half);
-        const size_t sm = size_t(TWs) * (kD2TY * kD2Rows + 2 * c->half);
+        const size_t sm = size_t(TWs) * (kD2TY * kD2Rows + 2 * c->half) * 5 + 16;
         dim3 grid(Wp / (kD2TX * 4), (rows + kD2TY * kD2Rows - 1) / (kD2TY * kD2Rows));
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<uint4>(),
+        k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<int2>(),
                                                                     c->n, c->half, TWs, c->NW, Wp, desc);
         BSM_TRY(check_launch(c, "descriptor"));
     }
