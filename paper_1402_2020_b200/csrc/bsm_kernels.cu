@@ -173,7 +173,10 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
     const uint32_t* tb = t4 + ((threadIdx.y * kD2Rows + half) * TWs >> 2) + threadIdx.x;
     const int rowW = TWs >> 2;
     const int full = n >> 5;
-    for (int w = 0; w < NW; ++w) {
+    // blockIdx.z splits the word range (small images: more CTAs than SMs)
+    const int wper = (NW + gridDim.z - 1) / gridDim.z;
+    const int wbeg = blockIdx.z * wper, wend = min(NW, wbeg + wper);
+    for (int w = wbeg; w < wend; ++w) {
         uint32_t acc[kD2Rows][4];
 #pragma unroll
         for (int r = 0; r < kD2Rows; ++r)
@@ -1609,6 +1612,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         const int TWs = desc4_tile_width(c->half);
         const size_t sm = size_t(TWs) * (kD2TY * kD2Rows + 2 * c->half) * 5 + 16;
         dim3 grid(Wp / (kD2TX * 4), (rows + kD2TY * kD2Rows - 1) / (kD2TY * kD2Rows));
+        grid.z = unsigned(std::max(1, std::min((c->NW + 7) / 8, (4 * c->sm_count + int(grid.x * grid.y) - 1) /
+                                                                    int(grid.x * grid.y))));
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<int2>(),
                                                                     c->n, c->half, TWs, c->NW, Wp, desc);
