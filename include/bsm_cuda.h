@@ -153,10 +153,9 @@ int bsm_measure_word_peaks(bsm_ctx* ctx, double* popc_words_per_s, double* csa_w
  * n arguments (validation / tests). */
 int bsm_device_exp(bsm_ctx* ctx, const double* x, int n, double* out);
 /* Refinement kernel choice (all bit-identical): -1 = auto (3 for grayscale,
- * 4 for Lab planes); 0 = per-bin window scans, device exp; 1 = thread-per-pixel
- * shared-memory bins, device exp; 2 = warp per pixel, host weight table;
- * 3 = four pixels per warp ordered fold, host weight table (grayscale only);
- * 4 = the same fold with the device exp. */
+ * 4 for Lab planes); 2 = warp per pixel, exact host weight table (grayscale);
+ * 3 = four pixels per warp, ordered fold, host weight table (grayscale);
+ * 4 = the same fold with the device restatement of libm's exp. */
 int bsm_set_refine_mode(bsm_ctx* ctx, int mode);
 
 #ifdef __cplusplus

@@ -190,7 +190,7 @@ class Context:
         return float(v.value)
 
     def set_refine_mode(self, mode: int) -> None:
-        """0: per-bin window scans (default), 1: shared-memory bins, 2: host weight table."""
+        """-1 auto, 2 warp per pixel + host weight table, 3 ordered fold + table, 4 fold + device exp."""
         check(lib().bsm_set_refine_mode(self.handle, int(mode)))
 
     def device_exp(self, x) -> np.ndarray:

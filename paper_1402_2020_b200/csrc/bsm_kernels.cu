@@ -48,79 +48,6 @@ constexpr int kCostStages = 3;
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // ---------------------------------------------------------------------------
-// K1 -- descriptor.  descriptor.hpp:95-105 (border), :214-219/:226-230
-// (interior), pack_bits :83-93.  Thread per pixel column, PY rows per thread;
-// the CTA stages its (32 + 2h) x (8*PY + 2h) image window (coordinates clamped
-// exactly like clamp_coord, image.hpp:148-150) in shared memory, so every
-// sample of a warp is one 32-byte conflict-free LDS.  Pair offsets are
-// warp-uniform (broadcast).  Gray values are compared as uint8: the gray
-// conversion table is strictly increasing (checked at context creation), so
-// I(p) > I(q) on floats is the same predicate.
-// Output word w of pixel (x, y): bit k = pair 32w + k.
-constexpr int kDescTX = 32, kDescTY = 8, kDescPY = 4;
-
-__global__ void __launch_bounds__(kDescTX* kDescTY)
-    k_descriptor(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
-                 int n, int half, int NW, int Wp, uint32_t* __restrict__ desc) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int TW = kDescTX + 2 * half;
-    const int TH = kDescTY * kDescPY + 2 * half;
-    int2* s_off = reinterpret_cast<int2*>(smem);
-    uint8_t* tile = smem + size_t(n) * sizeof(int2);
-    const int tid = threadIdx.y * kDescTX + threadIdx.x;
-    const int gx0 = blockIdx.x * kDescTX - half;
-    const int ly0 = blockIdx.y * kDescTY * kDescPY;  // local row of the CTA's first pixel
-    const int gy0 = ybeg + ly0 - half;
-    for (int i = tid; i < n; i += kDescTX * kDescTY) {
-        // tile-relative offset of each endpoint (dy*TW + dx)
-        const int2 o = offs[i];
-        s_off[i] = make_int2(o.x, o.y);
-    }
-    for (int idx = tid; idx < TW * TH; idx += kDescTX * kDescTY) {
-        const int r = idx / TW, c = idx - r * TW;
-        const int gx = min(max(gx0 + c, 0), W - 1);
-        const int gy = min(max(gy0 + r, 0), H - 1);
-        tile[idx] = img[size_t(gy) * W + gx];
-    }
-    __syncthreads();
-
-    const int x = blockIdx.x * kDescTX + threadIdx.x;
-    const int base = (threadIdx.y * kDescPY + half) * TW + threadIdx.x + half;
-    const int full = n >> 5;
-    for (int w = 0; w < NW; ++w) {
-        uint32_t acc[kDescPY];
-#pragma unroll
-        for (int j = 0; j < kDescPY; ++j) acc[j] = 0;
-        if (w < full) {
-            const int2* o = s_off + 32 * w;
-#pragma unroll 8
-            for (int k = 0; k < 32; ++k) {
-                const int2 ok = o[k];
-#pragma unroll
-                for (int j = 0; j < kDescPY; ++j) {
-                    const uint8_t* t = tile + base + j * TW;
-                    acc[j] |= uint32_t(t[ok.x] > t[ok.y]) << k;
-                }
-            }
-        } else if (w == full && (n & 31)) {
-            for (int k = 0; k < (n & 31); ++k) {
-                const int2 ok = s_off[32 * w + k];
-#pragma unroll
-                for (int j = 0; j < kDescPY; ++j) {
-                    const uint8_t* t = tile + base + j * TW;
-                    acc[j] |= uint32_t(t[ok.x] > t[ok.y]) << k;
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kDescPY; ++j) {
-            const int ly = ly0 + threadIdx.y * kDescPY + j;
-            if (ly < rows) desc[(size_t(ly) * NW + w) * Wp + x] = acc[j];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K1' -- descriptor, four pixels per thread.  Same contract as k_descriptor.
 // A thread owns pixels x..x+3 (x % 4 == 0) of two rows; per pair it reads the
 // 4 p-samples and the 4 q-samples as two aligned words each plus one PRMT
@@ -881,59 +808,6 @@ __global__ void k_make_vmap(const float* __restrict__ cd, const uint8_t* __restr
     vmap[i] = cv[i] ? (g | (1u << 24) | uint32_t(llround(double(cd[i])))) : g;
 }
 
-__global__ void k_vote_refine_tpp(const uint32_t* __restrict__ vmap, int W, int rows, int radius,
-                                  const double* __restrict__ wtab, int ncol, const int16_t* __restrict__ s2col,
-                                  const int* __restrict__ counters, const int* __restrict__ inv,
-                                  float* __restrict__ od, uint8_t* __restrict__ ov) {
-    extern __shared__ __align__(16) double bins[];  // [nbins][blockDim.x]
-    const int NT = blockDim.x, t = threadIdx.x;
-    const int max_bin = counters[0];
-    const int n_inv = counters[1];
-    for (int idx = blockIdx.x * NT + t; idx < n_inv; idx += gridDim.x * NT) {
-        const int p = inv[idx];
-        const int y = p / W, x = p - y * W;
-        const int u = int((vmap[p] >> 16) & 0xFFu);
-        for (int b = 0; b <= max_bin; ++b) bins[b * NT + t] = 0.0;
-        const int tu = u * (u + 1) / 2;
-        bool any = false;
-        for (int dy = -radius; dy <= radius; ++dy) {
-            const int py = y + dy;
-            if (py < 0 || py >= rows) continue;
-            const uint32_t* row = vmap + size_t(py) * W;
-            const int dy2 = dy * dy;
-            const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
-#pragma unroll 4
-            for (int dx = dx0; dx <= dx1; ++dx) {
-                const uint32_t e = __ldg(row + x + dx);
-                if (e & (1u << 24)) {
-                    const int v = int((e >> 16) & 0xFFu);
-                    const int tri = v >= u ? (v * (v + 1) / 2 + u) : (tu + v);
-                    const double w = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
-                    double* bp = bins + int(e & 0xFFFFu) * NT + t;
-                    *bp += w;
-                    any = true;
-                }
-            }
-        }
-        if (!any) {
-            od[p] = 0.0f;
-            ov[p] = 0;
-            continue;
-        }
-        int best = 0;
-        double bv = bins[t];
-        for (int b = 1; b <= max_bin; ++b) {
-            const double v = bins[b * NT + t];
-            if (v > bv) {
-                bv = v;
-                best = b;
-            }
-        }
-        od[p] = float(best);
-        ov[p] = 1;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // K6'' -- voting refinement with device-computed weights.  vote_weight
 // (refine.hpp:30-35) = exp(-(double(lab_sad)/lc + sqrt(dx^2+dy^2)/le)):
@@ -990,185 +864,6 @@ __device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const uns
         if (y == 0.0) y = 0.0;
     }
     return __dmul_rn(y, 0x1p-1022);
-}
-
-// lab: per-pixel float Lab plane (3 floats / px), or nullptr to use lab256 of
-// the gray value carried in the voter map.
-__global__ void k_vote_refine_exp(const uint32_t* __restrict__ vmap, const float* __restrict__ lab,
-                                  const float* __restrict__ lab256, int W, int rows, int radius, double lc,
-                                  const double* __restrict__ e_over_le, ExpDev ep,
-                                  const unsigned long long* __restrict__ etab, const int* __restrict__ counters,
-                                  const int* __restrict__ inv, float* __restrict__ od, uint8_t* __restrict__ ov) {
-    extern __shared__ __align__(16) double dyn[];
-    unsigned long long* stab = reinterpret_cast<unsigned long long*>(dyn);  // 256
-    float* slab = reinterpret_cast<float*>(stab + 256);                     // 768
-    double* bins = reinterpret_cast<double*>(slab + 768);                   // [nbins][NT]
-    const int NT = blockDim.x, t = threadIdx.x;
-    for (int i = t; i < 256; i += NT) stab[i] = etab[i];
-    if (!lab)
-        for (int i = t; i < 768; i += NT) slab[i] = lab256[i];
-    __syncthreads();
-    const int max_bin = counters[0];
-    const int n_inv = counters[1];
-    for (int idx = blockIdx.x * NT + t; idx < n_inv; idx += gridDim.x * NT) {
-        const int p = inv[idx];
-        const int y = p / W, x = p - y * W;
-        float lx0, lx1, lx2;
-        if (lab) {
-            lx0 = lab[3 * size_t(p)];
-            lx1 = lab[3 * size_t(p) + 1];
-            lx2 = lab[3 * size_t(p) + 2];
-        } else {
-            const int u = int((vmap[p] >> 16) & 0xFFu);
-            lx0 = slab[3 * u];
-            lx1 = slab[3 * u + 1];
-            lx2 = slab[3 * u + 2];
-        }
-        for (int b = 0; b <= max_bin; ++b) bins[b * NT + t] = 0.0;
-        bool any = false;
-        for (int dy = -radius; dy <= radius; ++dy) {
-            const int py = y + dy;
-            if (py < 0 || py >= rows) continue;
-            const uint32_t* row = vmap + size_t(py) * W;
-            const int dy2 = dy * dy;
-            const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
-#pragma unroll 2
-            for (int dx = dx0; dx <= dx1; ++dx) {
-                const uint32_t e = __ldg(row + x + dx);
-                if (e & (1u << 24)) {
-                    float l0, l1, l2;
-                    if (lab) {
-                        const size_t q = 3 * (size_t(py) * W + x + dx);
-                        l0 = __ldg(lab + q);
-                        l1 = __ldg(lab + q + 1);
-                        l2 = __ldg(lab + q + 2);
-                    } else {
-                        const int v = int((e >> 16) & 0xFFu);
-                        l0 = slab[3 * v];
-                        l1 = slab[3 * v + 1];
-                        l2 = slab[3 * v + 2];
-                    }
-                    // lab_sad(at_x, at_p), image.hpp:144-146: (|dL| + |da|) + |db| in float
-                    const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
-                                                fabsf(__fsub_rn(lx2, l2)));
-                    const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
-                    double* bp = bins + int(e & 0xFFFFu) * NT + t;
-                    *bp += exp_glibc(arg, ep, stab);
-                    any = true;
-                }
-            }
-        }
-        if (!any) {
-            od[p] = 0.0f;
-            ov[p] = 0;
-            continue;
-        }
-        int best = 0;
-        double bv = bins[t];
-        for (int b = 1; b <= max_bin; ++b) {
-            const double v = bins[b * NT + t];
-            if (v > bv) {
-                bv = v;
-                best = b;
-            }
-        }
-        od[p] = float(best);
-        ov[p] = 1;
-    }
-}
-
-// K6c -- the same refinement without bin storage: bins are visited in
-// ascending order, one window scan per distinct voter bin; each scan adds the
-// weights of that bin's voters in row-major order (the reference's order) and
-// finds the next larger bin.  Argmax: best starts at bin 0 with its sum (0.0
-// if it has no voter) and moves only on a strictly larger sum -- exactly the
-// reference's loop over all bins 0..max_bin (unvisited bins hold 0.0).
-// Registers only, so occupancy is full; work = (#distinct bins) window scans
-// of 4-byte voter words + one weight per voter.
-__global__ void __launch_bounds__(256) k_vote_refine_scan(
-    const uint32_t* __restrict__ vmap, const float* __restrict__ lab, const float* __restrict__ lab256, int W,
-    int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
-    const unsigned long long* __restrict__ etab, const int* __restrict__ counters, const int* __restrict__ inv,
-    float* __restrict__ od, uint8_t* __restrict__ ov) {
-    __shared__ unsigned long long stab[256];
-    __shared__ float slab[768];
-    const int t = threadIdx.x;
-    for (int i = t; i < 256; i += blockDim.x) stab[i] = etab[i];
-    if (!lab)
-        for (int i = t; i < 768; i += blockDim.x) slab[i] = lab256[i];
-    __syncthreads();
-    const int n_inv = counters[1];
-    for (int idx = blockIdx.x * blockDim.x + t; idx < n_inv; idx += gridDim.x * blockDim.x) {
-        const int p = inv[idx];
-        const int y = p / W, x = p - y * W;
-        float lx0, lx1, lx2;
-        if (lab) {
-            lx0 = lab[3 * size_t(p)];
-            lx1 = lab[3 * size_t(p) + 1];
-            lx2 = lab[3 * size_t(p) + 2];
-        } else {
-            const int u = int((vmap[p] >> 16) & 0xFFu);
-            lx0 = slab[3 * u];
-            lx1 = slab[3 * u + 1];
-            lx2 = slab[3 * u + 2];
-        }
-        const int ya = max(0, y - radius), yb = min(rows - 1, y + radius);
-        const int dx0 = max(-radius, -x), dx1 = min(radius, W - 1 - x);
-        int cur = -1;          // bin accumulated by this scan (-1: discovery only)
-        int best = 0;
-        double bv = 0.0;       // bins[best]
-        bool any = false;
-        while (true) {
-            int next = 0x7FFFFFFF;
-            double sum = 0.0;
-            for (int py = ya; py <= yb; ++py) {
-                const uint32_t* row = vmap + size_t(py) * W + x;
-                const int dy2 = (py - y) * (py - y);
-                for (int dx = dx0; dx <= dx1; ++dx) {
-                    const uint32_t e = __ldg(row + dx);
-                    if (!(e & (1u << 24))) continue;
-                    const int b = int(e & 0xFFFFu);
-                    if (b > cur) {
-                        next = min(next, b);
-                    } else if (b == cur) {
-                        float l0, l1, l2;
-                        if (lab) {
-                            const size_t q = 3 * (size_t(py) * W + x + dx);
-                            l0 = __ldg(lab + q);
-                            l1 = __ldg(lab + q + 1);
-                            l2 = __ldg(lab + q + 2);
-                        } else {
-                            const int v = int((e >> 16) & 0xFFu);
-                            l0 = slab[3 * v];
-                            l1 = slab[3 * v + 1];
-                            l2 = slab[3 * v + 2];
-                        }
-                        const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
-                                                    fabsf(__fsub_rn(lx2, l2)));
-                        const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
-                        sum += exp_glibc(arg, ep, stab);
-                    }
-                }
-            }
-            if (cur >= 0) {
-                any = true;
-                if (cur == 0) bv = sum;
-                else if (sum > bv) {
-                    bv = sum;
-                    best = cur;
-                }
-            }
-            if (next == 0x7FFFFFFF) break;
-            cur = next;
-        }
-        if (!any) {
-            od[p] = 0.0f;
-            ov[p] = 0;
-        } else {
-            od[p] = float(best);
-            ov[p] = 1;
-        }
-    }
 }
 
 // K6d -- voting refinement, NP invalid pixels per warp (LPP = 32/NP lanes
@@ -1447,8 +1142,8 @@ struct bsm_ctx {
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
-    DevBuf d_desc_off, d_desc4, d_pq, d_pqb, d_uoff;
-    int desc_off_tw = -1, desc4_tw = -1, uoff_tw = -1;
+    DevBuf d_desc4, d_pq, d_pqb, d_uoff;
+    int desc4_tw = -1, uoff_tw = -1;
     // tables
     float gray_lut[256], lab_lut[768];
     DevBuf d_rank;
@@ -1529,19 +1224,6 @@ int ensure_desc4_table(bsm_ctx* c) {
     return BSM_OK;
 }
 
-int ensure_desc_offsets(bsm_ctx* c) {
-    const int TW = kDescTX + 2 * c->half;
-    if (c->desc_off_tw == TW) return BSM_OK;
-    std::vector<int2> o(size_t(c->n));
-    for (int i = 0; i < c->n; ++i) {
-        const int16_t* p = &c->pairs[4 * size_t(i)];
-        o[size_t(i)] = make_int2(p[1] * TW + p[0], p[3] * TW + p[2]);
-    }
-    BSM_TRY(c->d_desc_off.ensure(o.size() * sizeof(int2)));
-    BSM_CUDA(cudaMemcpy(c->d_desc_off.p, o.data(), o.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    c->desc_off_tw = TW;
-    return BSM_OK;
-}
 
 int ensure_mask_offsets(bsm_ctx* c, int tile_px) {
     const int TW = tile_px + 2 * c->half;
@@ -1583,10 +1265,6 @@ int check_pattern(bsm_ctx* c) {
     return BSM_OK;
 }
 
-size_t desc_smem(const bsm_ctx* c) {
-    const int TW = kDescTX + 2 * c->half, TH = kDescTY * kDescPY + 2 * c->half;
-    return size_t(c->n) * sizeof(int2) + size_t(TW) * TH;
-}
 
 size_t mask_smem(const bsm_ctx* c) {
     const int TW = kMaskTile + 2 * c->half, TH = 2 * c->half + 1, G = (c->n + 31) / 32;
@@ -1604,7 +1282,6 @@ size_t mask4_smem(const bsm_ctx* c) {
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
     const int Wp = round_up(W, 128);
-    BSM_TRY(ensure_desc_offsets(c));
     BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? kM3Px : kMaskTile));
     {
         Scope s(c, T_DESC);
@@ -1683,58 +1360,40 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
     const size_t px = size_t(rows) * W;
     const int nbins = round_up(std::max(nbins_max, 1), 32);
     const int tb = 256;
-    const int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 4 : 3);
-    if (mode == 3 || (mode == 4 && c->exp_ok)) {
-        constexpr int NPX = 4;
+    int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 4 : 3);
+    if (lab && mode != 4) mode = 4;  // Lab planes: the weight table only covers gray pairs
+    if (mode == 4 && !c->exp_ok) {
+        if (lab) return set_err(BSM_UNSUPPORTED, "bsm: colour refine needs the device exp (" + c->exp_why + ")");
+        mode = 3;
+    }
+    if (mode == 3 || mode == 4) {
         const bool devexp = mode == 4;
-        if (devexp) BSM_TRY(ensure_elam(c, le, radius));
-        else BSM_TRY(ensure_weight_table(c, lc, le, radius));
-        BSM_TRY(c->vmap.ensure(px * 4));
-        k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
-        BSM_TRY(check_launch(c, "make_vmap"));
-        const int warps = 8;
-        const size_t sm = 256 * 8 + 768 * 4 + size_t(warps) * 32 * 12 + size_t(warps) * NPX * nbins * 8;
-        auto kern = devexp ? k_vote_refine_fold<NPX, true> : k_vote_refine_fold<NPX, false>;
-        BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
-        kern<<<c->sm_count * per_sm, warps * 32, sm, c->stream>>>(
-            c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
-            c->exp_dev, c->d_etab.as<unsigned long long>(), c->d_wtab.as<double>(), c->wt_ncol,
-            c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(),
-            c->ref_v.as<uint8_t>());
-        return check_launch(c, "vote_refine_fold");
-    }
-    if (c->exp_ok && mode == 0) {
-        BSM_TRY(ensure_elam(c, le, radius));
-        BSM_TRY(c->vmap.ensure(px * 4));
-        k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
-        BSM_TRY(check_launch(c, "make_vmap"));
-        k_vote_refine_scan<<<c->sm_count * 8, 256, 0, c->stream>>>(
-            c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
-            c->exp_dev, c->d_etab.as<unsigned long long>(), c->counters.as<int>(), c->inv.as<int>(),
-            c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
-        return check_launch(c, "vote_refine_scan");
-    }
-    if (c->exp_ok && mode == 1) {
         const size_t fixed = 256 * 8 + 768 * 4;
-        int nt = int((200 * 1024 - fixed) / (size_t(nbins) * 8)) / 32 * 32;
-        if (nt >= 32) {
-            nt = std::min(nt, 256);
-            BSM_TRY(ensure_elam(c, le, radius));
+        // bins of NP pixels per warp: 4 (default) or 1 for very wide disparity ranges
+        const int np = (fixed + 8 * 32 * 12 + size_t(8) * 4 * nbins * 8 <= 200 * 1024) ? 4 : 1;
+        const int warps =
+            std::min(8, int((200 * 1024 - fixed) / (size_t(32) * 12 + size_t(np) * nbins * 8)));
+        if (warps >= 1) {
+            if (devexp) BSM_TRY(ensure_elam(c, le, radius));
+            else BSM_TRY(ensure_weight_table(c, lc, le, radius));
             BSM_TRY(c->vmap.ensure(px * 4));
             k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
             BSM_TRY(check_launch(c, "make_vmap"));
-            const size_t sm = fixed + size_t(nbins) * nt * 8;
-            BSM_CUDA(cudaFuncSetAttribute(k_vote_refine_exp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            const int per_sm = std::max(1, int((220 * 1024) / sm));
-            k_vote_refine_exp<<<c->sm_count * per_sm, nt, sm, c->stream>>>(
+            const size_t sm = fixed + size_t(warps) * 32 * 12 + size_t(warps) * np * nbins * 8;
+            auto kern = np == 4 ? (devexp ? k_vote_refine_fold<4, true> : k_vote_refine_fold<4, false>)
+                                : (devexp ? k_vote_refine_fold<1, true> : k_vote_refine_fold<1, false>);
+            BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
+            kern<<<c->sm_count * per_sm, warps * 32, sm, c->stream>>>(
                 c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
-                c->exp_dev, c->d_etab.as<unsigned long long>(), c->counters.as<int>(), c->inv.as<int>(),
-                c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
-            return check_launch(c, "vote_refine_exp");
+                c->exp_dev, c->d_etab.as<unsigned long long>(), c->d_wtab.as<double>(), c->wt_ncol,
+                c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(),
+                c->ref_v.as<uint8_t>());
+            return check_launch(c, "vote_refine_fold");
         }
+        if (lab) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too wide for the colour refine bins");
     }
-    if (lab) return set_err(BSM_UNSUPPORTED, "bsm: colour refine needs the device exp (" + c->exp_why + ")");
+    // mode 2 (or bins too wide for the fold): warp per pixel, exact host weight table
     BSM_TRY(ensure_weight_table(c, lc, le, radius));
     const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
     const size_t sm = size_t(warps) * nbins * 8;
@@ -1951,7 +1610,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_desc_off, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
@@ -2056,10 +1715,9 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
-    c->desc_off_tw = -1;
     c->desc4_tw = -1;
     c->uoff_tw = -1;
-    if (desc_smem(c) > 200 * 1024 || mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024)
+    if (mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
 }
@@ -2325,7 +1983,8 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
 }
 
 int bsm_set_refine_mode(bsm_ctx* c, int mode) {
-    if (!c || mode < -1 || mode > 4) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad refine mode");
+    if (!c || mode < -1 || mode > 4 || mode == 0 || mode == 1)
+        return set_err(BSM_INVALID_ARGUMENT, "bsm: bad refine mode");
     c->refine_mode = mode;
     return BSM_OK;
 }
