@@ -78,6 +78,15 @@ inline DescriptorField field_u8(const std::vector<uint8_t>& img, int W, int H, c
     throw_status(bsm_compute_field_u8(ctx.get(), img.data(), W, H, f.descriptor_data(), f.mask_data()));
     return f;
 }
+// Arbitrary float planes (colour views): the float-plane kernels (n <= 4096).
+inline DescriptorField field_f32(const float* gray, const float* lab, int W, int H, const SamplingPattern& pat) {
+    static_assert(sizeof(Lab) == 3 * sizeof(float), "Lab must be three packed floats");
+    Context& ctx = context();
+    ctx.use_pattern(flat_pairs(pat), pat.n, pat.window);
+    DescriptorField f(W, H, pat.n);
+    throw_status(bsm_compute_field_f32(ctx.get(), gray, lab, W, H, f.descriptor_data(), f.mask_data()));
+    return f;
+}
 }  // namespace detail
 
 inline DescriptorField compute_field(const GrayImage& gray, const LabImage& lab, const SamplingPattern& pat,
@@ -86,7 +95,8 @@ inline DescriptorField compute_field(const GrayImage& gray, const LabImage& lab,
     if (gray.width != lab.width || gray.height != lab.height)
         throw DimensionMismatch("compute_field: gray/lab dimensions differ");
     const auto u8 = detail::u8_from_planes(&gray, &lab);
-    if (!u8) detail::colour_unsupported("compute_field");
+    if (!u8)
+        return detail::field_f32(gray.values.data(), &lab.values[0].l, gray.width, gray.height, pat);
     return detail::field_u8(*u8, gray.width, gray.height, pat);
 }
 
@@ -94,7 +104,10 @@ inline BitString compute_descriptor(const GrayImage& gray, const SamplingPattern
     if (x < 0 || x >= gray.width || y < 0 || y >= gray.height)
         throw InvalidArgument("compute_descriptor: pixel outside image");
     const auto u8 = detail::u8_from_planes(&gray, nullptr);
-    if (!u8) detail::colour_unsupported("compute_descriptor");
+    if (!u8) {
+        const std::vector<float> lab(gray.values.size() * 3, 0.0f);  // the mask is not read
+        return detail::field_f32(gray.values.data(), lab.data(), gray.width, gray.height, pat).descriptor_at(x, y);
+    }
     return detail::field_u8(*u8, gray.width, gray.height, pat).descriptor_at(x, y);
 }
 
@@ -102,7 +115,10 @@ inline BitString compute_mask(const LabImage& lab, const SamplingPattern& pat, i
     if (x < 0 || x >= lab.width || y < 0 || y >= lab.height)
         throw InvalidArgument("compute_mask: pixel outside image");
     const auto u8 = detail::u8_from_planes(nullptr, &lab);
-    if (!u8) detail::colour_unsupported("compute_mask");
+    if (!u8) {
+        const std::vector<float> gray(lab.values.size(), 0.0f);  // the descriptor is not read
+        return detail::field_f32(gray.data(), &lab.values[0].l, lab.width, lab.height, pat).mask_at(x, y);
+    }
     return detail::field_u8(*u8, lab.width, lab.height, pat).mask_at(x, y);
 }
 

@@ -155,11 +155,5 @@ inline std::optional<std::vector<uint8_t>> u8_from_planes(const GrayImage* gray,
     return v;
 }
 
-[[noreturn]] inline void colour_unsupported(const char* where) {
-    throw Error(std::string(where) +
-                ": colour (non-grayscale) input is not yet supported by the GPU path; "
-                "pass r = g = b images");
-}
-
 }  // namespace detail
 }  // namespace bsm

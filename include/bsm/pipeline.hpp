@@ -1,5 +1,5 @@
 // bsm/pipeline.hpp -- run_pipeline (reference pipeline.hpp:14-61): the fused
-// device pipeline behind one C-ABI call (bsm_pipeline_u8).
+// device pipeline behind one C-ABI call (bsm_pipeline_u8 / bsm_pipeline_rgb).
 #pragma once
 
 #include <optional>
@@ -29,8 +29,7 @@ inline PipelineResult run_pipeline(const RgbImage& left, const RgbImage& right, 
         throw DimensionMismatch("pipeline: left/right dimensions differ");
     cfg.validate();
     const auto L = detail::gray_view(left);
-    const auto R = detail::gray_view(right);
-    if (!L || !R) detail::colour_unsupported("run_pipeline");
+    const auto R = L ? detail::gray_view(right) : std::nullopt;
     detail::Context& ctx = detail::context();
     ctx.use_pattern(detail::flat_pairs(pattern), pattern.n, pattern.window);
     const int W = left.width, H = left.height;
@@ -40,7 +39,13 @@ inline PipelineResult run_pipeline(const RgbImage& left, const RgbImage& right, 
     bsm_maps m{res.refined.disparity.data(), res.refined.valid.data(), res.left_wta.disparity.data(),
                res.right_wta.disparity.data(), res.checked.disparity.data(), res.checked.valid.data(),
                want_unmasked ? res.unmasked->disparity.data() : nullptr};
-    detail::throw_status(bsm_pipeline_u8(ctx.get(), L->data(), R->data(), W, H, &p, want_unmasked ? 1 : 0, &m));
+    if (L && R) {
+        detail::throw_status(bsm_pipeline_u8(ctx.get(), L->data(), R->data(), W, H, &p, want_unmasked ? 1 : 0, &m));
+    } else {  // colour: interleaved RGB through the exact 2^24-colour tables
+        static_assert(sizeof(Rgb8) == 3, "Rgb8 must be three packed bytes");
+        detail::throw_status(bsm_pipeline_rgb(ctx.get(), &left.pixels[0].r, &right.pixels[0].r, W, H, &p,
+                                              want_unmasked ? 1 : 0, &m));
+    }
     return res;
 }
 

@@ -47,8 +47,14 @@ inline DisparityMap vote_refine(const DisparityMap& map, const LabImage& lab, co
         throw DimensionMismatch("vote_refine: map/image dimensions differ");
     params.validate();
     const auto u8 = detail::u8_from_planes(nullptr, &lab);
-    if (!u8) detail::colour_unsupported("vote_refine");
     DisparityMap out(map.width, map.height);
+    if (!u8) {
+        detail::throw_status(bsm_vote_refine_lab(detail::context().get(), map.disparity.data(), map.valid.data(),
+                                                 &lab.values[0].l, map.width, map.height, params.lambda_c,
+                                                 params.lambda_e, params.vote_radius, out.disparity.data(),
+                                                 out.valid.data()));
+        return out;
+    }
     detail::throw_status(bsm_vote_refine_u8(detail::context().get(), map.disparity.data(), map.valid.data(),
                                             u8->data(), map.width, map.height, params.lambda_c, params.lambda_e,
                                             params.vote_radius, out.disparity.data(), out.valid.data()));

@@ -107,6 +107,19 @@ int bsm_vote_refine_u8(bsm_ctx* ctx, const float* d, const uint8_t* v, const uin
 int bsm_vote_refine_lab(bsm_ctx* ctx, const float* d, const uint8_t* v, const float* lab, int W, int H,
                         double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v);
 
+/* compute_field (descriptor.hpp:200-239) of arbitrary float planes (a
+ * GrayImage and a LabImage, e.g. of a colour view); n <= 4096. */
+int bsm_compute_field_f32(bsm_ctx* ctx, const float* gray, const float* lab, int W, int H, uint64_t* desc,
+                          uint64_t* mask);
+
+/* run_pipeline (pipeline.hpp:25-56) of a colour pair: interleaved RGB, 3 bytes
+ * per pixel (to_gray / to_lab through exact 2^24-entry tables). */
+int bsm_pipeline_rgb(bsm_ctx* ctx, const uint8_t* left_rgb, const uint8_t* right_rgb, int W, int H,
+                     const bsm_params* params, int want_unmasked, bsm_maps* out);
+
+/* to_gray / to_lab of all 2^24 colours, index (r<<16)|(g<<8)|b (host). */
+int bsm_rgb24_tables(float* gray16M, float* lab48M);
+
 /* run_pipeline (pipeline.hpp:25-56) of a grayscale pair (r=g=b), host buffers. */
 int bsm_pipeline_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H,
                     const bsm_params* params, int want_unmasked, bsm_maps* out);

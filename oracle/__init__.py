@@ -204,6 +204,21 @@ class Reference(_Lib):
             raise ValueError(self.err())
         return d, m
 
+    def compute_field(self, gray, lab, pairs, window, threads=1):
+        """compute_field (descriptor.hpp:200) of float gray / Lab planes."""
+        gray = np.ascontiguousarray(gray, np.float32)
+        lab = np.ascontiguousarray(lab, np.float32)
+        H, W = gray.shape
+        n = pairs.shape[0]
+        words = (n + 63) // 64
+        d = np.zeros((H, W, words), np.uint64)
+        m = np.zeros((H, W, words), np.uint64)
+        rc = self.f("compute_field", [_P, _P, _I, _I, _P, _I, _I, _I, _P, _P])(
+            _p(gray), _p(lab), W, H, _p(np.ascontiguousarray(pairs, np.int16)), n, window, threads, _p(d), _p(m))
+        if rc:
+            raise ValueError(self.err())
+        return d, m
+
     def quarter_threshold(self, w):
         w = np.ascontiguousarray(w, np.float32)
         return self.f("quarter_threshold", [_P, _I], C.c_float)(_p(w), len(w))

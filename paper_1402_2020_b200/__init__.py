@@ -253,6 +253,29 @@ def to_gray_lab(rgb):
     return g, l
 
 
+def _rgb(img, name="image") -> np.ndarray:
+    a = np.ascontiguousarray(img)
+    if a.dtype != np.uint8 or a.ndim != 3 or a.shape[2] != 3:
+        raise InvalidArgument(f"bsm: {name} must be a 2-D uint8 grayscale or (H, W, 3) uint8 RGB array")
+    if a.shape[0] < 1 or a.shape[1] < 1:
+        raise InvalidArgument("bsm: image dimensions must be >= 1")
+    return a
+
+
+def _view(img, name="image") -> np.ndarray:
+    """A grayscale (H, W) or RGB (H, W, 3) uint8 view."""
+    a = np.asarray(img)
+    return _rgb(a, name) if a.ndim == 3 else _u8(a, name)
+
+
+def rgb24_tables():
+    """to_gray / to_lab of every 24-bit colour, index (r << 16) | (g << 8) | b."""
+    g = np.zeros(1 << 24, np.float32)
+    l = np.zeros((1 << 24, 3), np.float32)
+    check(lib().bsm_rgb24_tables(_ptr(g), _ptr(l)))
+    return g, l
+
+
 def _u8(img, name="image") -> np.ndarray:
     a = np.ascontiguousarray(img)
     if a.dtype != np.uint8 or a.ndim != 2:
@@ -265,19 +288,38 @@ def _u8(img, name="image") -> np.ndarray:
 # ---------------------------------------------------------------------------
 # Hot path
 def compute_field(img, pattern: SamplingPattern, threads: int = 1, ctx: Optional[Context] = None):
-    """compute_field (descriptor.hpp:200-239) of a grayscale view.
+    """compute_field (descriptor.hpp:200-239).
 
+    `img` is a grayscale uint8 view, an (H, W, 3) uint8 RGB view, or the
+    reference's own argument pair (gray (H, W) float32, lab (H, W, 3) float32).
     Returns (descriptors, masks), each (H, W, words64) uint64 in the
     reference's AoS layout (descriptor.hpp:48-50).
     """
-    a = _u8(img)
     ctx = ctx or default_context()
     ctx.set_pattern(pattern)
-    H, W = a.shape
     words = (pattern.n + 63) // 64
+    if isinstance(img, tuple):
+        if len(img) != 2:
+            raise InvalidArgument("bsm: compute_field expects (gray, lab) planes")
+        g = np.ascontiguousarray(img[0], dtype=np.float32)
+        lab = np.ascontiguousarray(img[1], dtype=np.float32)
+        if g.ndim != 2 or lab.ndim != 3 or lab.shape[2] != 3:
+            raise InvalidArgument("bsm: planes must be gray (H, W) and lab (H, W, 3)")
+        if lab.shape[:2] != g.shape:
+            raise DimensionMismatch("compute_field: gray/lab dimensions differ")
+    else:
+        a = _view(img)
+        if a.ndim == 2:
+            H, W = a.shape
+            desc = np.zeros((H, W, words), np.uint64)
+            mask = np.zeros((H, W, words), np.uint64)
+            check(lib().bsm_compute_field_u8(ctx.handle, _ptr(a), W, H, _ptr(desc), _ptr(mask)))
+            return desc, mask
+        g, lab = to_gray_lab(a)
+    H, W = g.shape
     desc = np.zeros((H, W, words), np.uint64)
     mask = np.zeros((H, W, words), np.uint64)
-    check(lib().bsm_compute_field_u8(ctx.handle, _ptr(a), W, H, _ptr(desc), _ptr(mask)))
+    check(lib().bsm_compute_field_f32(ctx.handle, _ptr(g), _ptr(lab), W, H, _ptr(desc), _ptr(mask)))
     return desc, mask
 
 
@@ -365,11 +407,12 @@ def run_pipeline(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern]
                  outputs: str = "all") -> PipelineResult:
     """run_pipeline (pipeline.hpp:25-56, and the config overload :58-61).
 
+    Views are grayscale (H, W) uint8 or colour (H, W, 3) uint8 RGB.
     outputs='refined' downloads only the refined map (the others are None-filled
     with empty arrays) -- the end-to-end serving path.
     """
-    L = _u8(left, "left")
-    R = _u8(right, "right")
+    L = _view(left, "left")
+    R = _view(right, "right")
     if L.shape != R.shape:
         raise DimensionMismatch("pipeline: left/right dimensions differ")
     cfg.validate()
@@ -377,7 +420,7 @@ def run_pipeline(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern]
         pattern = generate_pattern(cfg=cfg)
     ctx = ctx or default_context()
     ctx.set_pattern(pattern)
-    H, W = L.shape
+    H, W = L.shape[:2]
     full = outputs == "all"
     mk = lambda dt: np.empty((H, W), dt)
     rd, rv = mk(np.float32), mk(np.uint8)
@@ -390,8 +433,8 @@ def run_pipeline(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern]
                     rwd.ctypes.data if rwd is not None else None, cd.ctypes.data if cd is not None else None,
                     cv.ctypes.data if cv is not None else None, ud.ctypes.data if ud is not None else None)
     p = _params(cfg)
-    check(lib().bsm_pipeline_u8(ctx.handle, _ptr(L), _ptr(R), W, H, C.byref(p), 1 if want_unmasked else 0,
-                                C.byref(maps)))
+    fn = lib().bsm_pipeline_rgb if L.ndim == 3 else lib().bsm_pipeline_u8
+    check(fn(ctx.handle, _ptr(L), _ptr(R), W, H, C.byref(p), 1 if want_unmasked else 0, C.byref(maps)))
     ones = np.ones((H, W), np.uint8)
     res = PipelineResult(
         refined=DisparityMap(rd, rv),

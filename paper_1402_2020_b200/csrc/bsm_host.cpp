@@ -73,9 +73,9 @@ namespace {
 // BT.601 luma in float, same expression shape as image.hpp:95.
 float luma(uint8_t r, uint8_t g, uint8_t b) { return 0.299f * float(r) + 0.587f * float(g) + 0.114f * float(b); }
 
-void lab_of(uint8_t R, uint8_t G, uint8_t B, float* out) {
-    const double r = decode(R / 255.0), g = decode(G / 255.0), b = decode(B / 255.0);
-    // sRGB -> XYZ (D65) normalised by the matrix row sums (image.hpp:113-115).
+// sRGB -> XYZ (D65) normalised by the matrix row sums (image.hpp:113-115),
+// then CIE Lab; r, g, b are the decoded linear channels.
+void lab_from_linear(double r, double g, double b, float* out) {
     const double X = (0.4124564 * r + 0.3575761 * g + 0.1804375 * b) / 0.9504700;
     const double Y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
     const double Z = (0.0193339 * r + 0.1191920 * g + 0.9503041 * b) / 1.0888300;
@@ -83,6 +83,10 @@ void lab_of(uint8_t R, uint8_t G, uint8_t B, float* out) {
     out[0] = float(std::clamp(116.0 * fy - 16.0, 0.0, 100.0));
     out[1] = float(500.0 * (fx - fy));
     out[2] = float(200.0 * (fy - fz));
+}
+
+void lab_of(uint8_t R, uint8_t G, uint8_t B, float* out) {
+    lab_from_linear(decode(R / 255.0), decode(G / 255.0), decode(B / 255.0), out);
 }
 }  // namespace
 
@@ -92,6 +96,30 @@ void gray_lab_lut(float* gray256, float* lab768) {
         gray256[v] = luma(c, c, c);
         lab_of(c, c, c, lab768 + 3 * v);
     }
+}
+
+void rgb24_tables(std::vector<float>& gray, std::vector<float>& lab) {
+    // Every colour through the very loop that converts images (to_gray_lab),
+    // so the FP contraction is the same as for per-pixel conversion.
+    gray.resize(size_t(1) << 24);
+    lab.resize(size_t(3) << 24);
+    auto work = [&](int r0, int r1) {
+        std::vector<uint8_t> rgb(size_t(3) << 16);
+        for (int r = r0; r < r1; ++r) {
+            for (int g = 0; g < 256; ++g)
+                for (int b = 0; b < 256; ++b) {
+                    uint8_t* p = &rgb[3 * ((size_t(g) << 8) | size_t(b))];
+                    p[0] = uint8_t(r);
+                    p[1] = uint8_t(g);
+                    p[2] = uint8_t(b);
+                }
+            to_gray_lab(rgb.data(), size_t(1) << 16, &gray[size_t(r) << 16], &lab[(size_t(r) << 16) * 3]);
+        }
+    };
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t) pool.emplace_back(work, int(256 * t / nt), int(256 * (t + 1) / nt));
+    for (auto& th : pool) th.join();
 }
 
 void to_gray_lab(const uint8_t* rgb, size_t npx, float* gray, float* lab) {

@@ -21,6 +21,10 @@ void gray_lab_lut(float* gray256, float* lab768);
 // Per-pixel to_gray / to_lab of interleaved RGB (image.hpp:90-140).
 void to_gray_lab(const uint8_t* rgb, size_t npx, float* gray, float* lab);
 
+// The same conversions for all 2^24 colours, index (r << 16) | (g << 8) | b
+// (gray: 64 MiB, Lab: 192 MiB); multithreaded, built once per context.
+void rgb24_tables(std::vector<float>& gray, std::vector<float>& lab);
+
 // rank[c*256 + v] = dense rank of lab_sad(Lab[c], Lab[v]) among the 256 values
 // of row c (equal values share a rank).  lab_sad: image.hpp:144-146.
 void sad_rank_table(const float* lab768, uint8_t* rank65536);

@@ -464,6 +464,193 @@ __global__ void __launch_bounds__(32, 16)
 }
 
 // ---------------------------------------------------------------------------
+// Colour / float-plane path (compute_field on arbitrary GrayImage + LabImage,
+// run_pipeline on RGB).  Same contracts as K1/K2 with float planes.
+//
+// k_rgb_planes: interleaved RGB -> gray (f32) and Lab (3 x f32) planes via the
+// host-built 2^24-entry conversion tables (bit-identical to the reference's
+// to_gray / to_lab, image.hpp:90-140).
+__global__ void k_rgb_planes(const uint8_t* __restrict__ rgb, size_t n, const float* __restrict__ gtab,
+                             const float* __restrict__ ltab, float* __restrict__ gray, float* __restrict__ lab) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = (uint32_t(rgb[3 * i]) << 16) | (uint32_t(rgb[3 * i + 1]) << 8) | uint32_t(rgb[3 * i + 2]);
+    gray[i] = __ldg(gtab + k);
+    lab[3 * i] = __ldg(ltab + 3 * size_t(k));
+    lab[3 * i + 1] = __ldg(ltab + 3 * size_t(k) + 1);
+    lab[3 * i + 2] = __ldg(ltab + 3 * size_t(k) + 2);
+}
+
+// K1f: descriptor bits I(p) > I(q) on a float gray plane (descriptor.hpp:95-105,
+// 214-230).  Thread per pixel column x 4 rows; clamped float tile.
+constexpr int kDfTX = 32, kDfTY = 8, kDfPY = 4;
+
+__global__ void __launch_bounds__(kDfTX* kDfTY)
+    k_descriptor_f32(const float* __restrict__ gray, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
+                     int n, int half, int NW, int Wp, uint32_t* __restrict__ desc) {
+    extern __shared__ __align__(16) float ftile[];
+    const int TW = kDfTX + 2 * half, TH = kDfTY * kDfPY + 2 * half;
+    const int tid = threadIdx.y * kDfTX + threadIdx.x;
+    const int gx0 = blockIdx.x * kDfTX - half;
+    const int ly0 = blockIdx.y * kDfTY * kDfPY;
+    const int gy0 = ybeg + ly0 - half;
+    for (int idx = tid; idx < TW * TH; idx += kDfTX * kDfTY) {
+        const int r = idx / TW, c = idx - r * TW;
+        ftile[idx] = __ldg(gray + size_t(min(max(gy0 + r, 0), H - 1)) * W + min(max(gx0 + c, 0), W - 1));
+    }
+    __syncthreads();
+    const int x = blockIdx.x * kDfTX + threadIdx.x;
+    const float* t0 = ftile + (threadIdx.y * kDfPY + half) * TW + threadIdx.x + half;
+    for (int w = 0; w < NW; ++w) {
+        uint32_t acc[kDfPY] = {0u, 0u, 0u, 0u};
+        const int cnt = min(32, max(0, n - 32 * w));
+        for (int k = 0; k < cnt; ++k) {
+            const int2 o = __ldg(offs + 32 * w + k);  // tile-relative (py*TW + px) of p and q
+#pragma unroll
+            for (int j = 0; j < kDfPY; ++j) acc[j] |= uint32_t(t0[j * TW + o.x] > t0[j * TW + o.y]) << k;
+        }
+#pragma unroll
+        for (int j = 0; j < kDfPY; ++j) {
+            const int ly = ly0 + threadIdx.y * kDfPY + j;
+            if (ly < rows) desc[(size_t(ly) * NW + w) * Wp + x] = acc[j];
+        }
+    }
+}
+
+// K2f: mask on a float Lab plane (descriptor.hpp:118-154, 64-76).  One warp
+// per CTA, kM3Px pixels per CTA, one pixel per pass.  The window SADs t[slot]
+// are kept as float bit patterns (non-negative floats order like u32); lane l
+// owns pairs 128l + 32m + t, forms a = max(t[P], t[Q]) for 32 pairs per chunk,
+// transposes the 32 words into 32 bit planes (5-stage in-register 32x32 bit
+// transpose), selects the k-th smallest MSB-first over 32 bits, and emits
+// bit = a <= T with a 32-plane comparator.
+__device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
+    // afterwards x[j] bit t = (original x[t]) bit j
+#pragma unroll
+    for (int sidx = 0; sidx < 5; ++sidx) {
+        const int sh = 16 >> sidx;
+        const uint32_t mk = sidx == 0 ? 0x0000FFFFu : sidx == 1 ? 0x00FF00FFu : sidx == 2 ? 0x0F0F0F0Fu
+                           : sidx == 3 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i & sh) continue;
+            const uint32_t t = ((x[i] >> sh) ^ x[i + sh]) & mk;
+            x[i + sh] ^= t;
+            x[i] ^= t << sh;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32, 8)
+    k_mask_f32(const float* __restrict__ lab, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
+               const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words, int half,
+               int NW, int Wp, uint32_t* __restrict__ mask) {
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
+    uint32_t* planes = tv + rho_words;                    // [32 planes][4 chunks][32 lanes]
+    float* ltile = reinterpret_cast<float*>(planes + 32 * 4 * 32);  // (2h+1) x (kM3Px + 2h) x 3
+    const int G = (n + 31) >> 5;
+    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
+    const int lane = threadIdx.x;
+    const int x0 = blockIdx.x * kM3Px;
+    const int ly = blockIdx.y;
+    const int y = ybeg + ly;
+    for (int idx = lane; idx < TW * TH; idx += 32) {
+        const int r = idx / TW, c = idx - r * TW;
+        const size_t g = size_t(min(max(y - half + r, 0), H - 1)) * W + min(max(x0 - half + c, 0), W - 1);
+        ltile[3 * idx] = __ldg(lab + 3 * g);
+        ltile[3 * idx + 1] = __ldg(lab + 3 * g + 1);
+        ltile[3 * idx + 2] = __ldg(lab + 3 * g + 2);
+    }
+    if (lane == 0) tv[u] = 0xFFFFFFFFu;  // sentinel: larger than every SAD
+    __syncwarp();
+    const int k = max(1, n / 4);
+    const unsigned full = 0xFFFFFFFFu;
+    const int rem = n & 31;
+#pragma unroll 1
+    for (int px = 0; px < kM3Px; ++px) {
+        const int ci = half * TW + half + px;
+        const float c0 = ltile[3 * ci], c1 = ltile[3 * ci + 1], c2 = ltile[3 * ci + 2];
+        for (int j = lane; j < u; j += 32) {
+            const int o = ci + __ldg(uoff + j);
+            // lab_sad(centre, window pixel), image.hpp:144-146
+            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(c0, ltile[3 * o])), fabsf(__fsub_rn(c1, ltile[3 * o + 1]))),
+                                        fabsf(__fsub_rn(c2, ltile[3 * o + 2])));
+            tv[j] = __float_as_uint(sad);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int m = 0; m < 4; ++m) {
+            uint32_t x[32];
+#pragma unroll
+            for (int t4 = 0; t4 < 8; ++t4) {
+                const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
+                x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
+                x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
+                x[4 * t4 + 3] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
+            }
+            transpose32(x);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) planes[(j * 4 + m) * 32 + lane] = x[j];
+        }
+        __syncwarp();
+        // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF)
+        uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u};
+        uint32_t T = 0;
+        int kk = k;
+#pragma unroll 1
+        for (int j = 31; j >= 0; --j) {
+            uint32_t pl[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) pl[m] = planes[(j * 4 + m) * 32 + lane];
+            const int zl = __popc(eq[0] & ~pl[0]) + __popc(eq[1] & ~pl[1]) + __popc(eq[2] & ~pl[2]) +
+                           __popc(eq[3] & ~pl[3]);
+            const int zeros = int(__reduce_add_sync(full, uint32_t(zl)));
+            if (zeros >= kk) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) eq[m] &= ~pl[m];
+            } else {
+                kk -= zeros;
+                T |= 1u << j;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) eq[m] &= pl[m];
+            }
+        }
+        // bit = a <= T
+        uint32_t lt[4] = {0u, 0u, 0u, 0u}, e2[4] = {~0u, ~0u, ~0u, ~0u};
+#pragma unroll 1
+        for (int j = 31; j >= 0; --j) {
+            uint32_t pl[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) pl[m] = planes[(j * 4 + m) * 32 + lane];
+            if ((T >> j) & 1u) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    lt[m] |= e2[m] & ~pl[m];
+                    e2[m] &= pl[m];
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) e2[m] &= ~pl[m];
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int w = 4 * lane + m;
+            if (w < NW) {
+                uint32_t v = lt[m] | e2[m];
+                if (w >= G) v = 0u;
+                else if (rem && w == G - 1) v &= (1u << rem) - 1u;
+                mask[(size_t(ly) * NW + w) * Wp + x0 + px] = v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
 // (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
 // :68-75 (ties -> smaller d).  No cost volume is materialised.
@@ -804,7 +991,7 @@ __global__ void k_make_vmap(const float* __restrict__ cd, const uint8_t* __restr
                             const uint8_t* __restrict__ gray, size_t n, uint32_t* __restrict__ vmap) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t g = uint32_t(gray[i]) << 16;
+    const uint32_t g = gray ? uint32_t(gray[i]) << 16 : 0u;
     vmap[i] = cv[i] ? (g | (1u << 24) | uint32_t(llround(double(cd[i])))) : g;
 }
 
@@ -1143,6 +1330,9 @@ struct bsm_ctx {
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
     DevBuf d_desc4, d_pq, d_pqb, d_uoff;
+    DevBuf d_descf, d_rgb_gray, d_rgb_lab, planes;
+    int descf_tw = -1;
+    bool rgb_ready = false;
     int desc4_tw = -1, uoff_tw = -1;
     // tables
     float gray_lut[256], lab_lut[768];
@@ -1419,8 +1609,83 @@ int validate_params(const bsm_params* p) {
 // The fused device pipeline.  Views are full W x H device images; the
 // refined output covers rows [out0, out0 + out_rows); fields, WTA and the
 // check cover the halo-extended rows [r0, r1).
-int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int H, int out0, int out_rows,
-                    const bsm_params* p, bool want_unmasked) {
+// k_descriptor_f32's per-pair table: tile-relative offsets py*TW + px.
+int ensure_descf_table(bsm_ctx* c) {
+    const int TW = kDfTX + 2 * c->half;
+    if (c->descf_tw == TW) return BSM_OK;
+    const int G = (c->n + 31) / 32;
+    std::vector<int2> t(size_t(G) * 32, make_int2(0, 0));
+    for (int i = 0; i < c->n; ++i) {
+        const int16_t* p = &c->pairs[4 * size_t(i)];
+        t[size_t(i)] = make_int2(p[1] * TW + p[0], p[3] * TW + p[2]);
+    }
+    BSM_TRY(c->d_descf.ensure(t.size() * sizeof(int2)));
+    BSM_CUDA(cudaMemcpy(c->d_descf.p, t.data(), t.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    c->descf_tw = TW;
+    return BSM_OK;
+}
+
+size_t maskf_smem(const bsm_ctx* c) {
+    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
+    return size_t(round_up(c->mslots + 1, 4)) * 4 + 32 * 4 * 32 * 4 + size_t(TW) * TH * 12;
+}
+
+// Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
+int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, int ybeg, int rows,
+                     uint32_t* desc, uint32_t* mask) {
+    if (c->n > 4096) return set_err(BSM_UNSUPPORTED, "bsm: float-plane (colour) fields support n <= 4096");
+    const int Wp = round_up(W, 128);
+    BSM_TRY(ensure_descf_table(c));
+    BSM_TRY(ensure_mask_offsets(c, kM3Px));
+    {
+        Scope s(c, T_DESC);
+        const int TW = kDfTX + 2 * c->half, TH = kDfTY * kDfPY + 2 * c->half;
+        const size_t sm = size_t(TW) * TH * 4;
+        dim3 grid(Wp / kDfTX, (rows + kDfTY * kDfPY - 1) / (kDfTY * kDfPY));
+        BSM_CUDA(cudaFuncSetAttribute(k_descriptor_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        k_descriptor_f32<<<grid, dim3(kDfTX, kDfTY), sm, c->stream>>>(gray, W, H, ybeg, rows, c->d_descf.as<int2>(),
+                                                                      c->n, c->half, c->NW, Wp, desc);
+        BSM_TRY(check_launch(c, "descriptor_f32"));
+    }
+    {
+        Scope s(c, T_MASK);
+        const size_t sm = maskf_smem(c);
+        BSM_CUDA(cudaFuncSetAttribute(k_mask_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        dim3 grid(Wp / kM3Px, rows);
+        k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
+                                                c->d_pqb.as<uint4>() + 3 * 1024, c->n, c->d_uoff.as<int32_t>(),
+                                                c->mslots, round_up(c->mslots + 1, 4), c->half, c->NW, Wp, mask);
+        BSM_TRY(check_launch(c, "mask_f32"));
+    }
+    return BSM_OK;
+}
+
+// The 2^24-colour conversion tables on the device (built once per context).
+int ensure_rgb_tables(bsm_ctx* c) {
+    if (c->rgb_ready) return BSM_OK;
+    std::vector<float> g, l;
+    bsmh::rgb24_tables(g, l);
+    BSM_TRY(c->d_rgb_gray.ensure(g.size() * 4));
+    BSM_TRY(c->d_rgb_lab.ensure(l.size() * 4));
+    BSM_CUDA(cudaMemcpy(c->d_rgb_gray.p, g.data(), g.size() * 4, cudaMemcpyHostToDevice));
+    BSM_CUDA(cudaMemcpy(c->d_rgb_lab.p, l.data(), l.size() * 4, cudaMemcpyHostToDevice));
+    c->rgb_ready = true;
+    return BSM_OK;
+}
+
+// Device views of a pair: grayscale uint8 images, or float gray + Lab planes
+// (colour input / arbitrary GrayImage + LabImage).
+struct Views {
+    const uint8_t* u8l = nullptr;
+    const uint8_t* u8r = nullptr;
+    const float* gl = nullptr;
+    const float* ll = nullptr;
+    const float* gr = nullptr;
+    const float* lr = nullptr;
+};
+
+int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_rows, const bsm_params* p,
+                    bool want_unmasked) {
     BSM_TRY(check_pattern(c));
     BSM_TRY(validate_params(p));
     const int r0 = std::max(0, out0 - p->vote_radius);
@@ -1446,8 +1711,13 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
     BSM_TRY(c->counters.ensure(64));
     BSM_TRY(c->inv.ensure(px * 4));
 
-    BSM_TRY(field_device(c, dl, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
-    BSM_TRY(field_device(c, dr, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
+    if (v.u8l) {
+        BSM_TRY(field_device(c, v.u8l, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
+        BSM_TRY(field_device(c, v.u8r, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
+    } else {
+        BSM_TRY(field_device_f32(c, v.gl, v.ll, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
+        BSM_TRY(field_device_f32(c, v.gr, v.lr, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
+    }
     BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(), W, rows, p->d_max,
                        false, true, c->keys_l.as<uint32_t>(), T_WTA_L));
     BSM_TRY(wta_device(c, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>(), c->fdl.as<uint32_t>(), W, rows, p->d_max,
@@ -1474,8 +1744,9 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
         Scope s(c, T_REFINE);
         BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
         BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
-        BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), dl + size_t(r0) * W, nullptr, W, rows,
-                              p->vote_radius, p->d_max, p->lambda_c, p->lambda_e));
+        BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), v.u8l ? v.u8l + size_t(r0) * W : nullptr,
+                              v.u8l ? nullptr : v.ll + size_t(3) * r0 * W, W, rows, p->vote_radius, p->d_max,
+                              p->lambda_c, p->lambda_e));
     }
     c->last_W = W;
     c->last_rows = rows;
@@ -1484,6 +1755,13 @@ int pipeline_device(bsm_ctx* c, const uint8_t* dl, const uint8_t* dr, int W, int
     c->last_out_rows = out_rows;
     c->last_unmasked = want_unmasked ? 1 : 0;
     return BSM_OK;
+}
+
+Views u8views(const uint8_t* l, const uint8_t* r) {
+    Views v;
+    v.u8l = l;
+    v.u8r = r;
+    return v;
 }
 
 int fetch(bsm_ctx* c, bsm_maps* o) {
@@ -1610,7 +1888,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
@@ -1716,8 +1994,9 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
     c->desc4_tw = -1;
+    c->descf_tw = -1;
     c->uoff_tw = -1;
-    if (mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024)
+    if (mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024 || (n <= 4096 && maskf_smem(c) > 200 * 1024))
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
 }
@@ -1880,7 +2159,7 @@ int bsm_pipeline_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W
     BSM_TRY(validate_params(params));
     if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
     BSM_TRY(upload_views(c, left, right, W, H));
-    BSM_TRY(pipeline_device(c, c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>(), W, H, 0, H, params,
+    BSM_TRY(pipeline_device(c, u8views(c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>()), W, H, 0, H, params,
                             want_unmasked != 0));
     BSM_TRY(fetch(c, out));
     return sync(c);
@@ -1892,7 +2171,7 @@ int bsm_pipeline_u8_device(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_r
     BSM_TRY(check_pattern(c));
     BSM_TRY(check_dims(W, H));
     if (!d_left || !d_right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
-    return pipeline_device(c, d_left, d_right, W, H, 0, H, params, want_unmasked != 0);
+    return pipeline_device(c, u8views(d_left, d_right), W, H, 0, H, params, want_unmasked != 0);
 }
 
 int bsm_fetch_maps(bsm_ctx* c, bsm_maps* out) {
@@ -1911,7 +2190,8 @@ int bsm_pipeline_band_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, 
     if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
     if (y0 < 0 || y1 > H || y0 >= y1) return set_err(BSM_INVALID_ARGUMENT, "bsm: band rows out of range");
     BSM_TRY(upload_views(c, left, right, W, H));
-    BSM_TRY(pipeline_device(c, c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>(), W, H, y0, y1 - y0, params, false));
+    BSM_TRY(pipeline_device(c, u8views(c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>()), W, H, y0, y1 - y0, params,
+                            false));
     bsm_maps m = {};
     m.refined_d = refined_d;
     m.refined_v = refined_v;
@@ -1997,7 +2277,7 @@ int bsm_pipeline_band_u8_device(bsm_ctx* c, const uint8_t* d_left, const uint8_t
     BSM_TRY(validate_params(params));
     if (!d_left || !d_right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
     if (y0 < 0 || y1 > H || y0 >= y1) return set_err(BSM_INVALID_ARGUMENT, "bsm: band rows out of range");
-    return pipeline_device(c, d_left, d_right, W, H, y0, y1 - y0, params, false);
+    return pipeline_device(c, u8views(d_left, d_right), W, H, y0, y1 - y0, params, false);
 }
 
 int bsm_result_device(bsm_ctx* c, const float** refined_d, const uint8_t** refined_v, int* row0, int* nrows) {
@@ -2019,6 +2299,82 @@ int bsm_copy_result_device(bsm_ctx* c, float* dst_d, uint8_t* dst_v) {
     if (dst_d) BSM_CUDA(cudaMemcpyAsync(dst_d, c->ref_d.as<float>() + off, n * 4, cudaMemcpyDeviceToDevice, c->stream));
     if (dst_v) BSM_CUDA(cudaMemcpyAsync(dst_v, c->ref_v.as<uint8_t>() + off, n, cudaMemcpyDeviceToDevice, c->stream));
     return BSM_OK;
+}
+
+int bsm_rgb24_tables(float* gray, float* lab) {
+    if (!gray || !lab) return set_err(BSM_INVALID_ARGUMENT, "bsm: null output pointer");
+    std::vector<float> g, l;
+    bsmh::rgb24_tables(g, l);
+    std::memcpy(gray, g.data(), g.size() * 4);
+    std::memcpy(lab, l.data(), l.size() * 4);
+    return BSM_OK;
+}
+
+int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, uint64_t* desc,
+                          uint64_t* mask) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    if (!gray || !lab) return set_err(BSM_INVALID_ARGUMENT, "bsm: null plane");
+    const size_t px = size_t(W) * H;
+    const int Wp = round_up(W, 128);
+    const size_t fbytes = size_t(H) * c->NW * Wp * 4;
+    BSM_TRY(c->planes.ensure(px * 16));
+    float* g = c->planes.as<float>();
+    float* l = g + px;
+    BSM_CUDA(cudaMemcpyAsync(g, gray, px * 4, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(l, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
+    BSM_TRY(c->fdl.ensure(fbytes));
+    BSM_TRY(c->fml.ensure(fbytes));
+    BSM_TRY(field_device_f32(c, g, l, W, H, 0, H, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
+    const size_t aos = size_t(H) * W * c->NW;
+    BSM_TRY(c->aux0.ensure(aos * 4));
+    const int tb = 256;
+    for (int which = 0; which < 2; ++which) {
+        uint64_t* dst = which == 0 ? desc : mask;
+        if (!dst) continue;
+        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(
+            which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H, c->NW, Wp, c->aux0.as<uint32_t>());
+        BSM_TRY(check_launch(c, "soa_to_aos"));
+        BSM_CUDA(cudaMemcpyAsync(dst, c->aux0.p, aos * 4, cudaMemcpyDeviceToHost, c->stream));
+        BSM_TRY(sync(c));
+    }
+    return sync(c);
+}
+
+int bsm_pipeline_rgb(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W, int H, const bsm_params* params,
+                     int want_unmasked, bsm_maps* out) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    BSM_TRY(ensure_rgb_tables(c));
+    const size_t px = size_t(W) * H;
+    BSM_TRY(c->img_l.ensure(px * 3));
+    BSM_TRY(c->img_r.ensure(px * 3));
+    BSM_TRY(c->planes.ensure(px * 32));
+    {
+        Scope s(c, T_H2D);
+        BSM_CUDA(cudaMemcpyAsync(c->img_l.p, left, px * 3, cudaMemcpyHostToDevice, c->stream));
+        BSM_CUDA(cudaMemcpyAsync(c->img_r.p, right, px * 3, cudaMemcpyHostToDevice, c->stream));
+    }
+    Views v;
+    float* base = c->planes.as<float>();
+    v.gl = base;
+    v.gr = base + px;
+    v.ll = base + 2 * px;
+    v.lr = base + 5 * px;
+    const int tb = 256;
+    k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->img_l.as<uint8_t>(), px, c->d_rgb_gray.as<float>(),
+                                                                  c->d_rgb_lab.as<float>(), base, base + 2 * px);
+    BSM_TRY(check_launch(c, "rgb_planes"));
+    k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->img_r.as<uint8_t>(), px, c->d_rgb_gray.as<float>(),
+                                                                  c->d_rgb_lab.as<float>(), base + px, base + 5 * px);
+    BSM_TRY(check_launch(c, "rgb_planes"));
+    BSM_TRY(pipeline_device(c, v, W, H, 0, H, params, want_unmasked != 0));
+    BSM_TRY(fetch(c, out));
+    return sync(c);
 }
 
 int bsm_stream(bsm_ctx* c, void** stream) {

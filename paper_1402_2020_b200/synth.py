@@ -65,3 +65,23 @@ def synth_pair(config: int, seed: int, width: int, height: int, with_gt: bool = 
 def workload_pair(key: str, index: int = 0, with_gt: bool = False):
     w = WORKLOADS[key]
     return synth_pair(w.config, w.seed + index, w.width, w.height, with_gt)
+
+
+def colour_pair(height: int, width: int, seed: int = 1):
+    """(left, right) (H, W, 3) uint8 RGB views of a synthetic colour pair.
+
+    The scene geometry is synth_pair's (configs[0] builder, disparities
+    below 60); each view's gray
+    level is mapped through three different tone curves and perturbed by
+    independent per-channel noise, so r, g and b differ everywhere and the
+    colour conversion is exercised on genuinely colour input.
+    """
+    left, right = synth_pair(0, seed, width, height)
+    v = np.arange(256, dtype=np.float64)
+    luts = np.stack([v, 255.0 * np.sqrt(v / 255.0), 255.0 - 0.8 * v]).round().astype(np.int32)
+    rng = np.random.default_rng(seed)
+    out = []
+    for img in (left, right):
+        c = np.stack([luts[k][img] for k in range(3)], axis=-1) + rng.integers(-6, 7, size=img.shape + (3,))
+        out.append(np.clip(c, 0, 255).astype(np.uint8))
+    return out[0], out[1]

@@ -2,7 +2,8 @@
 // against include/bsm/ (the drop-in C++ API over libbsm_cuda.so).
 //   shim_test host                    -- host-side checks, no device needed
 //   shim_test gpu L.raw R.raw W H D out.bin
-//                                     -- run_pipeline on a grayscale pair, maps to out.bin
+//                                     -- run_pipeline on a grayscale (W*H bytes) or RGB
+//                                        (3*W*H bytes) pair, maps to out.bin
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -82,13 +83,20 @@ static int host_checks() {
 
 static int gpu_run(const char* lpath, const char* rpath, int W, int H, int D, const char* out) {
     using namespace bsm;
-    std::vector<uint8_t> L(size_t(W) * H), R(size_t(W) * H);
-    std::ifstream(lpath, std::ios::binary).read(reinterpret_cast<char*>(L.data()), std::streamsize(L.size()));
-    std::ifstream(rpath, std::ios::binary).read(reinterpret_cast<char*>(R.data()), std::streamsize(R.size()));
+    // a W*H file is a grayscale view, a 3*W*H file interleaved RGB
+    std::ifstream lf(lpath, std::ios::binary | std::ios::ate), rf(rpath, std::ios::binary | std::ios::ate);
+    const size_t bytes = size_t(lf.tellg());
+    const int ch = bytes == size_t(3) * W * H ? 3 : 1;
+    std::vector<uint8_t> L(bytes), R(bytes);
+    lf.seekg(0);
+    rf.seekg(0);
+    lf.read(reinterpret_cast<char*>(L.data()), std::streamsize(bytes));
+    rf.read(reinterpret_cast<char*>(R.data()), std::streamsize(bytes));
     RgbImage left(W, H), right(W, H);
-    for (size_t i = 0; i < L.size(); ++i) {
-        left.pixels[i] = {L[i], L[i], L[i]};
-        right.pixels[i] = {R[i], R[i], R[i]};
+    for (size_t i = 0; i < size_t(W) * H; ++i) {
+        const size_t k = ch * i;
+        left.pixels[i] = {L[k], L[k + (ch - 1) / 2], L[k + ch - 1]};
+        right.pixels[i] = {R[k], R[k + (ch - 1) / 2], R[k + ch - 1]};
     }
     BsmConfig cfg;
     cfg.d_max = D;

@@ -49,11 +49,15 @@ def test_shim_no_cpu_fallback():
 
 
 @pytest.mark.gpu
-def test_shim_pipeline_matches_reference(tmp_path, ref, default_pairs):
-    from paper_1402_2020_b200.synth import workload_pair
-    left, right = workload_pair("c1")
-    L, R = left[140:180, 60:220].copy(), right[140:180, 60:220].copy()
-    H, W = L.shape
+@pytest.mark.parametrize("colour", [False, True])
+def test_shim_pipeline_matches_reference(tmp_path, ref, default_pairs, colour):
+    from paper_1402_2020_b200.synth import workload_pair, colour_pair
+    if colour:
+        L, R = colour_pair(40, 160, seed=5)
+    else:
+        left, right = workload_pair("c1")
+        L, R = left[140:180, 60:220].copy(), right[140:180, 60:220].copy()
+    H, W = L.shape[:2]
     (tmp_path / "l.raw").write_bytes(L.tobytes())
     (tmp_path / "r.raw").write_bytes(R.tobytes())
     out = subprocess.run([build(), "gpu", str(tmp_path / "l.raw"), str(tmp_path / "r.raw"), str(W), str(H), "60",
@@ -68,7 +72,7 @@ def test_shim_pipeline_matches_reference(tmp_path, ref, default_pairs):
         v = raw[off:off + W * H].reshape(H, W)
         off += W * H
         maps.append((d, v))
-    want = ref.pipeline(L, R, default_pairs, 26, 60, threads=8, want_unmasked=True)
+    want = ref.pipeline(L, R, default_pairs, 26, 60, threads=8, want_unmasked=True, channels=3 if colour else 1)
     assert np.array_equal(maps[0][0], want["refined_d"]) and np.array_equal(maps[0][1], want["refined_v"])
     assert np.array_equal(maps[1][0], want["left_d"])
     assert np.array_equal(maps[2][0], want["right_d"])

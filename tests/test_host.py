@@ -57,6 +57,18 @@ def test_rgb_conversion_matches_reference(ref):
     assert np.array_equal(l.view(np.uint32), l2.view(np.uint32))
 
 
+def test_rgb24_tables_match_reference_exhaustively(ref):
+    # every 24-bit colour, in 16 slices of 2^20 (index (r << 16) | (g << 8) | b)
+    g, l = bsm.rgb24_tables()
+    k = np.arange(1 << 20, dtype=np.uint32)
+    for s in range(16):
+        idx = k + (s << 20)
+        rgb = np.stack([(idx >> 16) & 255, (idx >> 8) & 255, idx & 255], axis=-1).astype(np.uint8)
+        g2, l2 = ref.to_gray_lab(rgb.reshape(1024, 1024, 3))
+        assert np.array_equal(g[idx].view(np.uint32), g2.reshape(-1).view(np.uint32)), s
+        assert np.array_equal(l[idx].view(np.uint32), l2.reshape(-1, 3).view(np.uint32)), s
+
+
 def test_pattern_errors():
     with pytest.raises(bsm.InvalidArgument, match="n must be >= 1"):
         bsm.generate_pattern(0)
