@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <random>
 #include <thread>
 
@@ -295,6 +296,144 @@ void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<
         for (int g : touched) mark[size_t(g)] = 0;
     }
     if (cost_after) *cost_after = double(total) / ng;
+}
+
+bool balanced_gather_order(const uint32_t* pq, int n, int u, std::vector<int>& slot, int& nslots,
+                           std::vector<int>& order, std::vector<uint8_t>& flip) {
+    constexpr int B = 32, STEPS = 128;
+    if (n != B * STEPS || u < B) return false;
+    // (1) offsets -> banks with exactly 2 * STEPS endpoint references per bank
+    //     and at most `cap` offsets per bank (rank-table rows).
+    std::vector<int> w(size_t(u), 0);
+    for (int i = 0; i < n; ++i) {
+        ++w[pq[i] & 0xFFFFu];
+        ++w[pq[i] >> 16];
+    }
+    const int target = 2 * STEPS;
+    for (int o = 0; o < u; ++o)
+        if (w[size_t(o)] > target) return false;
+    const int cap = (u + B - 1) / B + 1;
+    std::vector<int> ord(static_cast<size_t>(u));
+    for (int o = 0; o < u; ++o) ord[size_t(o)] = o;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return w[size_t(a)] > w[size_t(b)]; });
+    std::vector<int> bank(size_t(u), -1), sum(B, 0), cnt(B, 0);
+    for (int o : ord) {
+        int best = -1;
+        for (int b = 0; b < B; ++b)
+            if (cnt[size_t(b)] < cap && (best < 0 || sum[size_t(b)] < sum[size_t(best)])) best = b;
+        if (best < 0) return false;
+        bank[size_t(o)] = best;
+        sum[size_t(best)] += w[size_t(o)];
+        ++cnt[size_t(best)];
+    }
+    // local search: moves / swaps that reduce sum |sum_b - target|
+    std::mt19937_64 rng(777);
+    auto dev = [&](int b, int delta) { return std::abs(sum[size_t(b)] + delta - target); };
+    for (int it = 0; it < 2000000; ++it) {
+        bool done = true;
+        for (int b = 0; b < B; ++b)
+            if (sum[size_t(b)] != target) done = false;
+        if (done) break;
+        const int o1 = int(rng() % uint64_t(u)), b1 = bank[size_t(o1)];
+        const int b2 = int(rng() % uint64_t(B));
+        if (b2 == b1) continue;
+        if ((it & 1) && cnt[size_t(b2)] < cap) {  // move o1 -> b2
+            const int d0 = dev(b1, 0) + dev(b2, 0), d1 = dev(b1, -w[size_t(o1)]) + dev(b2, w[size_t(o1)]);
+            if (d1 < d0 || (d1 == d0 && (rng() & 1))) {
+                sum[size_t(b1)] -= w[size_t(o1)], sum[size_t(b2)] += w[size_t(o1)];
+                --cnt[size_t(b1)], ++cnt[size_t(b2)];
+                bank[size_t(o1)] = b2;
+            }
+        } else {  // swap o1 with a random offset of b2
+            int o2 = int(rng() % uint64_t(u));
+            for (int k = 0; k < u && bank[size_t(o2)] != b2; ++k) o2 = (o2 + 1) % u;
+            if (bank[size_t(o2)] != b2) continue;
+            const int dw = w[size_t(o2)] - w[size_t(o1)];
+            const int d0 = dev(b1, 0) + dev(b2, 0), d1 = dev(b1, dw) + dev(b2, -dw);
+            if (d1 < d0 || (d1 == d0 && (rng() & 1))) {
+                sum[size_t(b1)] += dw, sum[size_t(b2)] -= dw;
+                bank[size_t(o1)] = b2, bank[size_t(o2)] = b1;
+            }
+        }
+    }
+    for (int b = 0; b < B; ++b)
+        if (sum[size_t(b)] != target) return false;
+    // (2) Eulerian orientation of the bank multigraph (every degree is even):
+    //     closed walks give each bank STEPS outgoing (A) and STEPS incoming (B) ends.
+    std::vector<std::vector<int>> adj(B);
+    for (int i = 0; i < n; ++i) {
+        adj[size_t(bank[pq[i] & 0xFFFFu])].push_back(i);
+        adj[size_t(bank[pq[i] >> 16])].push_back(i);
+    }
+    std::vector<int> ptr(B, 0), from(static_cast<size_t>(n), -1);
+    for (int v0 = 0; v0 < B; ++v0) {
+        for (;;) {
+            int v = v0;
+            bool moved = false;
+            for (;;) {
+                auto& a = adj[size_t(v)];
+                while (ptr[size_t(v)] < int(a.size()) && from[size_t(a[size_t(ptr[size_t(v)])])] >= 0) ++ptr[size_t(v)];
+                if (ptr[size_t(v)] == int(a.size())) break;
+                const int e = a[size_t(ptr[size_t(v)])];
+                from[size_t(e)] = v;
+                const int bp = bank[pq[e] & 0xFFFFu], bq = bank[pq[e] >> 16];
+                v = bp == v ? bq : bp;
+                moved = true;
+            }
+            if (!moved || v != v0) {
+                if (v != v0) return false;  // cannot happen with even degrees
+                break;
+            }
+        }
+    }
+    // (3) split the STEPS-regular bipartite multigraph (A bank -> B bank) into
+    //     STEPS perfect matchings; step s, lane = A bank.
+    std::vector<std::vector<int>> ab(size_t(B) * B);
+    for (int i = 0; i < n; ++i) {
+        if (from[size_t(i)] < 0) return false;
+        const int bp = bank[pq[i] & 0xFFFFu], bq = bank[pq[i] >> 16];
+        const int a = from[size_t(i)], b = bp == a ? bq : bp;
+        ab[size_t(a) * B + b].push_back(i);
+    }
+    order.assign(static_cast<size_t>(n), -1);
+    flip.assign(static_cast<size_t>(n), 0);
+    for (int st = 0; st < STEPS; ++st) {
+        std::vector<int> match_b(B, -1);  // B bank -> A bank
+        for (int a = 0; a < B; ++a) {
+            std::vector<char> vis(B, 0);
+            std::function<bool(int)> aug = [&](int x) -> bool {
+                for (int y = 0; y < B; ++y) {
+                    if (ab[size_t(x) * B + y].empty() || vis[size_t(y)]) continue;
+                    vis[size_t(y)] = 1;
+                    if (match_b[size_t(y)] < 0 || aug(match_b[size_t(y)])) {
+                        match_b[size_t(y)] = x;
+                        return true;
+                    }
+                }
+                return false;
+            };
+            if (!aug(a)) return false;
+        }
+        for (int y = 0; y < B; ++y) {
+            const int x = match_b[size_t(y)];
+            const int i = ab[size_t(x) * B + y].back();
+            ab[size_t(x) * B + y].pop_back();
+            const int pos = 128 * x + st;  // lane x, chunk st / 32, bit st % 32
+            order[size_t(pos)] = i;
+            flip[size_t(pos)] = uint8_t(bank[pq[i] & 0xFFFFu] != x);  // P is not the lane's bank
+        }
+    }
+    // (4) slots: bank b's offsets take rows 0, 1, ... (slot = b + 32 * row)
+    slot.assign(static_cast<size_t>(u), -1);
+    std::vector<int> row(B, 0);
+    int rows = 0;
+    for (int o = 0; o < u; ++o) {
+        const int b = bank[size_t(o)];
+        slot[size_t(o)] = b + B * row[size_t(b)]++;
+        rows = std::max(rows, row[size_t(b)]);
+    }
+    nslots = B * rows;
+    return true;
 }
 
 }  // namespace bsmh

@@ -1229,6 +1229,24 @@ __global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int
     dst[i] = src[(size_t(y) * NW + w) * Wp + x];
 }
 
+// k_soa_to_aos with the pipeline's bit order undone: reference bit k of a
+// pixel's string is device bit pos[k].
+__global__ void k_soa_to_aos_perm(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+                                  const int* __restrict__ pos, int n, uint32_t* __restrict__ dst) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
+    const size_t total = size_t(H) * W * NW;
+    if (i >= total) return;
+    const int w = int(i % NW);
+    const size_t yx = i / NW;
+    const int x = int(yx % W), y = int(yx / W);
+    uint32_t v = 0;
+    for (int b = 0; b < 32 && 32 * w + b < n; ++b) {
+        const int j = __ldg(pos + 32 * w + b);
+        v |= ((__ldg(src + (size_t(y) * NW + (j >> 5)) * Wp + x) >> (j & 31)) & 1u) << b;
+    }
+    dst[i] = v;
+}
+
 __global__ void k_keys_to_float(const uint32_t* __restrict__ keys, size_t n, float* __restrict__ out) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) out[i] = float(keys[i] & 0xFFFFu);
@@ -1325,6 +1343,9 @@ struct bsm_ctx {
     int n = 0, window = 0, half = 0, NW = 0, u = 0, upad = 0;
     int mslots = 0;                 // rank-table slots used by the mask kernels
     std::vector<int> slot_used;     // slot -> used-offset index (-1: empty)
+    std::vector<int> order;         // bit position -> pair index (identity unless permuted)
+    bool permuted = false;
+    DevBuf d_pos;                   // pair index -> bit position (permuted only)
     double slot_cost[2] = {0, 0};   // avg wavefronts per gather before/after placement
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
@@ -1403,7 +1424,7 @@ int ensure_desc4_table(bsm_ctx* c) {
     const int G = (c->n + 31) / 32;
     std::vector<int2> t(size_t(G) * 32, make_int2(0, 0));
     for (int i = 0; i < c->n; ++i) {
-        const int16_t* p = &c->pairs[4 * size_t(i)];
+        const int16_t* p = &c->pairs[4 * size_t(c->order[size_t(i)])];
         const int TH = kD2TY * kD2Rows + 2 * c->half, S4 = TWs * TH / 4;
         auto woff = [&](int px, int py) { return ((c->half + px) & 3) * S4 + py * (TWs / 4) + ((c->half + px) >> 2); };
         t[size_t(i)] = make_int2(woff(p[0], p[1]), woff(p[2], p[3]));
@@ -1616,7 +1637,7 @@ int ensure_descf_table(bsm_ctx* c) {
     const int G = (c->n + 31) / 32;
     std::vector<int2> t(size_t(G) * 32, make_int2(0, 0));
     for (int i = 0; i < c->n; ++i) {
-        const int16_t* p = &c->pairs[4 * size_t(i)];
+        const int16_t* p = &c->pairs[4 * size_t(c->order[size_t(i)])];
         t[size_t(i)] = make_int2(p[1] * TW + p[0], p[3] * TW + p[2]);
     }
     BSM_TRY(c->d_descf.ensure(t.size() * sizeof(int2)));
@@ -1888,7 +1909,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
@@ -1963,13 +1984,37 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
     // Rank-table slot placement (k_mask4): minimise shared-memory bank
     // conflicts of the per-pair gathers; identity for the n > 4096 kernel.
+    // For n = 4096 a bank-balanced pair order (bsmh::balanced_gather_order)
+    // makes every gather conflict-free; the descriptor bits follow the same
+    // order (the masked Hamming cost is invariant under a common permutation
+    // of descriptor and mask bits) and the per-stage API un-permutes.
     std::vector<int> rslot(size_t(c->u));
+    std::vector<uint8_t> flip;
+    c->permuted = false;
     if (n <= 4096) {
-        c->mslots = round_up(c->u, 32) + 32;
-        bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, rslot, &c->slot_cost[0], &c->slot_cost[1]);
+        int ns = 0;
+        if (bsmh::balanced_gather_order(pq.data(), n, c->u, rslot, ns, c->order, flip)) {
+            c->permuted = true;
+            c->mslots = ns;
+            c->slot_cost[0] = c->slot_cost[1] = 1.0;
+        } else {
+            rslot.assign(size_t(c->u), 0);
+            c->mslots = round_up(c->u, 32) + 32;
+            bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, rslot, &c->slot_cost[0], &c->slot_cost[1]);
+        }
     } else {
         c->mslots = c->u;
         for (int o = 0; o < c->u; ++o) rslot[size_t(o)] = o;
+    }
+    if (!c->permuted) {
+        c->order.resize(size_t(n));
+        for (int i = 0; i < n; ++i) c->order[size_t(i)] = i;
+        flip.assign(size_t(n), 0);
+    } else {
+        std::vector<int> pos(static_cast<size_t>(n));
+        for (int j = 0; j < n; ++j) pos[size_t(c->order[size_t(j)])] = j;
+        BSM_TRY(c->d_pos.ensure(pos.size() * 4));
+        BSM_CUDA(cudaMemcpy(c->d_pos.p, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice));
     }
     c->slot_used.assign(size_t(c->mslots), -1);
     for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
@@ -1985,11 +2030,13 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     // k_mask4: lane-block order -- lane l, chunk m, t: pair 128l + 32m + t at
     // uint4 [(m*8 + t/4)*32 + l], component t%4.
     pqb.resize(4 * 4096, uint32_t(4 * c->mslots));  // pads -> sentinel slot mslots
-    for (int i = 0; i < std::min(n, 4096); ++i) {
-        const int l = i >> 7, m = (i >> 5) & 3, t = i & 31;
+    for (int j = 0; j < std::min(n, 4096); ++j) {
+        const int l = j >> 7, m = (j >> 5) & 3, t = j & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
-        pqb[2 * 4096 + at] = uint32_t(4 * rslot[size_t(pq[size_t(i)] & 0xFFFFu)]);
-        pqb[3 * 4096 + at] = uint32_t(4 * rslot[size_t(pq[size_t(i)] >> 16)]);
+        const uint32_t e = pq[size_t(c->order[size_t(j)])];
+        const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
+        pqb[2 * 4096 + at] = uint32_t(4 * rslot[size_t(a)]);
+        pqb[3 * 4096 + at] = uint32_t(4 * rslot[size_t(b)]);
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
@@ -1999,6 +2046,20 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     if (mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024 || (n <= 4096 && maskf_smem(c) > 200 * 1024))
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
+}
+
+// Device SoA field -> reference AoS words in c->aux0 (bit order restored).
+static int soa_to_aos(bsm_ctx* c, const uint32_t* src, int W, int H) {
+    const int Wp = round_up(W, 128), tb = 256;
+    const size_t aos = size_t(H) * W * c->NW;
+    if (c->permuted)
+        k_soa_to_aos_perm<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wp,
+                                                                              c->d_pos.as<int>(), c->n,
+                                                                              c->aux0.as<uint32_t>());
+    else
+        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wp,
+                                                                         c->aux0.as<uint32_t>());
+    return check_launch(c, "soa_to_aos");
 }
 
 int bsm_compute_field_u8(bsm_ctx* c, const uint8_t* img, int W, int H, uint64_t* desc, uint64_t* mask) {
@@ -2018,9 +2079,7 @@ int bsm_compute_field_u8(bsm_ctx* c, const uint8_t* img, int W, int H, uint64_t*
     for (int which = 0; which < 2; ++which) {
         uint64_t* dst = which == 0 ? desc : mask;
         if (!dst) continue;
-        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(
-            which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H, c->NW, Wp, c->aux0.as<uint32_t>());
-        BSM_TRY(check_launch(c, "soa_to_aos"));
+        BSM_TRY(soa_to_aos(c, which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H));
         BSM_CUDA(cudaMemcpyAsync(dst, c->aux0.p, aos * 4, cudaMemcpyDeviceToHost, c->stream));
         BSM_TRY(sync(c));
     }
@@ -2333,9 +2392,7 @@ int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W
     for (int which = 0; which < 2; ++which) {
         uint64_t* dst = which == 0 ? desc : mask;
         if (!dst) continue;
-        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(
-            which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H, c->NW, Wp, c->aux0.as<uint32_t>());
-        BSM_TRY(check_launch(c, "soa_to_aos"));
+        BSM_TRY(soa_to_aos(c, which == 0 ? c->fdl.as<uint32_t>() : c->fml.as<uint32_t>(), W, H));
         BSM_CUDA(cudaMemcpyAsync(dst, c->aux0.p, aos * 4, cudaMemcpyDeviceToHost, c->stream));
         BSM_TRY(sync(c));
     }
