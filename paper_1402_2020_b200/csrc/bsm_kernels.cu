@@ -1056,13 +1056,15 @@ __device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const uns
 // K6d -- voting refinement, NP invalid pixels per warp (LPP = 32/NP lanes
 // each).  Per window row the LPP lanes of a pixel form the bins and weights of
 // LPP consecutive voters in parallel (weight from the exact host table, or
-// the device exp for Lab planes), stage them, then fold them in voter order:
-// lane sl owns the bins b with (b % LPP) == sl and walks the staged entries in
-// order, keeping its current bin's running sum in a register.  Per bin the
-// additions are therefore the reference's row-major sequence; the NP pixels
-// fold side by side, so one warp step advances NP voters.
+// the device exp for Lab planes; the loads of a batch of CB chunks are issued
+// together), stage them, then fold them in voter order: lane sl owns the bins
+// b with (b % LPP) == sl, finds its entries of the chunk from ballots of the
+// valid flag and the residue bits, and walks them in order, keeping its
+// current bin's running sum in a register.  Per bin the additions are
+// therefore the reference's row-major sequence; the NP pixels fold side by
+// side.
 template <int NP, bool DEVEXP>
-__global__ void __launch_bounds__(256) k_vote_refine_fold(
+__global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
     const uint32_t* __restrict__ vmap, const float* __restrict__ lab, const float* __restrict__ lab256, int W,
     int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
     const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
@@ -1116,25 +1118,39 @@ __global__ void __launch_bounds__(256) k_vote_refine_fold(
         double acc = 0.0;
         bool any = false;
         const int tu = u * (u + 1) / 2;
+        // Per window row, the loads of CB chunks (LPP voters each) are issued
+        // together (vmap, then the weights), then the chunks fold in order:
+        // one L2 round trip per batch instead of one per chunk.
+        constexpr int CB = 6;
+        const int nch = (2 * radius + LPP) / LPP;  // ceil((2r + 1) / LPP)
         for (int dy = -radius; dy <= radius; ++dy) {
             const int py = y + dy;
             const bool rowok = live && py >= 0 && py < rows;
             const uint32_t* row = vmap + size_t(rowok ? py : 0) * W;
             const int dy2 = dy * dy;
-            for (int dx0 = -radius; dx0 <= radius; dx0 += LPP) {
-                const int dx = dx0 + sl;
-                const int px = x + dx;
-                int bin = -1;
-                double w = 0.0;
-                if (rowok && dx <= radius && px >= 0 && px < W) {
-                    const uint32_t e = __ldg(row + px);
+            for (int c0 = 0; c0 < nch; c0 += CB) {
+                uint32_t ev[CB];
+#pragma unroll
+                for (int k = 0; k < CB; ++k) {
+                    const int dx = -radius + (c0 + k) * LPP + sl;
+                    const int px = x + dx;
+                    ev[k] = (rowok && dx <= radius && px >= 0 && px < W) ? __ldg(row + px) : 0u;
+                }
+                int bv[CB];
+                double wv[CB];
+#pragma unroll
+                for (int k = 0; k < CB; ++k) {
+                    const uint32_t e = ev[k];
+                    const int dx = -radius + (c0 + k) * LPP + sl;
+                    bv[k] = -1;
+                    wv[k] = 0.0;
                     if (e & (1u << 24)) {
-                        bin = int(e & 0xFFFFu);
+                        bv[k] = int(e & 0xFFFFu);
                         const int v = int((e >> 16) & 0xFFu);
                         if (DEVEXP) {
                             float l0, l1, l2;
                             if (lab) {
-                                const size_t q = 3 * (size_t(py) * W + px);
+                                const size_t q = 3 * (size_t(py) * W + x + dx);
                                 l0 = __ldg(lab + q);
                                 l1 = __ldg(lab + q + 1);
                                 l2 = __ldg(lab + q + 2);
@@ -1146,30 +1162,44 @@ __global__ void __launch_bounds__(256) k_vote_refine_fold(
                             const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
                                                         fabsf(__fsub_rn(lx2, l2)));
                             const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
-                            w = exp_glibc(arg, ep, stab);
+                            wv[k] = exp_glibc(arg, ep, stab);
                         } else {
                             const int tri = v >= u ? (v * (v + 1) / 2 + u) : (tu + v);
-                            w = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
+                            wv[k] = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
                         }
                     }
                 }
-                any |= (__ballot_sync(full, bin >= 0) & submask) != 0u;
-                sbn[lane] = bin;
-                sw[lane] = w;
-                __syncwarp();
 #pragma unroll
-                for (int j = 0; j < LPP; ++j) {
-                    const int b = sbn[sub * LPP + j];
-                    if (b >= 0 && (b % LPP) == sl) {
+                for (int k = 0; k < CB; ++k) {
+                    if (c0 + k >= nch) break;  // warp-uniform
+                    const int bin = bv[k];
+                    const double w = wv[k];
+                    // owner lane of bin b: b % LPP; the entries each owner
+                    // takes come from four ballots (valid + residue bits)
+                    const unsigned vb = __ballot_sync(full, bin >= 0) & submask;
+                    unsigned mine = vb >> (sub * LPP);
+#pragma unroll
+                    for (int kb = 0; (1 << kb) < LPP; ++kb) {
+                        const unsigned bk = __ballot_sync(full, (bin >> kb) & 1) >> (sub * LPP);
+                        mine &= ((sl >> kb) & 1) ? bk : ~bk;
+                    }
+                    any |= vb != 0u;
+                    sbn[lane] = bin;
+                    sw[lane] = w;
+                    __syncwarp();
+                    while (mine) {
+                        const int j = sub * LPP + __ffs(mine) - 1;
+                        mine &= mine - 1;
+                        const int b = sbn[j];
                         if (b != cur) {
                             if (cur >= 0) bins[cur] = acc;
                             cur = b;
                             acc = bins[b];
                         }
-                        acc += sw[sub * LPP + j];
+                        acc += sw[j];
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
         if (cur >= 0) bins[cur] = acc;
