@@ -334,14 +334,45 @@ __device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t
 
 constexpr int kM4Stage = 132;  // stage row stride (words): 16-B aligned, conflict-free read-out
 
-__global__ void __launch_bounds__(32, 16)
+// MSB-first k-th-smallest selection over 8 bit planes (4 words per lane,
+// 128 values per lane, 4096 per warp) fused with the comparator: at a bit
+// where the threshold takes 1, the still-equal values with a 0 there are
+// strictly below it.  Returns the output words (a <= T) in o.
+__device__ __forceinline__ uint4 select_le(const uint32_t (&pl)[8][4], int k) {
+    uint32_t eq0 = ~0u, eq1 = ~0u, eq2 = ~0u, eq3 = ~0u;
+    uint32_t lt0 = 0u, lt1 = 0u, lt2 = 0u, lt3 = 0u;
+    int kk = k;
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+        const uint32_t z0 = eq0 & ~pl[j][0], z1 = eq1 & ~pl[j][1], z2 = eq2 & ~pl[j][2], z3 = eq3 & ~pl[j][3];
+        const int zeros = int(__reduce_add_sync(0xFFFFFFFFu, uint32_t(__popc(z0) + __popc(z1) + __popc(z2) + __popc(z3))));
+        if (zeros >= kk) {  // warp-uniform: threshold bit 0
+            eq0 = z0;
+            eq1 = z1;
+            eq2 = z2;
+            eq3 = z3;
+        } else {  // threshold bit 1
+            kk -= zeros;
+            lt0 |= z0;
+            lt1 |= z1;
+            lt2 |= z2;
+            lt3 |= z3;
+            eq0 &= pl[j][0];
+            eq1 &= pl[j][1];
+            eq2 &= pl[j][2];
+            eq3 &= pl[j][3];
+        }
+    }
+    return make_uint4(lt0 | eq0, lt1 | eq1, lt2 | eq2, lt3 | eq3);
+}
+
+__global__ void __launch_bounds__(32, 12)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
             const uint8_t* __restrict__ rank, int half, int NW, int Wp, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
-    uint32_t* planes = rho + rho_words;                   // [2 px][8 planes][4 chunks][32 lanes]
-    uint32_t* stage = planes + 2 * 8 * 4 * 32;            // [kM3Px][kM4Stage]
+    uint32_t* stage = rho + rho_words;                    // [kM3Px][kM4Stage]
     uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * kM4Stage);  // 2 x 256
     uint8_t* tile = rrows + 512;                                            // (2h+1) x (kM3Px + 2h)
     const int G = (n + 31) >> 5;
@@ -360,7 +391,6 @@ __global__ void __launch_bounds__(32, 16)
     __syncwarp();
 
     const int k = max(1, n / 4);
-    const unsigned full = 0xFFFFFFFFu;
 #pragma unroll 1
     for (int q = 0; q < kM3Px; q += 2) {
         const int cia = half * TW + half + q, cib = cia + 1;
@@ -375,7 +405,8 @@ __global__ void __launch_bounds__(32, 16)
         }
         __syncwarp();
 
-#pragma unroll 1
+        uint32_t pa[8][4], pb[8][4];
+#pragma unroll
         for (int m = 0; m < 4; ++m) {
             uint32_t wa[8], wb[8];
 #pragma unroll
@@ -391,64 +422,18 @@ __global__ void __launch_bounds__(32, 16)
                 wa[t4] = __byte_perm(x01, x23, 0x5410);
                 wb[t4] = __byte_perm(x01, x23, 0x7632);
             }
-            uint32_t pa[8], pb[8];
-            bytes_to_planes(wa, pa);
-            bytes_to_planes(wb, pb);
+            uint32_t ta[8], tb[8];
+            bytes_to_planes(wa, ta);
+            bytes_to_planes(wb, tb);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                planes[((0 * 8 + j) * 4 + m) * 32 + lane] = pa[j];
-                planes[((1 * 8 + j) * 4 + m) * 32 + lane] = pb[j];
+                pa[j][m] = ta[j];
+                pb[j][m] = tb[j];
             }
         }
         __syncwarp();  // rho / rrows are rewritten by the next pass
-
-#pragma unroll 1
-        for (int px = 0; px < 2; ++px) {
-            uint32_t P[8][4];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-#pragma unroll
-                for (int m = 0; m < 4; ++m) P[j][m] = planes[((px * 8 + j) * 4 + m) * 32 + lane];
-            // MSB-first selection of the k-th smallest a (pads are 255: never below a real k-th).
-            uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u};
-            int kk = k, T = 0;
-#pragma unroll
-            for (int j = 7; j >= 0; --j) {
-                const int zl = __popc(eq[0] & ~P[j][0]) + __popc(eq[1] & ~P[j][1]) + __popc(eq[2] & ~P[j][2]) +
-                               __popc(eq[3] & ~P[j][3]);
-                const int zeros = int(__reduce_add_sync(full, uint32_t(zl)));
-                if (zeros >= kk) {
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) eq[m] &= ~P[j][m];
-                } else {
-                    kk -= zeros;
-                    T |= 1 << j;
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) eq[m] &= P[j][m];
-                }
-            }
-            // bit = a <= T: (a < T) | (a == T); eq already holds a == T.
-            uint32_t lt[4] = {0u, 0u, 0u, 0u}, e2[4] = {~0u, ~0u, ~0u, ~0u};
-#pragma unroll
-            for (int j = 7; j >= 0; --j) {
-                if ((T >> j) & 1) {
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        lt[m] |= e2[m] & ~P[j][m];
-                        e2[m] &= P[j][m];
-                    }
-                } else {
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) e2[m] &= ~P[j][m];
-                }
-            }
-            uint4 o;
-            o.x = lt[0] | e2[0];
-            o.y = lt[1] | e2[1];
-            o.z = lt[2] | e2[2];
-            o.w = lt[3] | e2[3];
-            *reinterpret_cast<uint4*>(stage + (q + px) * kM4Stage + 4 * lane) = o;
-        }
+        *reinterpret_cast<uint4*>(stage + q * kM4Stage + 4 * lane) = select_le(pa, k);
+        *reinterpret_cast<uint4*>(stage + (q + 1) * kM4Stage + 4 * lane) = select_le(pb, k);
     }
     __syncwarp();
     const int rem = n & 31;
@@ -1515,7 +1500,7 @@ size_t mask_smem(const bsm_ctx* c) {
 
 size_t mask4_smem(const bsm_ctx* c) {
     const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
-    return size_t(round_up(c->mslots + 1, 4)) * 4 + 2 * 8 * 4 * 32 * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
+    return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
            size_t(TW) * TH;
 }
 
