@@ -310,14 +310,31 @@ __device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
     return x ^ t ^ (t << 28);  // byte j, bit k  <-  byte k, bit j
 }
 
+// transpose8x8 on the two 32-bit halves directly (the first two stages stay
+// inside a half; left shifts as multiplies so they can issue on the FMA pipe).
+__device__ __forceinline__ void transpose8x8_32(uint32_t& lo, uint32_t& hi) {
+    uint32_t t;
+    t = (lo ^ (lo >> 7)) & 0x00AA00AAu;
+    lo = lo ^ t ^ (t * 128u);
+    t = (hi ^ (hi >> 7)) & 0x00AA00AAu;
+    hi = hi ^ t ^ (t * 128u);
+    t = (lo ^ (lo >> 14)) & 0x0000CCCCu;
+    lo = lo ^ t ^ (t * 16384u);
+    t = (hi ^ (hi >> 14)) & 0x0000CCCCu;
+    hi = hi ^ t ^ (t * 16384u);
+    t = (lo ^ (hi * 16u)) & 0xF0F0F0F0u;
+    lo ^= t;
+    hi ^= t >> 4;
+}
+
 // w[0..7]: 32 byte values (value t = byte t%4 of w[t/4]); planes[j] bit t = bit j of value t.
 __device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t (&pl)[8]) {
     uint32_t lo[4], hi[4];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-        const uint64_t y = transpose8x8(uint64_t(w[2 * b]) | (uint64_t(w[2 * b + 1]) << 32));
-        lo[b] = uint32_t(y);
-        hi[b] = uint32_t(y >> 32);
+        lo[b] = w[2 * b];
+        hi[b] = w[2 * b + 1];
+        transpose8x8_32(lo[b], hi[b]);
     }
     // 4x4 byte transposes: plane j = byte j of block 0..3
 #pragma unroll
