@@ -282,3 +282,143 @@ class Reference(_Lib):
             raise ValueError(self.err())
         out["seconds"] = secs.value
         return out
+
+
+REF_IO_PATH = os.path.join(HERE, "_ref", "libbsm_ref_io.so")
+
+
+class RefIO(_Lib):
+    """image_io.hpp / eval.hpp / JSON sidecars of the reference (oracle/ref_io_driver.cpp)."""
+
+    ERR = {10: "IoError", 11: "FormatError", 1: "InvalidArgument", 2: "DimensionMismatch", 12: "EmptyRegion",
+           9: "Error"}
+
+    def __init__(self, path: str | None = None):
+        super().__init__(path or REF_IO_PATH, "refio_")
+
+    def _raise(self, rc):
+        msg = self.f("last_error", [], C.c_char_p)().decode()
+        raise RefIOError(self.ERR.get(rc, "Error"), msg)
+
+    def load_image(self, path):
+        w, h = C.c_int(), C.c_int()
+        fn = self.f("load_image", [C.c_char_p, _P, _P, _P])
+        rc = fn(path.encode(), C.byref(w), C.byref(h), None)
+        if rc:
+            self._raise(rc)
+        out = np.zeros((h.value, w.value, 3), np.uint8)
+        fn(path.encode(), C.byref(w), C.byref(h), _p(out))
+        return out
+
+    def load_gt(self, path, scale):
+        w, h = C.c_int(), C.c_int()
+        fn = self.f("load_gt", [C.c_char_p, _D, _P, _P, _P, _P])
+        rc = fn(path.encode(), scale, C.byref(w), C.byref(h), None, None)
+        if rc:
+            self._raise(rc)
+        d = np.zeros((h.value, w.value), np.float32)
+        v = np.zeros((h.value, w.value), np.uint8)
+        fn(path.encode(), scale, C.byref(w), C.byref(h), _p(d), _p(v))
+        return d, v
+
+    def save_disparity(self, path, d, v, scale, pfm=False):
+        d = np.ascontiguousarray(d, np.float32)
+        v = np.ascontiguousarray(v, np.uint8)
+        rc = self.f("save_disparity", [C.c_char_p, _P, _P, _I, _I, _D, _I])(
+            path.encode(), _p(d), _p(v), d.shape[1], d.shape[0], scale, int(pfm))
+        if rc:
+            self._raise(rc)
+
+    def save_gray_pgm(self, path, g):
+        g = np.ascontiguousarray(g, np.float32)
+        rc = self.f("save_gray_pgm", [C.c_char_p, _P, _I, _I])(path.encode(), _p(g), g.shape[1], g.shape[0])
+        if rc:
+            self._raise(rc)
+
+    def save_ppm(self, path, rgb):
+        rgb = np.ascontiguousarray(rgb, np.uint8)
+        rc = self.f("save_ppm", [C.c_char_p, _P, _I, _I])(path.encode(), _p(rgb), rgb.shape[1], rgb.shape[0])
+        if rc:
+            self._raise(rc)
+
+    def save_config(self, path, n, S, seed, d_max, radius, threads, spread, lc, le, tol, gt_scale, generator):
+        iv = np.array([n, S, seed, d_max, radius, threads], np.int64)
+        dv = np.array([spread, lc, le, tol, gt_scale], np.float64)
+        rc = self.f("save_config", [C.c_char_p, _P, _P, C.c_char_p])(path.encode(), _p(iv), _p(dv),
+                                                                       generator.encode())
+        if rc:
+            self._raise(rc)
+
+    def load_config(self, path):
+        iv = np.zeros(6, np.int64)
+        dv = np.zeros(5, np.float64)
+        gen = C.create_string_buffer(256)
+        rc = self.f("load_config", [C.c_char_p, _P, _P, C.c_char_p, _I])(path.encode(), _p(iv), _p(dv), gen, 256)
+        if rc:
+            self._raise(rc)
+        keys = ["n", "window", "seed", "d_max", "vote_radius", "threads"]
+        out = {k: int(v) for k, v in zip(keys, iv)}
+        out.update({k: float(v) for k, v in zip(["spread", "lambda_c", "lambda_e", "lr_tolerance", "gt_scale"], dv)})
+        out["generator"] = gen.value.decode()
+        return out
+
+    def save_pattern(self, path, pairs, n, window, spread, seed):
+        pairs = np.ascontiguousarray(pairs, np.int16)
+        rc = self.f("save_pattern", [C.c_char_p, _P, _I, _I, _D, C.c_uint64])(
+            path.encode(), _p(pairs), n, window, spread, seed)
+        if rc:
+            self._raise(rc)
+
+    def load_pattern(self, path, cap=16384):
+        n, w, sp, sd = C.c_int(), C.c_int(), C.c_double(), C.c_uint64()
+        pairs = np.zeros((cap, 4), np.int16)
+        rc = self.f("load_pattern", [C.c_char_p, _P, _P, _P, _P, _P, _I])(
+            path.encode(), C.byref(n), C.byref(w), C.byref(sp), C.byref(sd), _p(pairs), cap)
+        if rc:
+            self._raise(rc)
+        return n.value, w.value, sp.value, sd.value, pairs[: n.value].copy()
+
+    def bad_pixel_rate(self, d, v, gd, gv, region, threshold):
+        H, W = d.shape
+        rate, cnt, bad = C.c_double(), C.c_long(), C.c_long()
+        args = [np.ascontiguousarray(x, t) for x, t in ((d, np.float32), (v, np.uint8), (gd, np.float32),
+                                                         (gv, np.uint8))]
+        reg = None if region is None else np.ascontiguousarray(region, np.float32)
+        rc = self.f("bad_pixel_rate", [_P, _P, _P, _P, _P, _I, _I, _D, _P, _P, _P])(
+            *[_p(a) for a in args], _p(reg), W, H, threshold, C.byref(rate), C.byref(cnt), C.byref(bad))
+        if rc:
+            self._raise(rc)
+        return rate.value, cnt.value, bad.value
+
+    def linear_fit_r2(self, xs, ys):
+        xs = np.ascontiguousarray(xs, np.float64)
+        ys = np.ascontiguousarray(ys, np.float64)
+        out = C.c_double()
+        rc = self.f("linear_fit_r2", [_P, _P, _I, _P])(_p(xs), _p(ys), len(xs), C.byref(out))
+        if rc:
+            self._raise(rc)
+        return out.value
+
+    def write_sweep_csv(self, path, n, err, secs):
+        n = np.ascontiguousarray(n, np.int32)
+        err = np.ascontiguousarray(err, np.float64)
+        secs = np.ascontiguousarray(secs, np.float64)
+        rc = self.f("write_sweep_csv", [C.c_char_p, _P, _P, _P, _I])(path.encode(), _p(n), _p(err), _p(secs), len(n))
+        if rc:
+            self._raise(rc)
+
+    def radiometric(self, path, rate9):
+        r = np.ascontiguousarray(rate9, np.float64).reshape(9)
+        dg, od = C.c_double(), C.c_double()
+        rc = self.f("write_radiometric_csv", [C.c_char_p, _P, _P, _P])(
+            path.encode() if path else None, _p(r), C.byref(dg), C.byref(od))
+        if rc:
+            self._raise(rc)
+        return dg.value, od.value
+
+
+class RefIOError(Exception):
+    def __init__(self, kind, msg):
+        super().__init__(f"{kind}: {msg}")
+        self.kind = kind
+        self.msg = msg

@@ -268,6 +268,10 @@ def _view(img, name="image") -> np.ndarray:
     return _rgb(a, name) if a.ndim == 3 else _u8(a, name)
 
 
+def _is_gray(rgb: np.ndarray) -> bool:
+    return bool(np.array_equal(rgb[:, :, 0], rgb[:, :, 1]) and np.array_equal(rgb[:, :, 1], rgb[:, :, 2]))
+
+
 def rgb24_tables():
     """to_gray / to_lab of every 24-bit colour, index (r << 16) | (g << 8) | b."""
     g = np.zeros(1 << 24, np.float32)
@@ -416,6 +420,8 @@ def run_pipeline(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern]
     if L.shape != R.shape:
         raise DimensionMismatch("pipeline: left/right dimensions differ")
     cfg.validate()
+    if L.ndim == 3 and _is_gray(L) and _is_gray(R):  # r = g = b views take the uint8 path
+        L, R = np.ascontiguousarray(L[:, :, 0]), np.ascontiguousarray(R[:, :, 0])
     if pattern is None:
         pattern = generate_pattern(cfg=cfg)
     ctx = ctx or default_context()
