@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round evidence in one GPU call: smoke, pytest -m gpu, bench of every workload
+# (+ torchrun launch, reference arm), launch list and ncu --set full captures
+# of the pipeline kernels.  Usage (under gpurun): bash tools/gpu_full.sh <tag>
+TAG=${1:-f}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > gpurun_out/${TAG}_smi.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/${TAG}_pytest_gpu.log
+bash tools/gpu_bench_all.sh ${TAG}
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_default.json 2> gpurun_out/${TAG}_bench_default.err
+echo "default bench rc=$?"; cut -c1-300 gpurun_out/${TAG}_bench_default.json
+bash tools/gpu_prof.sh ${TAG} c2
+for K in k_cost_wta k_mask4 k_descriptor4 k_vote_refine_fold k_lr_check_keys; do
+  python tools/summarize_ncu.py gpurun_out/${TAG}_${K}.ncu-rep >> gpurun_out/${TAG}_ncu_kernels_c2.txt 2>&1
+done
+echo done
