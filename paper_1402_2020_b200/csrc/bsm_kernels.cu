@@ -354,67 +354,91 @@ constexpr int kM4Stage = 132;  // stage row stride (words): 16-B aligned, confli
 // MSB-first k-th-smallest selection over 8 bit planes (4 words per lane,
 // 128 values per lane, 4096 per warp) fused with the comparator: at a bit
 // where the threshold takes 1, the still-equal values with a 0 there are
-// strictly below it.  Returns the output words (a <= T) in o.
-__device__ __forceinline__ uint4 select_le(const uint32_t (&pl)[8][4], int k) {
-    uint32_t eq0 = ~0u, eq1 = ~0u, eq2 = ~0u, eq3 = ~0u;
-    uint32_t lt0 = 0u, lt1 = 0u, lt2 = 0u, lt3 = 0u;
-    int kk = k;
+// strictly below it; the output words are (a <= T) = lt | eq.
+// Two selects in lockstep (the two pixels of a pass): the REDUX of one
+// overlaps the POPCs and the REDUX of the other.
+__device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][4], const uint32_t (&pb)[8][4], int k,
+                                           uint4& oa, uint4& ob) {
+    uint32_t ea[4] = {~0u, ~0u, ~0u, ~0u}, eb[4] = {~0u, ~0u, ~0u, ~0u};
+    uint32_t la[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
+    int ka = k, kb = k;
 #pragma unroll
     for (int j = 7; j >= 0; --j) {
-        const uint32_t z0 = eq0 & ~pl[j][0], z1 = eq1 & ~pl[j][1], z2 = eq2 & ~pl[j][2], z3 = eq3 & ~pl[j][3];
-        const int zeros = int(__reduce_add_sync(0xFFFFFFFFu, uint32_t(__popc(z0) + __popc(z1) + __popc(z2) + __popc(z3))));
-        if (zeros >= kk) {  // warp-uniform: threshold bit 0
-            eq0 = z0;
-            eq1 = z1;
-            eq2 = z2;
-            eq3 = z3;
-        } else {  // threshold bit 1
-            kk -= zeros;
-            lt0 |= z0;
-            lt1 |= z1;
-            lt2 |= z2;
-            lt3 |= z3;
-            eq0 &= pl[j][0];
-            eq1 &= pl[j][1];
-            eq2 &= pl[j][2];
-            eq3 &= pl[j][3];
+        uint32_t za[4], zb[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            za[m] = ea[m] & ~pa[j][m];
+            zb[m] = eb[m] & ~pb[j][m];
+        }
+        const uint32_t ca = uint32_t(__popc(za[0]) + __popc(za[1]) + __popc(za[2]) + __popc(za[3]));
+        const uint32_t cb = uint32_t(__popc(zb[0]) + __popc(zb[1]) + __popc(zb[2]) + __popc(zb[3]));
+        const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
+        const int zbs = int(__reduce_add_sync(0xFFFFFFFFu, cb));
+        // warp-uniform choices; written as selects so both chains stay branch-free
+        const bool ha = zas < ka, hb = zbs < kb;
+        ka -= ha ? zas : 0;
+        kb -= hb ? zbs : 0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            la[m] |= ha ? za[m] : 0u;
+            ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
+            lb[m] |= hb ? zb[m] : 0u;
+            eb[m] = hb ? (eb[m] & pb[j][m]) : zb[m];
         }
     }
-    return make_uint4(lt0 | eq0, lt1 | eq1, lt2 | eq2, lt3 | eq3);
+    oa = make_uint4(la[0] | ea[0], la[1] | ea[1], la[2] | ea[2], la[3] | ea[3]);
+    ob = make_uint4(lb[0] | eb[0], lb[1] | eb[1], lb[2] | eb[2], lb[3] | eb[3]);
 }
 
 __global__ void __launch_bounds__(32, 12)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
-            const uint8_t* __restrict__ rank, int half, int NW, int Wp, uint32_t* __restrict__ mask) {
+            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
     uint32_t* stage = rho + rho_words;                    // [kM3Px][kM4Stage]
     uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * kM4Stage);  // 2 x 256
-    uint8_t* tile = rrows + 512;                                            // (2h+1) x (kM3Px + 2h)
+    uint8_t* tile = rrows + 512;                                            // (2h+1) x TW
     const int G = (n + 31) >> 5;
-    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
+    const int TH = 2 * half + 1;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
     const int ly = blockIdx.y;
     const int y = ybeg + ly;
-    for (int idx = lane; idx < TW * TH; idx += 32) {
-        const int r = idx / TW, c = idx - r * TW;
-        const int gx = min(max(x0 - half + c, 0), W - 1);
-        const int gy = min(max(y - half + r, 0), H - 1);
-        tile[idx] = __ldg(img + size_t(gy) * W + gx);
+    // The tile starts at the word-aligned column a0 <= x0 - h; interior tiles of
+    // 4-byte-aligned rows load whole words, the rest bytes with clamping.
+    const int a0 = (x0 - half) & ~3, ay0 = y - half;
+    const int sh = x0 - half - a0;
+    if ((W & 3) == 0 && a0 >= 0 && a0 + TW <= W && ay0 >= 0 && ay0 + TH <= H) {
+        const int nw = TW >> 2;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(img + size_t(ay0) * W + a0);
+#pragma unroll 4
+        for (int idx = lane; idx < TH * nw; idx += 32) {
+            const int r = idx / nw;
+            reinterpret_cast<uint32_t*>(tile)[idx] = __ldg(src + size_t(r) * (W >> 2) + (idx - r * nw));
+        }
+    } else {
+#pragma unroll 4
+        for (int idx = lane; idx < TW * TH; idx += 32) {
+            const int r = idx / TW, c = idx - r * TW;
+            const int gx = min(max(a0 + c, 0), W - 1);
+            const int gy = min(max(ay0 + r, 0), H - 1);
+            tile[idx] = __ldg(img + size_t(gy) * W + gx);
+        }
     }
     if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
     __syncwarp();
 
     const int k = max(1, n / 4);
+    const int c0 = half * TW + sh + half;  // tile index of pixel x0
+    // rank rows of the next pass's two centre pixels, loaded one pass ahead
+    uint4 rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (lane >> 4)])) + (lane & 15));
 #pragma unroll 1
     for (int q = 0; q < kM3Px; q += 2) {
-        const int cia = half * TW + half + q, cib = cia + 1;
-        {
-            const uint4* src = reinterpret_cast<const uint4*>(rank + 256 * int(lane < 16 ? tile[cia] : tile[cib]));
-            reinterpret_cast<uint4*>(rrows)[lane] = __ldg(src + (lane & 15));
-        }
+        const int cia = c0 + q, cib = cia + 1;
+        reinterpret_cast<uint4*>(rrows)[lane] = rr;
+        if (q + 2 < kM3Px)
+            rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[cia + 2 + (lane >> 4)])) + (lane & 15));
         __syncwarp();
         for (int j = lane; j < u; j += 32) {
             const int o = __ldg(uoff + j);
@@ -449,8 +473,10 @@ __global__ void __launch_bounds__(32, 12)
             }
         }
         __syncwarp();  // rho / rrows are rewritten by the next pass
-        *reinterpret_cast<uint4*>(stage + q * kM4Stage + 4 * lane) = select_le(pa, k);
-        *reinterpret_cast<uint4*>(stage + (q + 1) * kM4Stage + 4 * lane) = select_le(pb, k);
+        uint4 oa, ob;
+        select_le2(pa, pb, k, oa, ob);
+        *reinterpret_cast<uint4*>(stage + q * kM4Stage + 4 * lane) = oa;
+        *reinterpret_cast<uint4*>(stage + (q + 1) * kM4Stage + 4 * lane) = ob;
     }
     __syncwarp();
     const int rem = n & 31;
@@ -546,13 +572,13 @@ __device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
 __global__ void __launch_bounds__(32, 8)
     k_mask_f32(const float* __restrict__ lab, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words, int half,
-               int NW, int Wp, uint32_t* __restrict__ mask) {
+               int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
     uint32_t* planes = tv + rho_words;                    // [32 planes][4 chunks][32 lanes]
     float* ltile = reinterpret_cast<float*>(planes + 32 * 4 * 32);  // (2h+1) x (kM3Px + 2h) x 3
     const int G = (n + 31) >> 5;
-    const int TW = kM3Px + 2 * half, TH = 2 * half + 1;
+    const int TH = 2 * half + 1;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
     const int ly = blockIdx.y;
@@ -1468,8 +1494,11 @@ int ensure_desc4_table(bsm_ctx* c) {
 }
 
 
-int ensure_mask_offsets(bsm_ctx* c, int tile_px) {
-    const int TW = tile_px + 2 * c->half;
+// Row stride of the k_mask4 / k_mask_f32 window tiles: kM3Px + 2h columns plus
+// up to 3 of alignment slack, a multiple of 4 (word-wide tile loads).
+int mask4_tw(int half) { return round_up(kM3Px + 2 * half + 3, 4); }
+
+int ensure_mask_offsets(bsm_ctx* c, int TW) {
     if (c->uoff_tw == TW) return BSM_OK;
     const int side = 2 * c->half + 1;
     std::vector<int32_t> o(size_t(c->mslots), 0);  // empty slots read the centre (harmless)
@@ -1516,7 +1545,7 @@ size_t mask_smem(const bsm_ctx* c) {
 }
 
 size_t mask4_smem(const bsm_ctx* c) {
-    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
+    const int TW = mask4_tw(c->half), TH = 2 * c->half + 1;
     return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
            size_t(TW) * TH;
 }
@@ -1525,7 +1554,7 @@ size_t mask4_smem(const bsm_ctx* c) {
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
     const int Wp = round_up(W, 128);
-    BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? kM3Px : kMaskTile));
+    BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? mask4_tw(c->half) : kMaskTile + 2 * c->half));
     {
         Scope s(c, T_DESC);
         BSM_TRY(ensure_desc4_table(c));
@@ -1551,7 +1580,7 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
                                                    c->d_pqb.as<uint4>() + 3 * 1024, c->n,
                                                    c->d_uoff.as<int32_t>(), c->mslots, round_up(c->mslots + 1, 4),
                                                    c->d_rank.as<uint8_t>(),
-                                                   c->half, c->NW, Wp, mask);
+                                                   c->half, mask4_tw(c->half), c->NW, Wp, mask);
         } else {
             BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             k_mask<64><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
@@ -1679,7 +1708,7 @@ int ensure_descf_table(bsm_ctx* c) {
 }
 
 size_t maskf_smem(const bsm_ctx* c) {
-    const int TW = kM3Px + 2 * c->half, TH = 2 * c->half + 1;
+    const int TW = mask4_tw(c->half), TH = 2 * c->half + 1;
     return size_t(round_up(c->mslots + 1, 4)) * 4 + 32 * 4 * 32 * 4 + size_t(TW) * TH * 12;
 }
 
@@ -1689,7 +1718,7 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
     if (c->n > 4096) return set_err(BSM_UNSUPPORTED, "bsm: float-plane (colour) fields support n <= 4096");
     const int Wp = round_up(W, 128);
     BSM_TRY(ensure_descf_table(c));
-    BSM_TRY(ensure_mask_offsets(c, kM3Px));
+    BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
         const int TW = kDfTX + 2 * c->half, TH = kDfTY * kDfPY + 2 * c->half;
@@ -1707,7 +1736,8 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
         dim3 grid(Wp / kM3Px, rows);
         k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
                                                 c->d_pqb.as<uint4>() + 3 * 1024, c->n, c->d_uoff.as<int32_t>(),
-                                                c->mslots, round_up(c->mslots + 1, 4), c->half, c->NW, Wp, mask);
+                                                c->mslots, round_up(c->mslots + 1, 4), c->half, mask4_tw(c->half),
+                                                c->NW, Wp, mask);
         BSM_TRY(check_launch(c, "mask_f32"));
     }
     return BSM_OK;
