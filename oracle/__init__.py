@@ -293,8 +293,8 @@ class RefIO(_Lib):
     ERR = {10: "IoError", 11: "FormatError", 1: "InvalidArgument", 2: "DimensionMismatch", 12: "EmptyRegion",
            9: "Error"}
 
-    def __init__(self, path: str | None = None):
-        super().__init__(path or REF_IO_PATH, "refio_")
+    def __init__(self, path: str | None = None, prefix: str = "refio_"):
+        super().__init__(path or REF_IO_PATH, prefix)
 
     def _raise(self, rc):
         msg = self.f("last_error", [], C.c_char_p)().decode()

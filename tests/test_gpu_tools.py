@@ -24,7 +24,10 @@ def rio():
     return RefIO()
 
 
-def _cli(*args):
+def _cli(*args, impl="python"):
+    if impl == "cpp":  # the C++ tool (paper_1402_2020_b200/csrc/bsm_cli.cpp)
+        return subprocess.run([os.path.join(ROOT, "paper_1402_2020_b200", "bsm"), *args], capture_output=True,
+                              text=True, cwd=ROOT)
     return subprocess.run([sys.executable, "-m", "paper_1402_2020_b200", *args], capture_output=True, text=True,
                           cwd=ROOT, env={**os.environ, "PYTHONPATH": ROOT})
 
@@ -34,8 +37,9 @@ def _crop(h=40, w=160, seed=1):
     return left[100:100 + h, 50:50 + w].copy(), right[100:100 + h, 50:50 + w].copy()
 
 
+@pytest.mark.parametrize("impl", ["python", "cpp"])
 @pytest.mark.parametrize("colour", [False, True])
-def test_cli_match_files_byte_identical(tmp_path, ref, rio, default_pairs, colour):
+def test_cli_match_files_byte_identical(tmp_path, ref, rio, default_pairs, colour, impl):
     if colour:
         L, R = colour_pair(36, 150, seed=3)
         bio.save_ppm(L, str(tmp_path / "l.ppm"))
@@ -48,7 +52,7 @@ def test_cli_match_files_byte_identical(tmp_path, ref, rio, default_pairs, colou
         lp, rp = str(tmp_path / "l.pgm"), str(tmp_path / "r.pgm")
     out = str(tmp_path / "d.pgm")
     r = _cli("match", lp, rp, out, "--d_max", "60", "--stages", "--gt_scale", "4",
-             "--emit-pattern", str(tmp_path / "pat.json"))
+             "--emit-pattern", str(tmp_path / "pat.json"), impl=impl)
     assert r.returncode == 0, r.stderr
     want = ref.pipeline(L, R, default_pairs, 26, 60, threads=16, want_unmasked=True, channels=3 if colour else 1)
     ones = np.ones_like(want["refined_v"])
@@ -64,17 +68,19 @@ def test_cli_match_files_byte_identical(tmp_path, ref, rio, default_pairs, colou
     rio.save_pattern(str(tmp_path / "want_pat.json"), default_pairs, 4096, 26, 4.0, 42)
     assert (tmp_path / "pat.json").read_bytes() == (tmp_path / "want_pat.json").read_bytes()
     # float output and a saved pattern fed back in
-    r = _cli("match", lp, rp, str(tmp_path / "d.pfm"), "--d_max", "60", "--pattern", str(tmp_path / "pat.json"))
+    r = _cli("match", lp, rp, str(tmp_path / "d.pfm"), "--d_max", "60", "--pattern", str(tmp_path / "pat.json"),
+             impl=impl)
     assert r.returncode == 0, r.stderr
     rio.save_disparity(str(tmp_path / "want.pfm"), want["refined_d"], want["refined_v"], 1.0, pfm=True)
     assert (tmp_path / "d.pfm").read_bytes() == (tmp_path / "want.pfm").read_bytes()
 
 
-def test_cli_bench_line(tmp_path):
+@pytest.mark.parametrize("impl", ["python", "cpp"])
+def test_cli_bench_line(tmp_path, impl):
     L, R = _crop(24, 96)
     for nm, im in (("l.pgm", L), ("r.pgm", R)):
         (tmp_path / nm).write_bytes(b"P5\n%d %d\n255\n" % (im.shape[1], im.shape[0]) + im.tobytes())
-    r = _cli("bench", str(tmp_path / "l.pgm"), str(tmp_path / "r.pgm"), "--d_max", "32", "--runs", "2")
+    r = _cli("bench", str(tmp_path / "l.pgm"), str(tmp_path / "r.pgm"), "--d_max", "32", "--runs", "2", impl=impl)
     assert r.returncode == 0, r.stderr
     assert r.stdout.startswith("median of 2 runs: ") and "(96x24, d_max=32, n=4096, threads=1)" in r.stdout
 
