@@ -390,7 +390,7 @@ __device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][4], const uin
     ob = make_uint4(lb[0] | eb[0], lb[1] | eb[1], lb[2] | eb[2], lb[3] | eb[3]);
 }
 
-__global__ void __launch_bounds__(32, 12)
+__global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
             const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
