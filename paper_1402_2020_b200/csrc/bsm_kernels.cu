@@ -722,6 +722,10 @@ __global__ void __launch_bounds__(256, 2)
     const int d0 = blockIdx.x * DC;
     const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
     const int nchunks = (NW + K - 1) / K;
+    // Tiles with no in-range (x, d) at all (d >= D, or every correspondence
+    // outside the image, matcher.hpp:100) exit before loading anything.
+    const int xhi = min(x0 + T, W) - 1;
+    if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
 
     // Per-thread copy assignments, fixed for all stages: a/m rows (tid>>5) and
     // (tid>>5)+8, column 4*(tid&31); three 16-B chunks of the other-view span.
@@ -780,6 +784,9 @@ __global__ void __launch_bounds__(256, 2)
     const int xs = lane * 4;
     const int ds = wi * 8;
     const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
+    // A warp whose 128 x 8 block has no in-range (x, d) only helps stage the
+    // tiles; its compute is skipped (warp-uniform).
+    const bool busy = d0 + ds < D && (RIGHT ? x0 + d0 + ds < W : xhi >= d0 + ds);
 
 #pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
@@ -787,6 +794,7 @@ __global__ void __launch_bounds__(256, 2)
         __syncthreads();
         if (c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
         cp_async_commit();
+        if (!busy) continue;
         const uint32_t* sa = csm + (c % ST) * STAGE;
         const uint32_t* sm = sa + SA;
         const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
