@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
             for (int b = 0; b < 4; ++b) acc[r][b] = 0;
         const int cnt = w < full ? 32 : (w == full ? (n & 31) : 0);
         if (cnt == 32) {
-#pragma unroll 8
+            // fully unrolled: acc[r][k >> 3] stays a static register choice
+#pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const int2 e = __ldg(ptab + 32 * w + k);  // tile-relative offsets of p and q
 #pragma unroll
