@@ -3,7 +3,7 @@
 # Usage (under gpurun): bash tools/gpu_round.sh <tag> [skip_tests] [ncu_kernels_regex]
 TAG=${1:-r}
 SKIP_TESTS=${2:-0}
-KREGEX=${3:-"k_mask2|k_cost_wta"}
+KREGEX=${3:-"k_mask4|k_cost_wta"}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > gpurun_out/${TAG}_smi.txt
 if [ "$SKIP_TESTS" = "0" ]; then
