@@ -289,30 +289,24 @@ __device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_
 }
 
 // ---------------------------------------------------------------------------
-// K2'' -- mask for n <= 4096 on bit planes.  Lane l owns pairs
-// [128l, 128l + 128) in four chunks of 32; for two pixels per pass it
+// K2'' -- mask for n <= 4096 on bit planes.  Lane l owns bit positions
+// [128l, 128l + 128) in four chunks of 32 (the pair at each position comes
+// from the bank-balanced order, so every 32-lane rank gather is one
+// shared-memory wavefront); for two pixels per pass it
 //   1. gathers a = max(rhoP, rhoQ) of both pixels per pair (one u32 rank-table
 //      gather + VIMNMX.U16x2 serves both), packs each pixel's 32 chunk values
 //      into eight byte registers,
-//   2. transposes them into 8 bit planes (four 8x8 bit-matrix transposes and a
-//      4x4 byte transpose): plane j, word m of lane l holds bit j of a for
-//      pairs 128l + 32m + t at bit t -- exactly the layout of output word
-//      4l + m,
+//   2. transposes them into 8 bit planes held in registers (four 8x8 bit-matrix
+//      transposes and a 4x4 byte transpose): plane j, word m of lane l holds
+//      bit j of a for positions 128l + 32m + t at bit t -- exactly the layout
+//      of output word 4l + m,
 //   3. selects the k-th smallest a MSB-first on the planes (per bit: LOP3 +
-//      POPC per word, one REDUX), and
-//   4. emits bit = a <= T with an 8-plane comparator, one word per (lane, m).
-// Small loop bodies (no 64-register arrays), so the code stays cache-resident.
-__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
-    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
-    x = x ^ t ^ (t << 7);
-    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
-    x = x ^ t ^ (t << 14);
-    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
-    return x ^ t ^ (t << 28);  // byte j, bit k  <-  byte k, bit j
-}
-
-// transpose8x8 on the two 32-bit halves directly (the first two stages stay
-// inside a half; left shifts as multiplies so they can issue on the FMA pipe).
+//      POPC per word, one REDUX; the two pixels in lockstep) with the a <= T
+//      comparator fused in, and stages one uint4 of output words per lane.
+// 8x8 bit-matrix transpose of the 8 bytes (lo: rows 0-3, hi: rows 4-7),
+// afterwards byte j bit k = input byte k bit j.  Three delta-swap stages on the
+// 32-bit halves (the first two stay inside a half; left shifts as multiplies
+// so they can issue on the FMA pipe).
 __device__ __forceinline__ void transpose8x8_32(uint32_t& lo, uint32_t& hi) {
     uint32_t t;
     t = (lo ^ (lo >> 7)) & 0x00AA00AAu;
@@ -1585,8 +1579,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
             const size_t sm4 = mask4_smem(c);
             BSM_CUDA(cudaFuncSetAttribute(k_mask4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
             dim3 grid3(Wp / kM3Px, rows);
-            k_mask4<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
-                                                   c->d_pqb.as<uint4>() + 3 * 1024, c->n,
+            k_mask4<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+                                                   c->d_pqb.as<uint4>() + 1024, c->n,
                                                    c->d_uoff.as<int32_t>(), c->mslots, round_up(c->mslots + 1, 4),
                                                    c->d_rank.as<uint8_t>(),
                                                    c->half, mask4_tw(c->half), c->NW, Wp, mask);
@@ -1743,8 +1737,8 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
         const size_t sm = maskf_smem(c);
         BSM_CUDA(cudaFuncSetAttribute(k_mask_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         dim3 grid(Wp / kM3Px, rows);
-        k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * 1024,
-                                                c->d_pqb.as<uint4>() + 3 * 1024, c->n, c->d_uoff.as<int32_t>(),
+        k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+                                                c->d_pqb.as<uint4>() + 1024, c->n, c->d_uoff.as<int32_t>(),
                                                 c->mslots, round_up(c->mslots + 1, 4), c->half, mask4_tw(c->half),
                                                 c->NW, Wp, mask);
         BSM_TRY(check_launch(c, "mask_f32"));
@@ -2089,25 +2083,18 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     }
     c->slot_used.assign(size_t(c->mslots), -1);
     for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
-    // Byte offsets into the u32 rank table (tables 0/1: group-major order,
-    // kept for layout compatibility; tables 2/3 below are k_mask4's).
-    std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->u));
-    for (int i = 0; i < std::min(n, 4096); ++i) {
-        const int g = i >> 5, l = i & 31;
-        const size_t at = (size_t(g >> 2) * 32 + l) * 4 + (g & 3);
-        pqb[at] = 4 * (pq[size_t(i)] & 0xFFFFu);
-        pqb[4096 + at] = 4 * (pq[size_t(i)] >> 16);
-    }
-    // k_mask4: lane-block order -- lane l, chunk m, t: pair 128l + 32m + t at
-    // uint4 [(m*8 + t/4)*32 + l], component t%4.
-    pqb.resize(4 * 4096, uint32_t(4 * c->mslots));  // pads -> sentinel slot mslots
+    // Byte offsets into the u32 rank table of each bit position's two
+    // endpoints (k_mask4 / k_mask_f32): P table at [0, 4096), Q table at
+    // [4096, 8192), lane-block order -- lane l, chunk m, t: bit 128l + 32m + t
+    // at uint4 [(m*8 + t/4)*32 + l], component t%4.  Pads read the sentinel.
+    std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->mslots));
     for (int j = 0; j < std::min(n, 4096); ++j) {
         const int l = j >> 7, m = (j >> 5) & 3, t = j & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
         const uint32_t e = pq[size_t(c->order[size_t(j)])];
         const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
-        pqb[2 * 4096 + at] = uint32_t(4 * rslot[size_t(a)]);
-        pqb[3 * 4096 + at] = uint32_t(4 * rslot[size_t(b)]);
+        pqb[at] = uint32_t(4 * rslot[size_t(a)]);
+        pqb[4096 + at] = uint32_t(4 * rslot[size_t(b)]);
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
