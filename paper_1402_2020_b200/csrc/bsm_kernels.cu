@@ -619,51 +619,38 @@ __global__ void __launch_bounds__(32, 8)
             for (int j = 0; j < 32; ++j) planes[(j * 4 + m) * 32 + lane] = x[j];
         }
         __syncwarp();
-        // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF)
-        uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u};
-        uint32_t T = 0;
+        // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
+        // the a <= T comparator fused in: where the threshold takes a 1, the
+        // still-equal keys with a 0 there are strictly below it.
+        uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u}, lt[4] = {0u, 0u, 0u, 0u};
         int kk = k;
 #pragma unroll 1
         for (int j = 31; j >= 0; --j) {
-            uint32_t pl[4];
+            uint32_t pl[4], z[4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) pl[m] = planes[(j * 4 + m) * 32 + lane];
-            const int zl = __popc(eq[0] & ~pl[0]) + __popc(eq[1] & ~pl[1]) + __popc(eq[2] & ~pl[2]) +
-                           __popc(eq[3] & ~pl[3]);
-            const int zeros = int(__reduce_add_sync(full, uint32_t(zl)));
+            for (int m = 0; m < 4; ++m) {
+                pl[m] = planes[(j * 4 + m) * 32 + lane];
+                z[m] = eq[m] & ~pl[m];
+            }
+            const int zeros = int(__reduce_add_sync(full, uint32_t(__popc(z[0]) + __popc(z[1]) + __popc(z[2]) +
+                                                                     __popc(z[3]))));
             if (zeros >= kk) {
 #pragma unroll
-                for (int m = 0; m < 4; ++m) eq[m] &= ~pl[m];
+                for (int m = 0; m < 4; ++m) eq[m] = z[m];
             } else {
                 kk -= zeros;
-                T |= 1u << j;
-#pragma unroll
-                for (int m = 0; m < 4; ++m) eq[m] &= pl[m];
-            }
-        }
-        // bit = a <= T
-        uint32_t lt[4] = {0u, 0u, 0u, 0u}, e2[4] = {~0u, ~0u, ~0u, ~0u};
-#pragma unroll 1
-        for (int j = 31; j >= 0; --j) {
-            uint32_t pl[4];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) pl[m] = planes[(j * 4 + m) * 32 + lane];
-            if ((T >> j) & 1u) {
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
-                    lt[m] |= e2[m] & ~pl[m];
-                    e2[m] &= pl[m];
+                    lt[m] |= z[m];
+                    eq[m] &= pl[m];
                 }
-            } else {
-#pragma unroll
-                for (int m = 0; m < 4; ++m) e2[m] &= ~pl[m];
             }
         }
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const int w = 4 * lane + m;
             if (w < NW) {
-                uint32_t v = lt[m] | e2[m];
+                uint32_t v = lt[m] | eq[m];
                 if (w >= G) v = 0u;
                 else if (rem && w == G - 1) v &= (1u << rem) - 1u;
                 mask[(size_t(ly) * NW + w) * Wp + x0 + px] = v;
