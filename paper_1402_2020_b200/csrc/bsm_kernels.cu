@@ -564,41 +564,38 @@ __device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
     }
 }
 
-__global__ void __launch_bounds__(32, 8)
+__global__ void __launch_bounds__(32, 16)
     k_mask_f32(const float* __restrict__ lab, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
-               const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words, int half,
-               int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
+               const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
+               int NW, int Wp, uint32_t* __restrict__ mask) {
+    // Lab samples are read through L1 (no shared tile): shared memory holds
+    // only the slot keys and the 16 KB of bit planes, for occupancy.
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
     uint32_t* planes = tv + rho_words;                    // [32 planes][4 chunks][32 lanes]
-    float* ltile = reinterpret_cast<float*>(planes + 32 * 4 * 32);  // (2h+1) x (kM3Px + 2h) x 3
     const int G = (n + 31) >> 5;
-    const int TH = 2 * half + 1;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
     const int ly = blockIdx.y;
     const int y = ybeg + ly;
-    for (int idx = lane; idx < TW * TH; idx += 32) {
-        const int r = idx / TW, c = idx - r * TW;
-        const size_t g = size_t(min(max(y - half + r, 0), H - 1)) * W + min(max(x0 - half + c, 0), W - 1);
-        ltile[3 * idx] = __ldg(lab + 3 * g);
-        ltile[3 * idx + 1] = __ldg(lab + 3 * g + 1);
-        ltile[3 * idx + 2] = __ldg(lab + 3 * g + 2);
-    }
     if (lane == 0) tv[u] = 0xFFFFFFFFu;  // sentinel: larger than every SAD
-    __syncwarp();
     const int k = max(1, n / 4);
     const unsigned full = 0xFFFFFFFFu;
     const int rem = n & 31;
 #pragma unroll 1
     for (int px = 0; px < kM3Px; ++px) {
-        const int ci = half * TW + half + px;
-        const float c0 = ltile[3 * ci], c1 = ltile[3 * ci + 1], c2 = ltile[3 * ci + 2];
+        const int x = min(x0 + px, W - 1);  // pad columns repeat the last pixel (not stored)
+        const size_t ci = 3 * (size_t(y) * W + x);
+        const float c0 = __ldg(lab + ci), c1 = __ldg(lab + ci + 1), c2 = __ldg(lab + ci + 2);
         for (int j = lane; j < u; j += 32) {
-            const int o = ci + __ldg(uoff + j);
+            const int e = __ldg(uxy + j);  // (dy << 16) | (dx & 0xFFFF)
+            const int gx = min(max(x + int(int16_t(e & 0xFFFF)), 0), W - 1);
+            const int gy = min(max(y + (e >> 16), 0), H - 1);
+            const size_t q = 3 * (size_t(gy) * W + gx);
             // lab_sad(centre, window pixel), image.hpp:144-146
-            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(c0, ltile[3 * o])), fabsf(__fsub_rn(c1, ltile[3 * o + 1]))),
-                                        fabsf(__fsub_rn(c2, ltile[3 * o + 2])));
+            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(c0, __ldg(lab + q))),
+                                                  fabsf(__fsub_rn(c1, __ldg(lab + q + 1)))),
+                                        fabsf(__fsub_rn(c2, __ldg(lab + q + 2))));
             tv[j] = __float_as_uint(sad);
         }
         __syncwarp();
@@ -1398,7 +1395,7 @@ struct bsm_ctx {
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
-    DevBuf d_desc4, d_pq, d_pqb, d_uoff;
+    DevBuf d_desc4, d_pq, d_pqb, d_uoff, d_uxy;
     DevBuf d_descf, d_rgb_gray, d_rgb_lab, planes;
     int descf_tw = -1;
     bool rgb_ready = false;
@@ -1500,6 +1497,16 @@ int ensure_mask_offsets(bsm_ctx* c, int TW) {
     }
     BSM_TRY(c->d_uoff.ensure(std::max<size_t>(4, o.size() * 4)));
     BSM_CUDA(cudaMemcpy(c->d_uoff.p, o.data(), o.size() * 4, cudaMemcpyHostToDevice));
+    // the same slots as (dy << 16) | (dx & 0xFFFF) for the float-plane kernel
+    std::vector<int32_t> xy(size_t(c->mslots), 0);
+    for (int k = 0; k < c->mslots; ++k) {
+        const int ui = c->slot_used[size_t(k)];
+        if (ui < 0) continue;
+        const int dy = c->used[size_t(ui)] / side - c->half, dx = c->used[size_t(ui)] % side - c->half;
+        xy[size_t(k)] = int32_t(uint32_t(dy) << 16 | (uint32_t(dx) & 0xFFFFu));
+    }
+    BSM_TRY(c->d_uxy.ensure(std::max<size_t>(4, xy.size() * 4)));
+    BSM_CUDA(cudaMemcpy(c->d_uxy.p, xy.data(), xy.size() * 4, cudaMemcpyHostToDevice));
     c->uoff_tw = TW;
     return BSM_OK;
 }
@@ -1697,10 +1704,7 @@ int ensure_descf_table(bsm_ctx* c) {
     return BSM_OK;
 }
 
-size_t maskf_smem(const bsm_ctx* c) {
-    const int TW = mask4_tw(c->half), TH = 2 * c->half + 1;
-    return size_t(round_up(c->mslots + 1, 4)) * 4 + 32 * 4 * 32 * 4 + size_t(TW) * TH * 12;
-}
+size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + 32 * 4 * 32 * 4; }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, int ybeg, int rows,
@@ -1725,9 +1729,8 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
         BSM_CUDA(cudaFuncSetAttribute(k_mask_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         dim3 grid(Wp / kM3Px, rows);
         k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
-                                                c->d_pqb.as<uint4>() + 1024, c->n, c->d_uoff.as<int32_t>(),
-                                                c->mslots, round_up(c->mslots + 1, 4), c->half, mask4_tw(c->half),
-                                                c->NW, Wp, mask);
+                                                c->d_pqb.as<uint4>() + 1024, c->n, c->d_uxy.as<int32_t>(),
+                                                c->mslots, round_up(c->mslots + 1, 4), c->NW, Wp, mask);
         BSM_TRY(check_launch(c, "mask_f32"));
     }
     return BSM_OK;
@@ -1961,7 +1964,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
