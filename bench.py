@@ -111,7 +111,7 @@ def cpu_reference_sample(workload, rows, threads, pairs_arr):
     R = np.ascontiguousarray(right[y0:y0 + rows])
     from paper_1402_2020_b200.synth import WORKLOADS
     w = WORKLOADS[workload]
-    out = ref.pipeline(L, R, pairs_arr, 26, w.d_max, threads=threads)
+    out = ref.pipeline(L, R, pairs_arr, 26, w.d_max, threads=threads, channels=3 if L.ndim == 3 else 1)
     return out["seconds"], L.shape[1] * rows * w.d_max, os.path.basename(ref.path)
 
 
@@ -138,7 +138,8 @@ def run_reference(args):
         "impl": "reference", "metric": "Mdisp-evals/s", "value": v, "unit": "Mdisp-evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 popcount / f64 votes",
-        "data": "synthetic (BASELINE.json generator, SURVEY.md 8(d))",
+        "data": ("synthetic colour views (synth.colour_pair)" if args.workload.endswith("rgb")
+                 else "synthetic (BASELINE.json generator, SURVEY.md 8(d))"),
         "config": {"workload": w.name, "width": w.width, "height": w.height, "d_max": w.d_max, "n": 4096,
                    "sample": f"{rows}-row band per step"},
         "cpu_baseline": {"value": v, "unit": "Mdisp-evals/s", "cores": threads, "kind": "reference",
@@ -155,7 +156,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c2rgb"])
     ap.add_argument("--ref-rows", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="few steps, no CPU leg (for ncu)")
@@ -186,6 +187,7 @@ def main():
     # (strong scaling); every other workload -> rank r matches pair index r of
     # the workload's seed sequence (independent units, weak scaling).
     bands = args.workload == "c5" and world > 1
+    colour = args.workload.endswith("rgb")  # interleaved RGB views (colour path)
     left, right = workload_pair(args.workload, index=0 if bands else rank)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -208,6 +210,10 @@ def main():
         all_v = [torch.empty_like(band_v) for _ in range(world)]
 
     def step_device():
+        if colour:
+            check(lib().bsm_pipeline_rgb_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
+                                                C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
+            return
         if not bands:
             check(lib().bsm_pipeline_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
                                                C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
@@ -266,8 +272,9 @@ def main():
 
     def step_e2e():
         if not bands:
-            check(lib().bsm_pipeline_u8(ctx.handle, C.c_void_p(h_left.data_ptr()), C.c_void_p(h_right.data_ptr()),
-                                        W, H, C.byref(p), 0, C.byref(maps)))
+            fn = lib().bsm_pipeline_rgb if colour else lib().bsm_pipeline_u8
+            check(fn(ctx.handle, C.c_void_p(h_left.data_ptr()), C.c_void_p(h_right.data_ptr()),
+                     W, H, C.byref(p), 0, C.byref(maps)))
             return
         with torch.cuda.stream(stream):
             d_left.copy_(h_left, non_blocking=True)
@@ -331,13 +338,15 @@ def main():
         "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong" if bands else "weak", "vs_baseline": None,
-        "dtype": "u32 popcount / f64 votes", "data": "synthetic (BASELINE.json generator, SURVEY.md 8(d))",
+        "dtype": "u32 popcount / f64 votes",
+        "data": ("synthetic colour views (synth.colour_pair: configs[0] scene, three tone curves + noise)" if colour
+                 else "synthetic (BASELINE.json generator, SURVEY.md 8(d))"),
         "config": {"workload": w.name, "width": W, "height": H, "d_max": D, "n": 4096,
                    "pairs_per_step": 1 if bands else world,
                    "parallelism": (f"row bands x{world} + NCCL all-gather" if bands
                                    else (f"pairs x{world}" if world > 1 else "1 pair")),
                    "l2": "256 MiB flush before every step (outside events); working set 3.2 GB >> L2"},
-        "e2e": {"value": e2e_value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 2 * W * H,
+        "e2e": {"value": e2e_value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 2 * W * H * (3 if colour else 1),
                 "d2h_bytes_per_step": 5 * (world * rows_max if bands else H) * W,
                 "ms_per_step": float(te.item()) / args.steps},
         "gpu_launches": launches * args.steps,

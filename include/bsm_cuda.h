@@ -117,6 +117,11 @@ int bsm_compute_field_f32(bsm_ctx* ctx, const float* gray, const float* lab, int
 int bsm_pipeline_rgb(bsm_ctx* ctx, const uint8_t* left_rgb, const uint8_t* right_rgb, int W, int H,
                      const bsm_params* params, int want_unmasked, bsm_maps* out);
 
+/* bsm_pipeline_rgb on device-resident interleaved-RGB views (serving path;
+ * results stay on the device: bsm_fetch_maps / bsm_result_device). */
+int bsm_pipeline_rgb_device(bsm_ctx* ctx, const uint8_t* d_left_rgb, const uint8_t* d_right_rgb, int W, int H,
+                            const bsm_params* params, int want_unmasked);
+
 /* to_gray / to_lab of all 2^24 colours, index (r<<16)|(g<<8)|b (host). */
 int bsm_rgb24_tables(float* gray16M, float* lab48M);
 

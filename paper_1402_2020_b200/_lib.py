@@ -93,6 +93,7 @@ _SIGS = {
     "bsm_set_refine_mode": [_P, _I],
     "bsm_pipeline_u8": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I, C.POINTER(bsm_maps)],
     "bsm_pipeline_rgb": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I, C.POINTER(bsm_maps)],
+    "bsm_pipeline_rgb_device": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I],
     "bsm_compute_field_f32": [_P, _P, _P, _I, _I, _P, _P],
     "bsm_rgb24_tables": [_P, _P],
     "bsm_pipeline_u8_device": [_P, _P, _P, _I, _I, C.POINTER(bsm_params), _I],

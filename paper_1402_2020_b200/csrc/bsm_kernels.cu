@@ -2447,6 +2447,32 @@ int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W
     return sync(c);
 }
 
+// Colour pair already on the device: RGB -> gray/Lab planes, then the fused pipeline.
+static int rgb_pipeline(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_right, int W, int H,
+                        const bsm_params* params, bool want_unmasked) {
+    BSM_TRY(ensure_rgb_tables(c));
+    const size_t px = size_t(W) * H;
+    BSM_TRY(c->planes.ensure(px * 32));
+    Views v;
+    float* base = c->planes.as<float>();
+    v.gl = base;
+    v.gr = base + px;
+    v.ll = base + 2 * px;
+    v.lr = base + 5 * px;
+    {
+        Scope s(c, T_DESC);  // the conversion is accounted with the descriptor stage
+        const int tb = 256;
+        k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(d_left, px, c->d_rgb_gray.as<float>(),
+                                                                      c->d_rgb_lab.as<float>(), base, base + 2 * px);
+        BSM_TRY(check_launch(c, "rgb_planes"));
+        k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(d_right, px, c->d_rgb_gray.as<float>(),
+                                                                      c->d_rgb_lab.as<float>(), base + px,
+                                                                      base + 5 * px);
+        BSM_TRY(check_launch(c, "rgb_planes"));
+    }
+    return pipeline_device(c, v, W, H, 0, H, params, want_unmasked);
+}
+
 int bsm_pipeline_rgb(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int W, int H, const bsm_params* params,
                      int want_unmasked, bsm_maps* out) {
     BSM_TRY(begin_call(c));
@@ -2454,32 +2480,27 @@ int bsm_pipeline_rgb(bsm_ctx* c, const uint8_t* left, const uint8_t* right, int 
     BSM_TRY(check_dims(W, H));
     BSM_TRY(validate_params(params));
     if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
-    BSM_TRY(ensure_rgb_tables(c));
     const size_t px = size_t(W) * H;
     BSM_TRY(c->img_l.ensure(px * 3));
     BSM_TRY(c->img_r.ensure(px * 3));
-    BSM_TRY(c->planes.ensure(px * 32));
     {
         Scope s(c, T_H2D);
         BSM_CUDA(cudaMemcpyAsync(c->img_l.p, left, px * 3, cudaMemcpyHostToDevice, c->stream));
         BSM_CUDA(cudaMemcpyAsync(c->img_r.p, right, px * 3, cudaMemcpyHostToDevice, c->stream));
     }
-    Views v;
-    float* base = c->planes.as<float>();
-    v.gl = base;
-    v.gr = base + px;
-    v.ll = base + 2 * px;
-    v.lr = base + 5 * px;
-    const int tb = 256;
-    k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->img_l.as<uint8_t>(), px, c->d_rgb_gray.as<float>(),
-                                                                  c->d_rgb_lab.as<float>(), base, base + 2 * px);
-    BSM_TRY(check_launch(c, "rgb_planes"));
-    k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->img_r.as<uint8_t>(), px, c->d_rgb_gray.as<float>(),
-                                                                  c->d_rgb_lab.as<float>(), base + px, base + 5 * px);
-    BSM_TRY(check_launch(c, "rgb_planes"));
-    BSM_TRY(pipeline_device(c, v, W, H, 0, H, params, want_unmasked != 0));
+    BSM_TRY(rgb_pipeline(c, c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>(), W, H, params, want_unmasked != 0));
     BSM_TRY(fetch(c, out));
     return sync(c);
+}
+
+int bsm_pipeline_rgb_device(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_right, int W, int H,
+                            const bsm_params* params, int want_unmasked) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    if (!d_left || !d_right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    return rgb_pipeline(c, d_left, d_right, W, H, params, want_unmasked != 0);
 }
 
 int bsm_stream(bsm_ctx* c, void** stream) {

@@ -33,6 +33,8 @@ WORKLOADS = {
     "c3": Workload("c3_640x480_d64_radiometric", 2, 640, 480, 64, 3),
     "c4": Workload("c4_64x1920x1080_d192", 3, 1920, 1080, 192, 4000, pairs=64),
     "c5": Workload("c5_4096x2160_d256", 4, 4096, 2160, 256, 5),
+    # colour input at the configs[1] size: colour_pair views
+    "c2rgb": Workload("c2rgb_1392x1104_d240_colour", 1, 1392, 1104, 240, 2),
 }
 
 _synth = None
@@ -64,6 +66,10 @@ def synth_pair(config: int, seed: int, width: int, height: int, with_gt: bool = 
 
 def workload_pair(key: str, index: int = 0, with_gt: bool = False):
     w = WORKLOADS[key]
+    if key.endswith("rgb"):
+        if with_gt:
+            raise ValueError("colour workloads carry no ground truth")
+        return colour_pair(w.height, w.width, seed=w.seed + index)
     return synth_pair(w.config, w.seed + index, w.width, w.height, with_gt)
 
 
