@@ -2,7 +2,7 @@
 # Bench every workload at N=1 (+ torchrun launch of the default), JSON lines to gpurun_out/<tag>_bench_<wl>.json
 TAG=${1:-b}
 mkdir -p gpurun_out
-for WL in c2 c1 c3 c5 c4; do
+for WL in c2 c1 c3 c5 c4 c2rgb; do
   timeout 600 python bench.py --workload $WL --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench_${WL}.json 2> gpurun_out/${TAG}_bench_${WL}.err
   echo "$WL rc=$?"; cut -c1-400 gpurun_out/${TAG}_bench_${WL}.json
 done
