@@ -219,15 +219,15 @@ int gather_cost(const int* s) {
 }
 }  // namespace
 
-void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<int>& slot, double* cost_before,
-                      double* cost_after) {
-    // gathers: 2 endpoints x 128 steps, 32 lanes each (pairs >= n: sentinel, excluded)
-    const int nsteps = 128;
+void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, int lane_pos, std::vector<int>& slot,
+                      double* cost_before, double* cost_after) {
+    // gathers: 2 endpoints x lane_pos steps, 32 lanes each (pairs >= n: sentinel, excluded)
+    const int nsteps = lane_pos;
     std::vector<int> gpair(size_t(2) * nsteps * 32, -1);  // offset index per (gather, lane), -1 = sentinel
     for (int e = 0; e < 2; ++e)
         for (int st = 0; st < nsteps; ++st)
             for (int l = 0; l < 32; ++l) {
-                const int i = 128 * l + st;  // st = 32m + t
+                const int i = lane_pos * l + st;  // st = 32m + t
                 if (i < n) gpair[(size_t(e) * nsteps + st) * 32 + l] = int(e ? (pq[i] >> 16) : (pq[i] & 0xFFFFu));
             }
     const int ng = 2 * nsteps;
@@ -300,8 +300,9 @@ void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<
 
 bool balanced_gather_order(const uint32_t* pq, int n, int u, std::vector<int>& slot, int& nslots,
                            std::vector<int>& order, std::vector<uint8_t>& flip) {
-    constexpr int B = 32, STEPS = 128;
-    if (n != B * STEPS || u < B) return false;
+    constexpr int B = 32;
+    const int STEPS = n / B;  // positions per lane: 32, 64 or 128
+    if ((STEPS != 32 && STEPS != 64 && STEPS != 128) || n != B * STEPS || u < B) return false;
     // (1) offsets -> banks with exactly 2 * STEPS endpoint references per bank
     //     and at most `cap` offsets per bank (rank-table rows).
     std::vector<int> w(size_t(u), 0);
@@ -418,7 +419,7 @@ bool balanced_gather_order(const uint32_t* pq, int n, int u, std::vector<int>& s
             const int x = match_b[size_t(y)];
             const int i = ab[size_t(x) * B + y].back();
             ab[size_t(x) * B + y].pop_back();
-            const int pos = 128 * x + st;  // lane x, chunk st / 32, bit st % 32
+            const int pos = STEPS * x + st;  // lane x, chunk st / 32, bit st % 32
             order[size_t(pos)] = i;
             flip[size_t(pos)] = uint8_t(bank[pq[i] & 0xFFFFu] != x);  // P is not the lane's bank
         }

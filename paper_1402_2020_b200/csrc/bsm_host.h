@@ -49,17 +49,18 @@ namespace bsmh {
 // a permutation of [0, nslots) restricted to u entries, nslots >= u) chosen by
 // a deterministic local search that minimises the total wavefront count.
 // `cost_before` / `cost_after` receive the average wavefronts per gather.
-void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, std::vector<int>& slot, double* cost_before,
-                      double* cost_after);
+void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, int lane_pos, std::vector<int>& slot,
+                      double* cost_before, double* cost_after);
 
-// Conflict-free gather order for n = 4096 (k_mask4 / k_mask_f32): offsets are
-// spread over the 32 shared-memory banks with exactly 256 endpoint references
-// per bank, the pairs are oriented along Eulerian walks of the bank multigraph
-// (each bank: 128 "A" ends, 128 "B" ends) and the resulting 128-regular
-// bipartite multigraph is split into 128 perfect matchings.  Position
-// j = 128 l + 32 m + t holds pair order[j]; its A end lies in bank l and the
-// B ends of one step (m, t) lie in 32 distinct banks, so every 32-lane gather
-// is a single wavefront.  flip[j] = 1 when the A end is the pair's q.
+// Conflict-free gather order for n = 32 S, S in {32, 64, 128} positions per
+// lane (k_mask4 / k_mask_f32): offsets are spread over the 32 shared-memory
+// banks with exactly 2S endpoint references per bank, the pairs are oriented
+// along Eulerian walks of the bank multigraph (each bank: S "A" ends, S "B"
+// ends) and the resulting S-regular bipartite multigraph is split into S
+// perfect matchings.  Position j = S l + st holds pair order[j]; its A end
+// lies in bank l and the B ends of one step st lie in 32 distinct banks, so
+// every 32-lane gather is a single wavefront.  flip[j] = 1 when the A end is
+// the pair's q.
 // Returns false (outputs unspecified) when no such order was found.
 bool balanced_gather_order(const uint32_t* pq, int n, int u, std::vector<int>& slot, int& nslots,
                            std::vector<int>& order, std::vector<uint8_t>& flip);

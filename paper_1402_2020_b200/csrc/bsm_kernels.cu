@@ -352,21 +352,27 @@ constexpr int kM4Stage = 132;  // stage row stride (words): 16-B aligned, confli
 // strictly below it; the output words are (a <= T) = lt | eq.
 // Two selects in lockstep (the two pixels of a pass): the REDUX of one
 // overlaps the POPCs and the REDUX of the other.
-__device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][4], const uint32_t (&pb)[8][4], int k,
-                                           uint4& oa, uint4& ob) {
-    uint32_t ea[4] = {~0u, ~0u, ~0u, ~0u}, eb[4] = {~0u, ~0u, ~0u, ~0u};
-    uint32_t la[4] = {0u, 0u, 0u, 0u}, lb[4] = {0u, 0u, 0u, 0u};
+template <int MCH>
+__device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][MCH], const uint32_t (&pb)[8][MCH], int k,
+                                           uint32_t (&oa)[MCH], uint32_t (&ob)[MCH]) {
+    uint32_t ea[MCH], eb[MCH], la[MCH], lb[MCH];
+#pragma unroll
+    for (int m = 0; m < MCH; ++m) {
+        ea[m] = eb[m] = ~0u;
+        la[m] = lb[m] = 0u;
+    }
     int ka = k, kb = k;
 #pragma unroll
     for (int j = 7; j >= 0; --j) {
-        uint32_t za[4], zb[4];
+        uint32_t za[MCH], zb[MCH];
+        uint32_t ca = 0, cb = 0;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < MCH; ++m) {
             za[m] = ea[m] & ~pa[j][m];
             zb[m] = eb[m] & ~pb[j][m];
+            ca += __popc(za[m]);
+            cb += __popc(zb[m]);
         }
-        const uint32_t ca = uint32_t(__popc(za[0]) + __popc(za[1]) + __popc(za[2]) + __popc(za[3]));
-        const uint32_t cb = uint32_t(__popc(zb[0]) + __popc(zb[1]) + __popc(zb[2]) + __popc(zb[3]));
         const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
         const int zbs = int(__reduce_add_sync(0xFFFFFFFFu, cb));
         // warp-uniform choices; written as selects so both chains stay branch-free
@@ -374,17 +380,29 @@ __device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][4], const uin
         ka -= ha ? zas : 0;
         kb -= hb ? zbs : 0;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < MCH; ++m) {
             la[m] |= ha ? za[m] : 0u;
             ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
             lb[m] |= hb ? zb[m] : 0u;
             eb[m] = hb ? (eb[m] & pb[j][m]) : zb[m];
         }
     }
-    oa = make_uint4(la[0] | ea[0], la[1] | ea[1], la[2] | ea[2], la[3] | ea[3]);
-    ob = make_uint4(lb[0] | eb[0], lb[1] | eb[1], lb[2] | eb[2], lb[3] | eb[3]);
+#pragma unroll
+    for (int m = 0; m < MCH; ++m) {
+        oa[m] = la[m] | ea[m];
+        ob[m] = lb[m] | eb[m];
+    }
 }
 
+// Stores MCH consecutive words (16-, 8- or 4-byte aligned).
+template <int MCH>
+__device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[MCH]) {
+    if constexpr (MCH == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    else if constexpr (MCH == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+    else dst[0] = w[0];
+}
+
+template <int MCH>
 __global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
@@ -441,9 +459,9 @@ __global__ void __launch_bounds__(32, 16)
         }
         __syncwarp();
 
-        uint32_t pa[8][4], pb[8][4];
+        uint32_t pa[8][MCH], pb[8][MCH];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < MCH; ++m) {
             uint32_t wa[8], wb[8];
 #pragma unroll
             for (int t4 = 0; t4 < 8; ++t4) {
@@ -468,10 +486,10 @@ __global__ void __launch_bounds__(32, 16)
             }
         }
         __syncwarp();  // rho / rrows are rewritten by the next pass
-        uint4 oa, ob;
-        select_le2(pa, pb, k, oa, ob);
-        *reinterpret_cast<uint4*>(stage + q * kM4Stage + 4 * lane) = oa;
-        *reinterpret_cast<uint4*>(stage + (q + 1) * kM4Stage + 4 * lane) = ob;
+        uint32_t oa[MCH], ob[MCH];
+        select_le2<MCH>(pa, pb, k, oa, ob);
+        store_words<MCH>(stage + q * kM4Stage + MCH * lane, oa);
+        store_words<MCH>(stage + (q + 1) * kM4Stage + MCH * lane, ob);
     }
     __syncwarp();
     const int rem = n & 31;
@@ -564,6 +582,7 @@ __device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
     }
 }
 
+template <int MCH>
 __global__ void __launch_bounds__(32, 16)
     k_mask_f32(const float* __restrict__ lab, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
@@ -572,7 +591,7 @@ __global__ void __launch_bounds__(32, 16)
     // only the slot keys and the 16 KB of bit planes, for occupancy.
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
-    uint32_t* planes = tv + rho_words;                    // [32 planes][4 chunks][32 lanes]
+    uint32_t* planes = tv + rho_words;                    // [32 planes][MCH chunks][32 lanes]
     const int G = (n + 31) >> 5;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
@@ -600,7 +619,7 @@ __global__ void __launch_bounds__(32, 16)
         }
         __syncwarp();
 #pragma unroll 1
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < MCH; ++m) {
             uint32_t x[32];
 #pragma unroll
             for (int t4 = 0; t4 < 8; ++t4) {
@@ -613,39 +632,44 @@ __global__ void __launch_bounds__(32, 16)
             }
             transpose32(x);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) planes[(j * 4 + m) * 32 + lane] = x[j];
+            for (int j = 0; j < 32; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
         }
         __syncwarp();
         // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
         // the a <= T comparator fused in: where the threshold takes a 1, the
         // still-equal keys with a 0 there are strictly below it.
-        uint32_t eq[4] = {~0u, ~0u, ~0u, ~0u}, lt[4] = {0u, 0u, 0u, 0u};
+        uint32_t eq[MCH], lt[MCH];
+#pragma unroll
+        for (int m = 0; m < MCH; ++m) {
+            eq[m] = ~0u;
+            lt[m] = 0u;
+        }
         int kk = k;
 #pragma unroll 1
         for (int j = 31; j >= 0; --j) {
-            uint32_t pl[4], z[4];
+            uint32_t pl[MCH], z[MCH], cnt = 0;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                pl[m] = planes[(j * 4 + m) * 32 + lane];
+            for (int m = 0; m < MCH; ++m) {
+                pl[m] = planes[(j * MCH + m) * 32 + lane];
                 z[m] = eq[m] & ~pl[m];
+                cnt += __popc(z[m]);
             }
-            const int zeros = int(__reduce_add_sync(full, uint32_t(__popc(z[0]) + __popc(z[1]) + __popc(z[2]) +
-                                                                     __popc(z[3]))));
+            const int zeros = int(__reduce_add_sync(full, cnt));
             if (zeros >= kk) {
 #pragma unroll
-                for (int m = 0; m < 4; ++m) eq[m] = z[m];
+                for (int m = 0; m < MCH; ++m) eq[m] = z[m];
             } else {
                 kk -= zeros;
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
+                for (int m = 0; m < MCH; ++m) {
                     lt[m] |= z[m];
                     eq[m] &= pl[m];
                 }
             }
         }
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const int w = 4 * lane + m;
+        for (int m = 0; m < MCH; ++m) {
+            const int w = MCH * lane + m;
             if (w < NW) {
                 uint32_t v = lt[m] | eq[m];
                 if (w >= G) v = 0u;
@@ -1388,6 +1412,7 @@ struct bsm_ctx {
     int n = 0, window = 0, half = 0, NW = 0, u = 0, upad = 0;
     int mslots = 0;                 // rank-table slots used by the mask kernels
     std::vector<int> slot_used;     // slot -> used-offset index (-1: empty)
+    int mch = 4;                    // k_mask4 / k_mask_f32 chunks of 32 positions per lane (1, 2, 4)
     std::vector<int> order;         // bit position -> pair index (identity unless permuted)
     bool permuted = false;
     DevBuf d_pos;                   // pair index -> bit position (permuted only)
@@ -1571,13 +1596,17 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         dim3 grid(Wp / kMaskTile, rows);
         if (c->n <= 4096) {
             const size_t sm4 = mask4_smem(c);
-            BSM_CUDA(cudaFuncSetAttribute(k_mask4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
             dim3 grid3(Wp / kM3Px, rows);
-            k_mask4<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
-                                                   c->d_pqb.as<uint4>() + 1024, c->n,
-                                                   c->d_uoff.as<int32_t>(), c->mslots, round_up(c->mslots + 1, 4),
-                                                   c->d_rank.as<uint8_t>(),
-                                                   c->half, mask4_tw(c->half), c->NW, Wp, mask);
+            auto launch = [&](auto kern) -> int {
+                BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
+                kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+                                                    c->d_pqb.as<uint4>() + 1024, c->n, c->d_uoff.as<int32_t>(),
+                                                    c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
+                                                    c->half, mask4_tw(c->half), c->NW, Wp, mask);
+                return BSM_OK;
+            };
+            // chunks of 32 positions per lane: the work scales with n
+            BSM_TRY(c->mch == 1 ? launch(k_mask4<1>) : c->mch == 2 ? launch(k_mask4<2>) : launch(k_mask4<4>));
         } else {
             BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             k_mask<64><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
@@ -1704,7 +1733,7 @@ int ensure_descf_table(bsm_ctx* c) {
     return BSM_OK;
 }
 
-size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + 32 * 4 * 32 * 4; }
+size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(32) * c->mch * 32 * 4; }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, int ybeg, int rows,
@@ -1726,11 +1755,15 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
     {
         Scope s(c, T_MASK);
         const size_t sm = maskf_smem(c);
-        BSM_CUDA(cudaFuncSetAttribute(k_mask_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         dim3 grid(Wp / kM3Px, rows);
-        k_mask_f32<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
-                                                c->d_pqb.as<uint4>() + 1024, c->n, c->d_uxy.as<int32_t>(),
-                                                c->mslots, round_up(c->mslots + 1, 4), c->NW, Wp, mask);
+        auto launch = [&](auto kern) -> int {
+            BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+                                              c->d_pqb.as<uint4>() + 1024, c->n, c->d_uxy.as<int32_t>(), c->mslots,
+                                              round_up(c->mslots + 1, 4), c->NW, Wp, mask);
+            return BSM_OK;
+        };
+        BSM_TRY(c->mch == 1 ? launch(k_mask_f32<1>) : c->mch == 2 ? launch(k_mask_f32<2>) : launch(k_mask_f32<4>));
         BSM_TRY(check_launch(c, "mask_f32"));
     }
     return BSM_OK;
@@ -2039,23 +2072,29 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
     // Rank-table slot placement (k_mask4): minimise shared-memory bank
     // conflicts of the per-pair gathers; identity for the n > 4096 kernel.
-    // For n = 4096 a bank-balanced pair order (bsmh::balanced_gather_order)
-    // makes every gather conflict-free; the descriptor bits follow the same
-    // order (the masked Hamming cost is invariant under a common permutation
-    // of descriptor and mask bits) and the per-stage API un-permutes.
+    // k_mask4 / k_mask_f32 give each lane MCH chunks of 32 bit positions
+    // (lane l: positions 32*MCH*l ..), MCH the smallest of 1, 2, 4 that holds n.
+    // For n = 1024 * MCH a bank-balanced pair order
+    // (bsmh::balanced_gather_order) makes every gather conflict-free; the
+    // descriptor bits follow the same order (the masked Hamming cost is
+    // invariant under a common permutation of descriptor and mask bits) and
+    // the per-stage API un-permutes.
+    c->mch = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
+    const int lane_pos = 32 * c->mch;  // positions per lane
     std::vector<int> rslot(size_t(c->u));
     std::vector<uint8_t> flip;
     c->permuted = false;
     if (n <= 4096) {
         int ns = 0;
-        if (bsmh::balanced_gather_order(pq.data(), n, c->u, rslot, ns, c->order, flip)) {
+        if (n == 32 * lane_pos && bsmh::balanced_gather_order(pq.data(), n, c->u, rslot, ns, c->order, flip)) {
             c->permuted = true;
             c->mslots = ns;
             c->slot_cost[0] = c->slot_cost[1] = 1.0;
         } else {
             rslot.assign(size_t(c->u), 0);
             c->mslots = round_up(c->u, 32) + 32;
-            bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, rslot, &c->slot_cost[0], &c->slot_cost[1]);
+            bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, lane_pos, rslot, &c->slot_cost[0],
+                                   &c->slot_cost[1]);
         }
     } else {
         c->mslots = c->u;
@@ -2075,11 +2114,12 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
     // Byte offsets into the u32 rank table of each bit position's two
     // endpoints (k_mask4 / k_mask_f32): P table at [0, 4096), Q table at
-    // [4096, 8192), lane-block order -- lane l, chunk m, t: bit 128l + 32m + t
-    // at uint4 [(m*8 + t/4)*32 + l], component t%4.  Pads read the sentinel.
+    // [4096, 8192), lane-block order -- lane l, chunk m < MCH, t: bit
+    // 32*MCH*l + 32m + t at uint4 [(m*8 + t/4)*32 + l], component t%4.  Pads
+    // read the sentinel.
     std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->mslots));
     for (int j = 0; j < std::min(n, 4096); ++j) {
-        const int l = j >> 7, m = (j >> 5) & 3, t = j & 31;
+        const int l = j / lane_pos, m = (j >> 5) % c->mch, t = j & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
         const uint32_t e = pq[size_t(c->order[size_t(j)])];
         const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
