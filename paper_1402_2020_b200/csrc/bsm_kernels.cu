@@ -1583,7 +1583,9 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         const int TWs = desc4_tile_width(c->half);
         const size_t sm = size_t(TWs) * (kD2TY * kD2Rows + 2 * c->half) * 5 + 16;
         dim3 grid(Wp / (kD2TX * 4), (rows + kD2TY * kD2Rows - 1) / (kD2TY * kD2Rows));
-        grid.z = unsigned(std::max(1, std::min((c->NW + 7) / 8, (4 * c->sm_count + int(grid.x * grid.y) - 1) /
+        // split the word range over grid.z until there are ~16 CTAs per SM (the
+        // tail of a partial last wave dominates otherwise; c2: 759 -> 3036 CTAs)
+        grid.z = unsigned(std::max(1, std::min((c->NW + 7) / 8, (16 * c->sm_count + int(grid.x * grid.y) - 1) /
                                                                     int(grid.x * grid.y))));
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<int2>(),
