@@ -302,7 +302,7 @@ bool balanced_gather_order(const uint32_t* pq, int n, int u, std::vector<int>& s
                            std::vector<int>& order, std::vector<uint8_t>& flip) {
     constexpr int B = 32;
     const int STEPS = n / B;  // positions per lane: 32, 64 or 128
-    if ((STEPS != 32 && STEPS != 64 && STEPS != 128) || n != B * STEPS || u < B) return false;
+    if ((STEPS != 32 && STEPS != 64 && STEPS != 128 && STEPS != 256) || n != B * STEPS || u < B) return false;
     // (1) offsets -> banks with exactly 2 * STEPS endpoint references per bank
     //     and at most `cap` offsets per bank (rank-table rows).
     std::vector<int> w(size_t(u), 0);

@@ -52,7 +52,7 @@ namespace bsmh {
 void place_rank_slots(const uint32_t* pq, int n, int u, int nslots, int lane_pos, std::vector<int>& slot,
                       double* cost_before, double* cost_after);
 
-// Conflict-free gather order for n = 32 S, S in {32, 64, 128} positions per
+// Conflict-free gather order for n = 32 S, S in {32, 64, 128, 256} positions per
 // lane (k_mask4 / k_mask_f32): offsets are spread over the 32 shared-memory
 // banks with exactly 2S endpoint references per bank, the pairs are oriented
 // along Eulerian walks of the bank multigraph (each bank: S "A" ends, S "B"

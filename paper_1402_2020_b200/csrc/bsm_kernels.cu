@@ -154,129 +154,12 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
 }
 
 // ---------------------------------------------------------------------------
-// K2 -- mask.  descriptor.hpp:118-154 (mask_at_pixel), quarter_threshold
-// :64-76.  Warp per pixel.
-//   1. rho[k] = dense rank of lab_sad(centre, window pixel k) for the u window
-//      offsets the pattern uses (gray views: rank[c][v], a 256x256 host table,
-//      so the float order and ties of the reference are preserved exactly).
-//   2. lane l of group g holds a = max(rho[P], rho[Q]) of pair 32g + l: the
-//      rank of the reference's weight max(t[p], t[q]).  Four groups per
-//      register, split into even/odd byte halves (16-bit SWAR lanes).
-//   3. T = k-th smallest a, k = max(1, n/4), by an 8-step bisection over the
-//      byte range: count(a <= mid) via SWAR borrow tests + one REDUX per step.
-//   4. bit = a <= T (ties at T included, descriptor.hpp:153), one ballot per
-//      group of 32 pairs = one output word; staged per CTA, then stored as
-//      coalesced 128-B rows.
-// CTA = 8 warps x 4 pixels = 32 consecutive pixels of one row.
-constexpr int kMaskWarps = 8, kMaskPxPerWarp = 4, kMaskTile = kMaskWarps * kMaskPxPerWarp;
-
-template <int MAXG4>
-__global__ void __launch_bounds__(kMaskWarps * 32)
-    k_mask(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint32_t* __restrict__ pq,
-           int n, const int32_t* __restrict__ uoff, int u, int upad, const uint8_t* __restrict__ rank,
-           int half, int NW, int Wp, uint32_t* __restrict__ mask) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int TW = kMaskTile + 2 * half;
-    const int TH = 2 * half + 1;
-    const int G = (n + 31) >> 5;
-    uint32_t* s_pq = reinterpret_cast<uint32_t*>(smem);         // n
-    int32_t* s_uoff = reinterpret_cast<int32_t*>(s_pq + n);     // u
-    uint32_t* stage = reinterpret_cast<uint32_t*>(s_uoff + u);  // G * 32
-    uint8_t* rho_all = reinterpret_cast<uint8_t*>(stage + G * kMaskTile);  // warps * upad
-    uint8_t* tile = rho_all + kMaskWarps * upad;                           // TH * TW
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int x0 = blockIdx.x * kMaskTile;
-    const int ly = blockIdx.y;
-    const int y = ybeg + ly;
-    for (int i = tid; i < n; i += blockDim.x) s_pq[i] = pq[i];
-    for (int i = tid; i < u; i += blockDim.x) s_uoff[i] = uoff[i];
-    for (int idx = tid; idx < TW * TH; idx += blockDim.x) {
-        const int r = idx / TW, c = idx - r * TW;
-        const int gx = min(max(x0 - half + c, 0), W - 1);
-        const int gy = min(max(y - half + r, 0), H - 1);
-        tile[idx] = img[size_t(gy) * W + gx];
-    }
-    __syncthreads();
-
-    uint8_t* rho = rho_all + warp * upad;
-    const int k = max(1, n / 4);
-    for (int q = 0; q < kMaskPxPerWarp; ++q) {
-        const int px = warp * kMaskPxPerWarp + q;
-        const int ci = half * TW + half + px;
-        const uint8_t* rrow = rank + 256 * int(tile[ci]);
-        for (int j = lane; j < u; j += 32) rho[j] = __ldg(rrow + tile[ci + s_uoff[j]]);
-        __syncwarp();
-
-        uint32_t E[MAXG4], O[MAXG4];
-#pragma unroll
-        for (int j = 0; j < MAXG4; ++j) {
-            uint32_t r = 0xFFFFFFFFu;
-            if (4 * j < G) {
-                r = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int i = 32 * (4 * j + b) + lane;
-                    uint32_t a = 255;
-                    if (i < n) {
-                        const uint32_t e = s_pq[i];
-                        a = max(uint32_t(rho[e & 0xFFFF]), uint32_t(rho[e >> 16]));
-                    }
-                    r |= a << (8 * b);
-                }
-            }
-            E[j] = r & 0x00FF00FFu;
-            O[j] = (r >> 8) & 0x00FF00FFu;
-        }
-        // Smallest R with #{a <= R} >= k.  Pads (a = 255) are never counted:
-        // every probed mid is < 255.
-        int lo = 0, hi = 255;
-#pragma unroll 1
-        for (int it = 0; it < 8; ++it) {
-            const int mid = (lo + hi) >> 1;
-            const uint32_t T9 = uint32_t(0x100 + mid) * 0x00010001u;
-            uint32_t acc = 0;
-#pragma unroll
-            for (int j = 0; j < MAXG4; ++j) acc += ((T9 - E[j]) & 0x01000100u) + ((T9 - O[j]) & 0x01000100u);
-            const uint32_t cnt = __reduce_add_sync(0xFFFFFFFFu, ((acc & 0xFFFFu) + (acc >> 16)) >> 8);
-            if (int(cnt) >= k) hi = mid;
-            else lo = mid + 1;
-        }
-        const uint32_t T9 = uint32_t(0x100 + lo) * 0x00010001u;
-#pragma unroll
-        for (int j = 0; j < MAXG4; ++j) {
-            if (4 * j < G) {
-                const uint32_t fe = T9 - E[j], fo = T9 - O[j];
-                uint32_t wd[4];
-                wd[0] = __ballot_sync(0xFFFFFFFFu, fe & 0x100u);
-                wd[1] = __ballot_sync(0xFFFFFFFFu, fo & 0x100u);
-                wd[2] = __ballot_sync(0xFFFFFFFFu, fe & 0x1000000u);
-                wd[3] = __ballot_sync(0xFFFFFFFFu, fo & 0x1000000u);
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int g = 4 * j + b;
-                    if (g < G && lane == (g & 31)) {
-                        uint32_t v = wd[b];
-                        const int rem = n - 32 * g;
-                        if (rem < 32) v &= (1u << rem) - 1u;
-                        stage[g * kMaskTile + px] = v;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    for (int idx = tid; idx < NW * kMaskTile; idx += blockDim.x) {
-        const int w = idx / kMaskTile, j = idx - w * kMaskTile;
-        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = w < G ? stage[w * kMaskTile + j] : 0u;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Shared helpers of the n <= 4096 mask kernel (k_mask4): one warp per CTA,
-// kM3Px pixels per CTA, two pixels per pass.
+// K2 -- mask: shared helpers of k_mask4 (one warp per CTA, kM3Px pixels per
+// CTA, two pixels per pass).
 constexpr int kM3Px = 8;
+// rank-gather index tables (u32 byte offsets): P table, then Q table, each
+// sized for MCH = 8 chunks (8192 positions)
+constexpr int kPqTable = 8192;
 
 __device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
     uint32_t r;
@@ -344,7 +227,6 @@ __device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t
     }
 }
 
-constexpr int kM4Stage = 132;  // stage row stride (words): 16-B aligned, conflict-free read-out
 
 // MSB-first k-th-smallest selection over 8 bit planes (4 words per lane,
 // 128 values per lane, 4096 per warp) fused with the comparator: at a bit
@@ -397,10 +279,49 @@ __device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][MCH], const u
 // Stores MCH consecutive words (16-, 8- or 4-byte aligned).
 template <int MCH>
 __device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[MCH]) {
-    if constexpr (MCH == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    if constexpr (MCH == 8) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(dst + 4) = make_uint4(w[4], w[5], w[6], w[7]);
+    } else if constexpr (MCH == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
     else if constexpr (MCH == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
     else dst[0] = w[0];
 }
+
+// One pixel's select (the split variant for MCH = 8, where two pixels' planes
+// would not fit the register budget).
+template <int MCH>
+__device__ __forceinline__ void select_le1(const uint32_t (&pa)[8][MCH], int k, uint32_t (&oa)[MCH]) {
+    uint32_t ea[MCH], la[MCH];
+#pragma unroll
+    for (int m = 0; m < MCH; ++m) {
+        ea[m] = ~0u;
+        la[m] = 0u;
+    }
+    int ka = k;
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+        uint32_t za[MCH], ca = 0;
+#pragma unroll
+        for (int m = 0; m < MCH; ++m) {
+            za[m] = ea[m] & ~pa[j][m];
+            ca += __popc(za[m]);
+        }
+        const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
+        const bool ha = zas < ka;
+        ka -= ha ? zas : 0;
+#pragma unroll
+        for (int m = 0; m < MCH; ++m) {
+            la[m] |= ha ? za[m] : 0u;
+            ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < MCH; ++m) oa[m] = la[m] | ea[m];
+}
+
+// Output staging row stride (words) of k_mask4<MCH>: 32 MCH words per pixel +
+// 4 of padding (16-B aligned rows, conflict-free read-out).
+__host__ __device__ constexpr int mask4_stage_stride(int mch) { return 32 * mch + 4; }
 
 template <int MCH>
 __global__ void __launch_bounds__(32, 16)
@@ -409,8 +330,9 @@ __global__ void __launch_bounds__(32, 16)
             const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
-    uint32_t* stage = rho + rho_words;                    // [kM3Px][kM4Stage]
-    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * kM4Stage);  // 2 x 256
+    constexpr int STG = mask4_stage_stride(MCH);
+    uint32_t* stage = rho + rho_words;                    // [kM3Px][STG]
+    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * STG);  // 2 x 256
     uint8_t* tile = rrows + 512;                                            // (2h+1) x TW
     const int G = (n + 31) >> 5;
     const int TH = 2 * half + 1;
@@ -459,10 +381,9 @@ __global__ void __launch_bounds__(32, 16)
         }
         __syncwarp();
 
-        uint32_t pa[8][MCH], pb[8][MCH];
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            uint32_t wa[8], wb[8];
+        // a = max(rhoP, rhoQ) of 32 positions of chunk m for both pixels, as
+        // byte registers wa (pixel A) and wb (pixel B)
+        auto gather = [&](int m, uint32_t(&wa)[8], uint32_t(&wb)[8]) {
 #pragma unroll
             for (int t4 = 0; t4 < 8; ++t4) {
                 const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
@@ -476,20 +397,44 @@ __global__ void __launch_bounds__(32, 16)
                 wa[t4] = __byte_perm(x01, x23, 0x5410);
                 wb[t4] = __byte_perm(x01, x23, 0x7632);
             }
-            uint32_t ta[8], tb[8];
-            bytes_to_planes(wa, ta);
-            bytes_to_planes(wb, tb);
+        };
+        if constexpr (MCH <= 4) {
+            uint32_t pa[8][MCH], pb[8][MCH];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                pa[j][m] = ta[j];
-                pb[j][m] = tb[j];
+            for (int m = 0; m < MCH; ++m) {
+                uint32_t wa[8], wb[8], ta[8], tb[8];
+                gather(m, wa, wb);
+                bytes_to_planes(wa, ta);
+                bytes_to_planes(wb, tb);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    pa[j][m] = ta[j];
+                    pb[j][m] = tb[j];
+                }
+            }
+            uint32_t oa[MCH], ob[MCH];
+            select_le2<MCH>(pa, pb, k, oa, ob);
+            store_words<MCH>(stage + q * STG + MCH * lane, oa);
+            store_words<MCH>(stage + (q + 1) * STG + MCH * lane, ob);
+        } else {
+            // one pixel's planes at a time: the gathers run twice
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side) {
+                uint32_t pl[8][MCH];
+#pragma unroll
+                for (int m = 0; m < MCH; ++m) {
+                    uint32_t wa[8], wb[8], t[8];
+                    gather(m, wa, wb);
+                    bytes_to_planes(side ? wb : wa, t);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) pl[j][m] = t[j];
+                }
+                uint32_t o[MCH];
+                select_le1<MCH>(pl, k, o);
+                store_words<MCH>(stage + (q + side) * STG + MCH * lane, o);
             }
         }
         __syncwarp();  // rho / rrows are rewritten by the next pass
-        uint32_t oa[MCH], ob[MCH];
-        select_le2<MCH>(pa, pb, k, oa, ob);
-        store_words<MCH>(stage + q * kM4Stage + MCH * lane, oa);
-        store_words<MCH>(stage + (q + 1) * kM4Stage + MCH * lane, ob);
     }
     __syncwarp();
     const int rem = n & 31;
@@ -497,7 +442,7 @@ __global__ void __launch_bounds__(32, 16)
         const int w = idx / kM3Px, j = idx - w * kM3Px;
         uint32_t v = 0;
         if (w < G) {
-            v = stage[j * kM4Stage + w];
+            v = stage[j * STG + w];
             if (rem && w == G - 1) v &= (1u << rem) - 1u;
         }
         mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
@@ -1409,7 +1354,7 @@ struct bsm_ctx {
     cudaStream_t stream = nullptr;
     int sm_count = 0;
     // pattern
-    int n = 0, window = 0, half = 0, NW = 0, u = 0, upad = 0;
+    int n = 0, window = 0, half = 0, NW = 0, u = 0;
     int mslots = 0;                 // rank-table slots used by the mask kernels
     std::vector<int> slot_used;     // slot -> used-offset index (-1: empty)
     int mch = 4;                    // k_mask4 / k_mask_f32 chunks of 32 positions per lane (1, 2, 4)
@@ -1420,7 +1365,7 @@ struct bsm_ctx {
     std::vector<int16_t> pairs;
     std::vector<int2> pair_xy;  // (px,py),(qx,qy) packed later per tile width
     std::vector<int16_t> used;  // used offsets as dy*(2h+1)+dx index list (host)
-    DevBuf d_desc4, d_pq, d_pqb, d_uoff, d_uxy;
+    DevBuf d_desc4, d_pqb, d_uoff, d_uxy;
     DevBuf d_descf, d_rgb_gray, d_rgb_lab, planes;
     int descf_tw = -1;
     bool rgb_ready = false;
@@ -1560,15 +1505,10 @@ int check_pattern(bsm_ctx* c) {
 }
 
 
-size_t mask_smem(const bsm_ctx* c) {
-    const int TW = kMaskTile + 2 * c->half, TH = 2 * c->half + 1, G = (c->n + 31) / 32;
-    return size_t(c->n) * 4 + size_t(c->u) * 4 + size_t(G) * kMaskTile * 4 + size_t(kMaskWarps) * c->upad +
-           size_t(TW) * TH;
-}
 
 size_t mask4_smem(const bsm_ctx* c) {
     const int TW = mask4_tw(c->half), TH = 2 * c->half + 1;
-    return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * kM4Stage * 4 + 512 +
+    return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * mask4_stage_stride(c->mch) * 4 + 512 +
            size_t(TW) * TH;
 }
 
@@ -1576,7 +1516,7 @@ size_t mask4_smem(const bsm_ctx* c) {
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
     const int Wp = round_up(W, 128);
-    BSM_TRY(ensure_mask_offsets(c, c->n <= 4096 ? mask4_tw(c->half) : kMaskTile + 2 * c->half));
+    BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
         BSM_TRY(ensure_desc4_table(c));
@@ -1594,27 +1534,21 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
     }
     {
         Scope s(c, T_MASK);
-        const size_t sm = mask_smem(c);
-        dim3 grid(Wp / kMaskTile, rows);
-        if (c->n <= 4096) {
-            const size_t sm4 = mask4_smem(c);
-            dim3 grid3(Wp / kM3Px, rows);
-            auto launch = [&](auto kern) -> int {
-                BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
-                kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
-                                                    c->d_pqb.as<uint4>() + 1024, c->n, c->d_uoff.as<int32_t>(),
-                                                    c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
-                                                    c->half, mask4_tw(c->half), c->NW, Wp, mask);
-                return BSM_OK;
-            };
-            // chunks of 32 positions per lane: the work scales with n
-            BSM_TRY(c->mch == 1 ? launch(k_mask4<1>) : c->mch == 2 ? launch(k_mask4<2>) : launch(k_mask4<4>));
-        } else {
-            BSM_CUDA(cudaFuncSetAttribute(k_mask<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            k_mask<64><<<grid, kMaskWarps * 32, sm, c->stream>>>(img, W, H, ybeg, rows, c->d_pq.as<uint32_t>(), c->n,
-                                                                 c->d_uoff.as<int32_t>(), c->u, c->upad,
-                                                                 c->d_rank.as<uint8_t>(), c->half, c->NW, Wp, mask);
-        }
+        const size_t sm4 = mask4_smem(c);
+        dim3 grid3(Wp / kM3Px, rows);
+        auto launch = [&](auto kern) -> int {
+            BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
+            kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+                                                c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<int32_t>(),
+                                                c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
+                                                c->half, mask4_tw(c->half), c->NW, Wp, mask);
+            return BSM_OK;
+        };
+        // chunks of 32 positions per lane: the work scales with n
+        BSM_TRY(c->mch == 1   ? launch(k_mask4<1>)
+                : c->mch == 2 ? launch(k_mask4<2>)
+                : c->mch == 4 ? launch(k_mask4<4>)
+                              : launch(k_mask4<8>));
         BSM_TRY(check_launch(c, "mask"));
     }
     return BSM_OK;
@@ -1740,7 +1674,6 @@ size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, int ybeg, int rows,
                      uint32_t* desc, uint32_t* mask) {
-    if (c->n > 4096) return set_err(BSM_UNSUPPORTED, "bsm: float-plane (colour) fields support n <= 4096");
     const int Wp = round_up(W, 128);
     BSM_TRY(ensure_descf_table(c));
     BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
@@ -1761,11 +1694,14 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
-                                              c->d_pqb.as<uint4>() + 1024, c->n, c->d_uxy.as<int32_t>(), c->mslots,
+                                              c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uxy.as<int32_t>(), c->mslots,
                                               round_up(c->mslots + 1, 4), c->NW, Wp, mask);
             return BSM_OK;
         };
-        BSM_TRY(c->mch == 1 ? launch(k_mask_f32<1>) : c->mch == 2 ? launch(k_mask_f32<2>) : launch(k_mask_f32<4>));
+        BSM_TRY(c->mch == 1   ? launch(k_mask_f32<1>)
+                : c->mch == 2 ? launch(k_mask_f32<2>)
+                : c->mch == 4 ? launch(k_mask_f32<4>)
+                              : launch(k_mask_f32<8>));
         BSM_TRY(check_launch(c, "mask_f32"));
     }
     return BSM_OK;
@@ -1999,7 +1935,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pq, &c->d_pqb, &c->d_uoff, &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col,
+    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pqb, &c->d_uoff, &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col,
                       &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
@@ -2069,9 +2005,6 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
         pq[size_t(i)] = uint32_t(idx[0]) | (uint32_t(idx[1]) << 16);
     }
     c->u = int(c->used.size());
-    c->upad = round_up(c->u, 16);
-    BSM_TRY(c->d_pq.ensure(pq.size() * 4));
-    BSM_CUDA(cudaMemcpy(c->d_pq.p, pq.data(), pq.size() * 4, cudaMemcpyHostToDevice));
     // Rank-table slot placement (k_mask4): minimise shared-memory bank
     // conflicts of the per-pair gathers; identity for the n > 4096 kernel.
     // k_mask4 / k_mask_f32 give each lane MCH chunks of 32 bit positions
@@ -2081,12 +2014,12 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     // descriptor bits follow the same order (the masked Hamming cost is
     // invariant under a common permutation of descriptor and mask bits) and
     // the per-stage API un-permutes.
-    c->mch = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
+    c->mch = n <= 1024 ? 1 : n <= 2048 ? 2 : n <= 4096 ? 4 : 8;
     const int lane_pos = 32 * c->mch;  // positions per lane
     std::vector<int> rslot(size_t(c->u));
     std::vector<uint8_t> flip;
     c->permuted = false;
-    if (n <= 4096) {
+    {
         int ns = 0;
         if (n == 32 * lane_pos && bsmh::balanced_gather_order(pq.data(), n, c->u, rslot, ns, c->order, flip)) {
             c->permuted = true;
@@ -2098,9 +2031,6 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
             bsmh::place_rank_slots(pq.data(), n, c->u, c->mslots, lane_pos, rslot, &c->slot_cost[0],
                                    &c->slot_cost[1]);
         }
-    } else {
-        c->mslots = c->u;
-        for (int o = 0; o < c->u; ++o) rslot[size_t(o)] = o;
     }
     if (!c->permuted) {
         c->order.resize(size_t(n));
@@ -2115,25 +2045,25 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     c->slot_used.assign(size_t(c->mslots), -1);
     for (int o = 0; o < c->u; ++o) c->slot_used[size_t(rslot[size_t(o)])] = o;
     // Byte offsets into the u32 rank table of each bit position's two
-    // endpoints (k_mask4 / k_mask_f32): P table at [0, 4096), Q table at
-    // [4096, 8192), lane-block order -- lane l, chunk m < MCH, t: bit
-    // 32*MCH*l + 32m + t at uint4 [(m*8 + t/4)*32 + l], component t%4.  Pads
-    // read the sentinel.
-    std::vector<uint32_t> pqb(2 * 4096, uint32_t(4 * c->mslots));
-    for (int j = 0; j < std::min(n, 4096); ++j) {
+    // endpoints (k_mask4 / k_mask_f32): P table at [0, kPqTable), Q table at
+    // [kPqTable, 2 kPqTable), lane-block order -- lane l, chunk m < MCH, t:
+    // bit 32*MCH*l + 32m + t at uint4 [(m*8 + t/4)*32 + l], component t%4.
+    // Pads read the sentinel.
+    std::vector<uint32_t> pqb(2 * kPqTable, uint32_t(4 * c->mslots));
+    for (int j = 0; j < n; ++j) {
         const int l = j / lane_pos, m = (j >> 5) % c->mch, t = j & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
         const uint32_t e = pq[size_t(c->order[size_t(j)])];
         const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
         pqb[at] = uint32_t(4 * rslot[size_t(a)]);
-        pqb[4096 + at] = uint32_t(4 * rslot[size_t(b)]);
+        pqb[kPqTable + at] = uint32_t(4 * rslot[size_t(b)]);
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
     c->desc4_tw = -1;
     c->descf_tw = -1;
     c->uoff_tw = -1;
-    if (mask_smem(c) > 200 * 1024 || mask4_smem(c) > 200 * 1024 || (n <= 4096 && maskf_smem(c) > 200 * 1024))
+    if (mask4_smem(c) > 200 * 1024 || maskf_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
     return BSM_OK;
 }
@@ -2165,7 +2095,6 @@ int bsm_compute_field_u8(bsm_ctx* c, const uint8_t* img, int W, int H, uint64_t*
     BSM_TRY(field_device(c, c->img_l.as<uint8_t>(), W, H, 0, H, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
     const size_t aos = size_t(H) * W * c->NW;
     BSM_TRY(c->aux0.ensure(aos * 4));
-    const int tb = 256;
     for (int which = 0; which < 2; ++which) {
         uint64_t* dst = which == 0 ? desc : mask;
         if (!dst) continue;
@@ -2478,7 +2407,6 @@ int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W
     BSM_TRY(field_device_f32(c, g, l, W, H, 0, H, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
     const size_t aos = size_t(H) * W * c->NW;
     BSM_TRY(c->aux0.ensure(aos * 4));
-    const int tb = 256;
     for (int which = 0; which < 2; ++which) {
         uint64_t* dst = which == 0 ? desc : mask;
         if (!dst) continue;
