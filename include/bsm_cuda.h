@@ -108,7 +108,7 @@ int bsm_vote_refine_lab(bsm_ctx* ctx, const float* d, const uint8_t* v, const fl
                         double lambda_c, double lambda_e, int vote_radius, float* out_d, uint8_t* out_v);
 
 /* compute_field (descriptor.hpp:200-239) of arbitrary float planes (a
- * GrayImage and a LabImage, e.g. of a colour view); n <= 4096. */
+ * GrayImage and a LabImage, e.g. of a colour view). */
 int bsm_compute_field_f32(bsm_ctx* ctx, const float* gray, const float* lab, int W, int H, uint64_t* desc,
                           uint64_t* mask);
 

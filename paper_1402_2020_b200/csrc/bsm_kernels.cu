@@ -172,8 +172,8 @@ __device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_
 }
 
 // ---------------------------------------------------------------------------
-// K2'' -- mask for n <= 4096 on bit planes.  Lane l owns bit positions
-// [128l, 128l + 128) in four chunks of 32 (the pair at each position comes
+// K2'' -- mask on bit planes.  Lane l owns bit positions [S l, S l + S) in
+// MCH chunks of 32 (S = 32 MCH; MCH = 1, 2, 4, 8 for n <= 1024 .. 8192) (the pair at each position comes
 // from the bank-balanced order, so every 32-lane rank gather is one
 // shared-memory wavefront); for two pixels per pass it
 //   1. gathers a = max(rhoP, rhoQ) of both pixels per pair (one u32 rank-table
@@ -2006,7 +2006,7 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     }
     c->u = int(c->used.size());
     // Rank-table slot placement (k_mask4): minimise shared-memory bank
-    // conflicts of the per-pair gathers; identity for the n > 4096 kernel.
+    // conflicts of the per-pair gathers.
     // k_mask4 / k_mask_f32 give each lane MCH chunks of 32 bit positions
     // (lane l: positions 32*MCH*l ..), MCH the smallest of 1, 2, 4 that holds n.
     // For n = 1024 * MCH a bank-balanced pair order
