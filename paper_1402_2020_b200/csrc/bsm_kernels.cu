@@ -173,16 +173,16 @@ __device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_
 
 // ---------------------------------------------------------------------------
 // K2'' -- mask on bit planes.  Lane l owns bit positions [S l, S l + S) in
-// MCH chunks of 32 (S = 32 MCH; MCH = 1, 2, 4, 8 for n <= 1024 .. 8192) (the pair at each position comes
-// from the bank-balanced order, so every 32-lane rank gather is one
-// shared-memory wavefront); for two pixels per pass it
+// MCH chunks of 32 (S = 32 MCH; MCH = 1, 2, 4, 8 for n <= 1024 .. 8192; the
+// pair at each position comes from the bank-balanced order, so every 32-lane
+// rank gather is one shared-memory wavefront); for two pixels per pass it
 //   1. gathers a = max(rhoP, rhoQ) of both pixels per pair (one u32 rank-table
 //      gather + VIMNMX.U16x2 serves both), packs each pixel's 32 chunk values
 //      into eight byte registers,
 //   2. transposes them into 8 bit planes held in registers (four 8x8 bit-matrix
 //      transposes and a 4x4 byte transpose): plane j, word m of lane l holds
-//      bit j of a for positions 128l + 32m + t at bit t -- exactly the layout
-//      of output word 4l + m,
+//      bit j of a for positions S l + 32m + t at bit t -- exactly the layout
+//      of output word MCH l + m (MCH = 8 forms one pixel's planes at a time),
 //   3. selects the k-th smallest a MSB-first on the planes (per bit: LOP3 +
 //      POPC per word, one REDUX; the two pixels in lockstep) with the a <= T
 //      comparator fused in, and stages one uint4 of output words per lane.
@@ -2005,10 +2005,10 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
         pq[size_t(i)] = uint32_t(idx[0]) | (uint32_t(idx[1]) << 16);
     }
     c->u = int(c->used.size());
-    // Rank-table slot placement (k_mask4): minimise shared-memory bank
-    // conflicts of the per-pair gathers.
     // k_mask4 / k_mask_f32 give each lane MCH chunks of 32 bit positions
-    // (lane l: positions 32*MCH*l ..), MCH the smallest of 1, 2, 4 that holds n.
+    // (lane l: positions 32*MCH*l ..), MCH the smallest of 1, 2, 4, 8 that
+    // holds n.  Otherwise the rank-table slots are placed by local search to
+    // limit the gathers' bank conflicts.
     // For n = 1024 * MCH a bank-balanced pair order
     // (bsmh::balanced_gather_order) makes every gather conflict-free; the
     // descriptor bits follow the same order (the masked Hamming cost is
