@@ -127,3 +127,57 @@ def test_radiometric_protocol_matches_reference(ref, rio, default_pairs):
             assert m.rate[i][j] == want
     dg, od = rio.radiometric(None, np.array(m.rate))
     assert (m.diagonal_mean(), m.off_diagonal_mean()) == (dg, od)
+
+
+def _write_scene(root, L, R, gt, scale):
+    os.makedirs(root, exist_ok=True)
+    bio.save_ppm(np.repeat(L[:, :, None], 3, 2) if L.ndim == 2 else L, os.path.join(root, "im2.ppm"))
+    bio.save_ppm(np.repeat(R[:, :, None], 3, 2) if R.ndim == 2 else R, os.path.join(root, "im6.ppm"))
+    bio.save_disparity(gt, os.path.join(root, "disp2.pgm"), scale)
+    mask = np.full(L.shape[:2] + (3,), 255, np.uint8)
+    mask[:, :12] = 0
+    bio.save_ppm(mask, os.path.join(root, "nonocc.ppm"))
+
+
+@pytest.mark.parametrize("impl", ["python", "cpp"])
+def test_cli_sweep_and_radiometric(tmp_path, impl):
+    # a scene directory in the stock layout and a 3-condition radiometric set
+    L, R, g = _scene(21)
+    scene = str(tmp_path / "scene")
+    _write_scene(scene, L, R, g, 4.0)
+    os.rename(os.path.join(scene, "nonocc.ppm"), os.path.join(scene, "nonocc.pgm.tmp"))
+    m = bio.load_image(os.path.join(scene, "nonocc.pgm.tmp"))
+    (tmp_path / "scene" / "nonocc.pgm").write_bytes(b"P5\n%d %d\n255\n" % (m.shape[1], m.shape[0]) +
+                                                    m[:, :, 0].tobytes())
+    os.remove(os.path.join(scene, "nonocc.pgm.tmp"))
+    out = str(tmp_path / "sweep.csv")
+    r = _cli("sweep", scene, "--d_max", "60", "--gt_scale", "4", "--n_values", "256,1024", "--out", out, impl=impl)
+    assert r.returncode == 0, r.stderr
+    lines = open(out).read().splitlines()
+    assert lines[0] == "n,avg_error,wall_time" and [ln.split(",")[0] for ln in lines[1:]] == ["256", "1024"]
+    # the sweep's error column equals the evaluation layer on the same scene
+    ds = bio.load_stereo_dataset(scene, "scene", 60, 4.0)
+    pts = ev.length_sweep([ev.SweepScene(ds.left, ds.right, ds.gt, ds.mask_nonocc, 60)], [256, 1024],
+                          bsm.BsmConfig(d_max=60, gt_scale=4.0))
+    assert [ln.split(",")[1] for ln in lines[1:]] == ["%.6f" % p.avg_error for p in pts]
+    assert "linear fit of time vs n" in r.stdout and os.path.exists(out + ".config.json")
+
+    rset = str(tmp_path / "rad")
+    os.makedirs(rset)
+    curves = [lambda x: x, lambda x: np.clip(x.astype(np.int32) * 3 // 4 + 40, 0, 255).astype(np.uint8),
+              lambda x: (255.0 * (x / 255.0) ** 0.7).round().astype(np.uint8)]
+    for c, f in enumerate(curves):
+        for side, img in (("left", L), ("right", R)):
+            v = f(img)
+            (tmp_path / "rad" / f"{side}_c{c}.pgm").write_bytes(b"P5\n%d %d\n255\n" % (v.shape[1], v.shape[0]) +
+                                                                v.tobytes())
+    bio.save_disparity(g, os.path.join(rset, "gt.pgm"), 4.0)
+    out = str(tmp_path / "rad.csv")
+    r = _cli("radiometric", rset, "--d_max", "60", "--gt_scale", "4", "--out", out, impl=impl)
+    assert r.returncode == 0, r.stderr
+    rs = bio.load_radiometric_set(rset, 60, 4.0)
+    m = ev.radiometric_protocol(rs.lefts, rs.rights, rs.gt, None, bsm.generate_pattern(), bsm.BsmConfig(d_max=60))
+    want = ["left_condition,right_condition,bad_pixel_rate"] + \
+        ["%d,%d,%.6f" % (i, j, m.rate[i][j]) for i in range(3) for j in range(3)]
+    assert open(out).read().splitlines() == want
+    assert ("diagonal mean %.2f, off-diagonal mean %.2f" % (m.diagonal_mean(), m.off_diagonal_mean())) in r.stdout
