@@ -9,7 +9,9 @@
 //   shared-memory read is a conflict-free 16-B lane-contiguous LDS.128.
 //   u32 word w of a pixel = bits 32w..32w+31 = the low/high half of the
 //   reference's u64 word w>>1 (bitstring.hpp:47-51).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -626,99 +628,88 @@ __global__ void __launch_bounds__(32, 16)
     }
 }
 
+// --- TMA staging helpers (cp.async.bulk.tensor + mbarrier) ----------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 3-D box (x, word, row) of a field into shared memory, completing on bar.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int w, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(w), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
 // (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
 // :68-75 (ties -> smaller d).  No cost volume is materialised.
 // CTA tile: 128 reference pixels of one row x 64 disparities; 8 warps, warp wi
 // owns disparities [d0 + 8wi, +8), lane l owns pixels [x0 + 4l, +4): a 4 x 8
-// register block of costs, so each staged word feeds 32 LOP3+POPC+IADD from
-// 5 LDS.128 (ref desc, ref mask, a 12-word window of the other view).
-// Words stream through a 3-stage cp.async ring of K = 8 words
-// ([8 x 128] desc, [8 x 128] mask, [8 x 192] other-view span).  The argmin
-// key is (cost << 16) | d (min cost, then smaller d); d-split CTAs merge
-// with atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
-__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr, bool valid) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_ptr));
-    const int sz = valid ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gptr), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
+// register block of costs, so each staged word feeds 32 word-ops from 5
+// LDS.128 (ref desc, ref mask, a 12-word window of the other view).
+// Words stream through a 3-stage ring of K = 16 words filled by TMA: one
+// thread arms the stage's mbarrier and issues three tensor-box copies
+// ([K x 128] desc, [K x 128] mask, [K x 192] other-view span); columns and
+// words outside the field arrive zero-filled, so the load path carries no
+// per-thread predicates or address arithmetic.  The argmin key is
+// (cost << 16) | d (min cost, then smaller d); d-split CTAs merge with
+// atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
 template <bool RIGHT, bool MASKED>
 __global__ void __launch_bounds__(256, 2)
-    k_cost_wta(const uint32_t* __restrict__ dref, const uint32_t* __restrict__ mref,
-               const uint32_t* __restrict__ doth, int W, int rows, int NW, int Wp, int D,
-               uint32_t* __restrict__ keys, uint32_t two) {
-    // `two` == 2 at run time: a register multiplier keeps the carry-save
-    // accumulate an IMAD (FMA pipe) instead of an IADD3 (ALU pipe).
+    k_cost_wta(const __grid_constant__ CUtensorMap tm_ref, const __grid_constant__ CUtensorMap tm_mask,
+                   const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
+                   uint32_t* __restrict__ keys, uint32_t two) {
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
-    constexpr int SA = K * T, SB = K * BW;                 // words per stage
+    constexpr int SA = K * T, SB = K * BW;
     constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
-    extern __shared__ __align__(16) uint32_t csm[];       // ST x {a, m, b} + red
-    uint32_t* red = csm + ST * STAGE;                      // [8][T]
+    constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * 4;
+    extern __shared__ __align__(128) uint32_t csm[];
+    uint32_t* red = csm + ST * STAGE;                                 // [8][T]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full barriers
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    // grid = (d-chunks, x-tiles, rows): the CTAs sharing a tile's reference
-    // words (same x-tile, different d) run back to back and hit in L2.
     const int x0 = blockIdx.y * T;
     const int y = blockIdx.z;
     const int d0 = blockIdx.x * DC;
     const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
     const int nchunks = (NW + K - 1) / K;
-    // Tiles with no in-range (x, d) at all (d >= D, or every correspondence
-    // outside the image, matcher.hpp:100) exit before loading anything.
     const int xhi = min(x0 + T, W) - 1;
     if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
 
-    // Per-thread copy assignments, fixed for all stages: a/m rows (tid>>5) and
-    // (tid>>5)+8, column 4*(tid&31); three 16-B chunks of the other-view span.
-    constexpr int NB = (SB / 4 + 255) / 256;
-    const int aw = tid >> 5, acol = (tid & 31) * 4;
-    const uint32_t* ga = dref + (size_t(y) * NW + aw) * Wp + x0 + acol;
-    const uint32_t* gm = MASKED ? mref + (size_t(y) * NW + aw) * Wp + x0 + acol : nullptr;
-    int bw[NB], bcol[NB];
-    bool bok[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        const int t = tid + 256 * i;
-        bw[i] = t / (BW / 4);
-        bcol[i] = (t - bw[i] * (BW / 4)) * 4;
-        const int gcol = bbase + bcol[i];
-        bok[i] = t < SB / 4 && gcol >= 0 && gcol < Wp;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    const uint32_t* gb = doth + size_t(y) * NW * Wp + bbase;
-
-    auto load_stage = [&](int c, int st) {
-        const int w0 = c * K;
+    __syncthreads();
+    auto load_stage = [&](int c, int st) {  // thread 0 only
         uint32_t* s = csm + st * STAGE;
-#pragma unroll
-        for (int h = 0; h < K / 8; ++h) {
-            const int w = aw + 8 * h;
-            const bool ok = w0 + w < NW;
-            const size_t off = size_t(w0 + 8 * h) * Wp;
-            cp_async16(s + w * T + acol, ok ? ga + off : dref, ok);
-            if constexpr (MASKED) cp_async16(s + SA + w * T + acol, ok ? gm + off : mref, ok);
-        }
-        uint32_t* sb = s + (MASKED ? 2 * SA : SA);
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            if (tid + 256 * i < SB / 4) {
-                const bool ok = bok[i] && w0 + bw[i] < NW;
-                cp_async16(sb + bw[i] * BW + bcol[i], ok ? gb + size_t(w0 + bw[i]) * Wp + bcol[i] : doth, ok);
-            }
-        }
+        mbar_expect_tx(bars + st, STAGE_BYTES);
+        tma_load_3d(s, &tm_ref, x0, c * K, y, bars + st);
+        if constexpr (MASKED) tma_load_3d(s + SA, &tm_mask, x0, c * K, y, bars + st);
+        tma_load_3d(s + (MASKED ? 2 * SA : SA), &tm_oth, bbase, c * K, y, bars + st);
     };
-
-#pragma unroll
-    for (int s = 0; s < ST - 1; ++s) {
-        if (s < nchunks) load_stage(s, s);
-        cp_async_commit();
-    }
+    if (tid == 0)
+        for (int s = 0; s < ST - 1 && s < nchunks; ++s) load_stage(s, s);
 
     uint32_t acc[4][8], ones[4][8];
 #pragma unroll
@@ -732,24 +723,17 @@ __global__ void __launch_bounds__(256, 2)
     const int xs = lane * 4;
     const int ds = wi * 8;
     const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
-    // A warp whose 128 x 8 block has no in-range (x, d) only helps stage the
-    // tiles; its compute is skipped (warp-uniform).
     const bool busy = d0 + ds < D && (RIGHT ? x0 + d0 + ds < W : xhi >= d0 + ds);
 
 #pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
-        cp_async_wait<ST - 2>();
-        __syncthreads();
-        if (c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
-        cp_async_commit();
+        mbar_wait(bars + c % ST, uint32_t(c / ST) & 1u);
+        __syncthreads();  // every warp is done with stage (c - 1) % ST before it is refilled
+        if (tid == 0 && c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
         if (!busy) continue;
         const uint32_t* sa = csm + (c % ST) * STAGE;
         const uint32_t* sm = sa + SA;
         const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
-        // Two words per step through a carry-save accumulator (Harley-Seal
-        // with one level): ones' = ones ^ x0 ^ x1, twos = maj(ones, x0, x1),
-        // acc += 2 * popc(twos).  One POPC per two words instead of two; the
-        // LOP3s and the IMAD accumulate run on the ALU and FMA pipes beside it.
 #pragma unroll 2
         for (int w = 0; w < K; w += 2) {
             uint32_t a[2][4], m[2][4], b[2][12];
@@ -772,20 +756,19 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
                 for (int s = 0; s < 8; ++s) {
                     const int e = RIGHT ? j + s : j - s + 8;
-                    uint32_t x0 = a[0][j] ^ b[0][e];
-                    uint32_t x1 = a[1][j] ^ b[1][e];
+                    uint32_t q0 = a[0][j] ^ b[0][e];
+                    uint32_t q1 = a[1][j] ^ b[1][e];
                     if constexpr (MASKED) {
-                        x0 &= m[0][j];
-                        x1 &= m[1][j];
+                        q0 &= m[0][j];
+                        q1 &= m[1][j];
                     }
                     const uint32_t o = ones[j][s];
-                    const uint32_t twos = (o & x0) | (o & x1) | (x0 & x1);
-                    ones[j][s] = o ^ x0 ^ x1;
+                    const uint32_t twos = (o & q0) | (o & q1) | (q0 & q1);
+                    ones[j][s] = o ^ q0 ^ q1;
                     acc[j][s] = __popc(twos) * two + acc[j][s];
                 }
         }
     }
-    cp_async_wait<0>();
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -1555,6 +1538,30 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
 }
 
 // WTA keys of rows [0, rows) of device fields (SoA); keys: rows x W.
+// Tensor map of a device field [rows][NW][Wp] u32 for TMA boxes of box_x
+// columns x kCostK words x 1 row; out-of-range boxes read zeros.
+int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int rows, int box_x) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        BSM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            return set_err(BSM_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }
+    const int Wp = round_up(W, 128);
+    const cuuint64_t dims[3] = {cuuint64_t(Wp), cuuint64_t(NW), cuuint64_t(std::max(rows, 1))};
+    const cuuint64_t strides[2] = {cuuint64_t(Wp) * 4, cuuint64_t(NW) * Wp * 4};
+    const cuuint32_t box[3] = {cuuint32_t(box_x), cuuint32_t(kCostK), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(field), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(BSM_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return BSM_OK;
+}
+
 int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uint32_t* doth, int W, int rows,
                int d_max, bool right, bool masked, uint32_t* keys, int timing) {
     Scope s(c, timing);
@@ -1563,10 +1570,14 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
     dim3 grid(dz, Wp / kCostTile, rows);
     const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
-    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4;
+    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 8;  // + stage mbarriers
+    CUtensorMap tr, tmk, to;
+    BSM_TRY(field_tensor_map(&tr, dref, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&tmk, mref ? mref : dref, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&to, doth, W, c->NW, rows, kCostTile + kCostDisp));
     auto launch = [&](auto kern) -> int {
         BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<grid, 256, sm, c->stream>>>(dref, mref, doth, W, rows, c->NW, Wp, d_max, keys, 2u);
+        kern<<<grid, 256, sm, c->stream>>>(tr, tmk, to, W, rows, c->NW, d_max, keys, 2u);
         return BSM_OK;
     };
     if (right) BSM_TRY(masked ? launch(k_cost_wta<true, true>) : launch(k_cost_wta<true, false>));
