@@ -650,6 +650,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
 // 3-D box (x, word, row) of a field into shared memory, completing on bar.
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int w, int y, uint64_t* bar) {
     asm volatile(
@@ -677,15 +680,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 template <bool RIGHT, bool MASKED>
 __global__ void __launch_bounds__(256, 2)
     k_cost_wta(const __grid_constant__ CUtensorMap tm_ref, const __grid_constant__ CUtensorMap tm_mask,
-                   const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
-                   uint32_t* __restrict__ keys, uint32_t two) {
+               const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
+               uint32_t* __restrict__ keys, uint32_t two) {
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
     constexpr int SA = K * T, SB = K * BW;
     constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
     constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * 4;
     extern __shared__ __align__(128) uint32_t csm[];
     uint32_t* red = csm + ST * STAGE;                                 // [8][T]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full barriers
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full, then [ST] empty
+    uint64_t* empty = bars + ST;
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const int x0 = blockIdx.y * T;
@@ -697,7 +701,10 @@ __global__ void __launch_bounds__(256, 2)
     if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
 
     if (tid == 0) {
-        for (int s = 0; s < ST; ++s) mbar_init(bars + s, 1);
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(bars + s, 1);
+            mbar_init(empty + s, 8);  // one arrival per warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -709,7 +716,7 @@ __global__ void __launch_bounds__(256, 2)
         tma_load_3d(s + (MASKED ? 2 * SA : SA), &tm_oth, bbase, c * K, y, bars + st);
     };
     if (tid == 0)
-        for (int s = 0; s < ST - 1 && s < nchunks; ++s) load_stage(s, s);
+        for (int s = 0; s < ST && s < nchunks; ++s) load_stage(s, s);
 
     uint32_t acc[4][8], ones[4][8];
 #pragma unroll
@@ -728,9 +735,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
         mbar_wait(bars + c % ST, uint32_t(c / ST) & 1u);
-        __syncthreads();  // every warp is done with stage (c - 1) % ST before it is refilled
-        if (tid == 0 && c + ST - 1 < nchunks) load_stage(c + ST - 1, (c + ST - 1) % ST);
-        if (!busy) continue;
+        if (busy) {
         const uint32_t* sa = csm + (c % ST) * STAGE;
         const uint32_t* sm = sa + SA;
         const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
@@ -767,6 +772,14 @@ __global__ void __launch_bounds__(256, 2)
                     ones[j][s] = o ^ q0 ^ q1;
                     acc[j][s] = __popc(twos) * two + acc[j][s];
                 }
+        }
+        }
+        // release the slot; thread 0 refills it once all 8 warps are done
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + c % ST);
+        if (tid == 0 && c + ST < nchunks) {
+            mbar_wait(empty + c % ST, uint32_t(c / ST) & 1u);
+            load_stage(c + ST, c % ST);
         }
     }
 #pragma unroll
@@ -1570,7 +1583,7 @@ int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uin
     if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
     dim3 grid(dz, Wp / kCostTile, rows);
     const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
-    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 8;  // + stage mbarriers
+    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 16;  // + full/empty mbarriers
     CUtensorMap tr, tmk, to;
     BSM_TRY(field_tensor_map(&tr, dref, W, c->NW, rows, kCostTile));
     BSM_TRY(field_tensor_map(&tmk, mref ? mref : dref, W, c->NW, rows, kCostTile));
