@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(256, 2)
         const uint32_t* sa = csm + (c % ST) * STAGE;
         const uint32_t* sm = sa + SA;
         const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
-#pragma unroll 2
+#pragma unroll 1
         for (int w = 0; w < K; w += 2) {
             uint32_t a[2][4], m[2][4], b[2][12];
 #pragma unroll
