@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
     int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
     const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
     const int16_t* __restrict__ s2col, const int* __restrict__ counters, const int* __restrict__ inv, int nbins_cap,
-    float* __restrict__ od, uint8_t* __restrict__ ov) {
+    float* __restrict__ od, uint8_t* __restrict__ ov, int* __restrict__ work) {
     constexpr int LPP = 32 / NP;
     extern __shared__ __align__(16) double fsm[];
     unsigned long long* stab = reinterpret_cast<unsigned long long*>(fsm);  // 256 (DEVEXP)
@@ -1073,8 +1073,14 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
     const unsigned submask = (LPP == 32) ? full : (((1u << LPP) - 1u) << (sub * LPP));
     const int max_bin = counters[0];
     const int n_inv = counters[1];
-    const int gw = blockIdx.x * nwarps + warp, nw = gridDim.x * nwarps;
-    for (int base = gw * NP; base < n_inv; base += nw * NP) {  // warp-uniform loop
+    // groups of NP pixels are taken from a work counter (*work == 0 at
+    // launch): the voter count varies per pixel, so a static stride leaves a tail
+    auto grab = [&]() {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(work, NP);
+        return __shfl_sync(0xFFFFFFFFu, b, 0);
+    };
+    for (int base = grab(); base < n_inv; base = grab()) {  // warp-uniform loop
         const int idx = base + sub;
         const bool live = idx < n_inv;
         const int p = live ? inv[idx] : 0;
@@ -1642,11 +1648,12 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
                                 : (devexp ? k_vote_refine_fold<1, true> : k_vote_refine_fold<1, false>);
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
+            BSM_CUDA(cudaMemsetAsync(c->counters.as<int>() + 2, 0, 4, c->stream));  // work counter
             kern<<<c->sm_count * per_sm, warps * 32, sm, c->stream>>>(
                 c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
                 c->exp_dev, c->d_etab.as<unsigned long long>(), c->d_wtab.as<double>(), c->wt_ncol,
                 c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(),
-                c->ref_v.as<uint8_t>());
+                c->ref_v.as<uint8_t>(), c->counters.as<int>() + 2);
             return check_launch(c, "vote_refine_fold");
         }
         if (lab) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too wide for the colour refine bins");
