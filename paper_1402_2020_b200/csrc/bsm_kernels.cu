@@ -455,18 +455,26 @@ __global__ void __launch_bounds__(32, 16)
 // Colour / float-plane path (compute_field on arbitrary GrayImage + LabImage,
 // run_pipeline on RGB).  Same contracts as K1/K2 with float planes.
 //
-// k_rgb_planes: interleaved RGB -> gray (f32) and Lab (3 x f32) planes via the
+// k_rgb_planes: interleaved RGB -> gray (f32) and Lab planes via the
 // host-built 2^24-entry conversion tables (bit-identical to the reference's
-// to_gray / to_lab, image.hpp:90-140).
+// to_gray / to_lab, image.hpp:90-140).  Device Lab planes hold one float4
+// (L, a, b, 0) per pixel, so a window sample is one 16-byte load.
 __global__ void k_rgb_planes(const uint8_t* __restrict__ rgb, size_t n, const float* __restrict__ gtab,
-                             const float* __restrict__ ltab, float* __restrict__ gray, float* __restrict__ lab) {
+                             const float* __restrict__ ltab, float* __restrict__ gray, float4* __restrict__ lab4) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = (uint32_t(rgb[3 * i]) << 16) | (uint32_t(rgb[3 * i + 1]) << 8) | uint32_t(rgb[3 * i + 2]);
     gray[i] = __ldg(gtab + k);
-    lab[3 * i] = __ldg(ltab + 3 * size_t(k));
-    lab[3 * i + 1] = __ldg(ltab + 3 * size_t(k) + 1);
-    lab[3 * i + 2] = __ldg(ltab + 3 * size_t(k) + 2);
+    lab4[i] = make_float4(__ldg(ltab + 3 * size_t(k)), __ldg(ltab + 3 * size_t(k) + 1), __ldg(ltab + 3 * size_t(k) + 2),
+                          0.0f);
+}
+
+// Caller Lab planes (3 floats per pixel, the reference's LabImage layout) ->
+// device float4 planes.
+__global__ void k_lab3_to_lab4(const float* __restrict__ lab, size_t n, float4* __restrict__ lab4) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    lab4[i] = make_float4(lab[3 * i], lab[3 * i + 1], lab[3 * i + 2], 0.0f);
 }
 
 // K1f: descriptor bits I(p) > I(q) on a float gray plane (descriptor.hpp:95-105,
@@ -531,11 +539,12 @@ __device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
 
 template <int MCH>
 __global__ void __launch_bounds__(32, 16)
-    k_mask_f32(const float* __restrict__ lab, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
+    k_mask_f32(const float4* __restrict__ lab4, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
-               int NW, int Wp, uint32_t* __restrict__ mask) {
-    // Lab samples are read through L1 (no shared tile): shared memory holds
-    // only the slot keys and the 16 KB of bit planes, for occupancy.
+               int NW, int Wp, uint32_t* __restrict__ mask, int half) {
+    // Lab samples (float4 per pixel) are read through L1 (no shared tile):
+    // shared memory holds only the slot keys and the 16 KB of bit planes,
+    // for occupancy.
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
     uint32_t* planes = tv + rho_words;                    // [32 planes][MCH chunks][32 lanes]
@@ -545,24 +554,33 @@ __global__ void __launch_bounds__(32, 16)
     const int ly = blockIdx.y;
     const int y = ybeg + ly;
     if (lane == 0) tv[u] = 0xFFFFFFFFu;  // sentinel: larger than every SAD
+    // windows of all kM3Px pixels inside the view: no clamping
+    const bool interior = x0 - half >= 0 && x0 + kM3Px - 1 + half < W && y - half >= 0 && y + half < H;
     const int k = max(1, n / 4);
     const unsigned full = 0xFFFFFFFFu;
     const int rem = n & 31;
 #pragma unroll 1
     for (int px = 0; px < kM3Px; ++px) {
         const int x = min(x0 + px, W - 1);  // pad columns repeat the last pixel (not stored)
-        const size_t ci = 3 * (size_t(y) * W + x);
-        const float c0 = __ldg(lab + ci), c1 = __ldg(lab + ci + 1), c2 = __ldg(lab + ci + 2);
-        for (int j = lane; j < u; j += 32) {
-            const int e = __ldg(uxy + j);  // (dy << 16) | (dx & 0xFFFF)
-            const int gx = min(max(x + int(int16_t(e & 0xFFFF)), 0), W - 1);
-            const int gy = min(max(y + (e >> 16), 0), H - 1);
-            const size_t q = 3 * (size_t(gy) * W + gx);
-            // lab_sad(centre, window pixel), image.hpp:144-146
-            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(c0, __ldg(lab + q))),
-                                                  fabsf(__fsub_rn(c1, __ldg(lab + q + 1)))),
-                                        fabsf(__fsub_rn(c2, __ldg(lab + q + 2))));
-            tv[j] = __float_as_uint(sad);
+        const float4 cc = __ldg(lab4 + size_t(y) * W + x);
+        // lab_sad(centre, window pixel), image.hpp:144-146
+        auto sad = [&](const float4 o) {
+            return __fadd_rn(__fadd_rn(fabsf(__fsub_rn(cc.x, o.x)), fabsf(__fsub_rn(cc.y, o.y))),
+                             fabsf(__fsub_rn(cc.z, o.z)));
+        };
+        if (interior) {
+            const float4* cp = lab4 + size_t(y) * W + x;
+            for (int j = lane; j < u; j += 32) {
+                const int e = __ldg(uxy + j);  // (dy << 16) | (dx & 0xFFFF)
+                tv[j] = __float_as_uint(sad(__ldg(cp + ((e >> 16) * W + int(int16_t(e & 0xFFFF))))));
+            }
+        } else {
+            for (int j = lane; j < u; j += 32) {
+                const int e = __ldg(uxy + j);
+                const int gx = min(max(x + int(int16_t(e & 0xFFFF)), 0), W - 1);
+                const int gy = min(max(y + (e >> 16), 0), H - 1);
+                tv[j] = __float_as_uint(sad(__ldg(lab4 + size_t(gy) * W + gx)));
+            }
         }
         __syncwarp();
 #pragma unroll 1
@@ -1045,7 +1063,7 @@ __device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const uns
 // side.
 template <int NP, bool DEVEXP>
 __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
-    const uint32_t* __restrict__ vmap, const float* __restrict__ lab, const float* __restrict__ lab256, int W,
+    const uint32_t* __restrict__ vmap, const float4* __restrict__ lab, const float* __restrict__ lab256, int W,
     int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
     const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
     const int16_t* __restrict__ s2col, const int* __restrict__ counters, const int* __restrict__ inv, int nbins_cap,
@@ -1090,9 +1108,10 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
         float lx0 = 0.f, lx1 = 0.f, lx2 = 0.f;
         if (DEVEXP) {
             if (lab) {
-                lx0 = lab[3 * size_t(p)];
-                lx1 = lab[3 * size_t(p) + 1];
-                lx2 = lab[3 * size_t(p) + 2];
+                const float4 c = lab[p];
+                lx0 = c.x;
+                lx1 = c.y;
+                lx2 = c.z;
             } else {
                 lx0 = slab[3 * u];
                 lx1 = slab[3 * u + 1];
@@ -1136,10 +1155,10 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
                         if (DEVEXP) {
                             float l0, l1, l2;
                             if (lab) {
-                                const size_t q = 3 * (size_t(py) * W + x + dx);
-                                l0 = __ldg(lab + q);
-                                l1 = __ldg(lab + q + 1);
-                                l2 = __ldg(lab + q + 2);
+                                const float4 o = __ldg(lab + size_t(py) * W + x + dx);
+                                l0 = o.x;
+                                l1 = o.y;
+                                l2 = o.z;
                             } else {
                                 l0 = slab[3 * v];
                                 l1 = slab[3 * v + 1];
@@ -1619,7 +1638,7 @@ int ensure_elam(bsm_ctx* c, double le, int radius) {
 // max_bin in counters[0]) into c->ref_d / c->ref_v (pre-filled with the input
 // map).  nbins_max bounds max_bin + 1.  lab: per-pixel Lab plane or nullptr
 // (grayscale: the gray value indexes the Lab table).
-int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t* gray, const float* lab, int W,
+int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t* gray, const float4* lab, int W,
                   int rows, int radius, int nbins_max, double lc, double le) {
     const size_t px = size_t(rows) * W;
     const int nbins = round_up(std::max(nbins_max, 1), 32);
@@ -1703,7 +1722,7 @@ int ensure_descf_table(bsm_ctx* c) {
 size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(32) * c->mch * 32 * 4; }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
-int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int H, int ybeg, int rows,
+int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, int H, int ybeg, int rows,
                      uint32_t* desc, uint32_t* mask) {
     const int Wp = round_up(W, 128);
     BSM_TRY(ensure_descf_table(c));
@@ -1726,7 +1745,7 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float* lab, int W, int
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
                                               c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uxy.as<int32_t>(), c->mslots,
-                                              round_up(c->mslots + 1, 4), c->NW, Wp, mask);
+                                              round_up(c->mslots + 1, 4), c->NW, Wp, mask, c->half);
             return BSM_OK;
         };
         BSM_TRY(c->mch == 1   ? launch(k_mask_f32<1>)
@@ -1757,9 +1776,9 @@ struct Views {
     const uint8_t* u8l = nullptr;
     const uint8_t* u8r = nullptr;
     const float* gl = nullptr;
-    const float* ll = nullptr;
+    const float4* ll = nullptr;  // Lab planes, float4 (L, a, b, 0) per pixel
     const float* gr = nullptr;
-    const float* lr = nullptr;
+    const float4* lr = nullptr;
 };
 
 int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_rows, const bsm_params* p,
@@ -1823,7 +1842,7 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
         BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
         BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
         BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), v.u8l ? v.u8l + size_t(r0) * W : nullptr,
-                              v.u8l ? nullptr : v.ll + size_t(3) * r0 * W, W, rows, p->vote_radius, p->d_max,
+                              v.u8l ? nullptr : v.ll + size_t(r0) * W, W, rows, p->vote_radius, p->d_max,
                               p->lambda_c, p->lambda_e));
     }
     c->last_W = W;
@@ -2347,6 +2366,7 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
     }
     BSM_TRY(c->img_l.ensure(px));
     BSM_TRY(c->aux2.ensure(px * 12));
+    BSM_TRY(c->aux3.ensure(px * 16));
     BSM_TRY(c->chk_d.ensure(px * 4));
     BSM_TRY(c->chk_v.ensure(px));
     BSM_TRY(c->ref_d.ensure(px * 4));
@@ -2355,6 +2375,8 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
     BSM_TRY(c->inv.ensure(std::max<size_t>(4, invalid.size() * 4)));
     BSM_CUDA(cudaMemsetAsync(c->img_l.p, 0, px, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->aux2.p, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
+    k_lab3_to_lab4<<<unsigned((px + 255) / 256), 256, 0, c->stream>>>(c->aux2.as<float>(), px, c->aux3.as<float4>());
+    BSM_TRY(check_launch(c, "lab3_to_lab4"));
     BSM_CUDA(cudaMemcpyAsync(c->chk_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->chk_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
@@ -2364,7 +2386,7 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
     if (!invalid.empty())
         BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_TRY(sync(c));
-    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), c->aux2.as<float>(),
+    BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), c->aux3.as<float4>(),
                           W, H, vote_radius, max_bin + 1, lambda_c, lambda_e));
     if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
     if (out_v) BSM_CUDA(cudaMemcpyAsync(out_v, c->ref_v.p, px, cudaMemcpyDeviceToHost, c->stream));
@@ -2428,11 +2450,14 @@ int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W
     const size_t px = size_t(W) * H;
     const int Wp = round_up(W, 128);
     const size_t fbytes = size_t(H) * c->NW * Wp * 4;
-    BSM_TRY(c->planes.ensure(px * 16));
+    BSM_TRY(c->planes.ensure(px * 32));
     float* g = c->planes.as<float>();
-    float* l = g + px;
+    float* l3 = g + px;
+    float4* l = reinterpret_cast<float4*>(g + 4 * px);  // 16-B aligned (planes is cudaMalloc'd)
     BSM_CUDA(cudaMemcpyAsync(g, gray, px * 4, cudaMemcpyHostToDevice, c->stream));
-    BSM_CUDA(cudaMemcpyAsync(l, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(l3, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
+    k_lab3_to_lab4<<<unsigned((px + 255) / 256), 256, 0, c->stream>>>(l3, px, l);
+    BSM_TRY(check_launch(c, "lab3_to_lab4"));
     BSM_TRY(c->fdl.ensure(fbytes));
     BSM_TRY(c->fml.ensure(fbytes));
     BSM_TRY(field_device_f32(c, g, l, W, H, 0, H, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
@@ -2453,22 +2478,24 @@ static int rgb_pipeline(bsm_ctx* c, const uint8_t* d_left, const uint8_t* d_righ
                         const bsm_params* params, bool want_unmasked) {
     BSM_TRY(ensure_rgb_tables(c));
     const size_t px = size_t(W) * H;
-    BSM_TRY(c->planes.ensure(px * 32));
+    const size_t lab_off = (2 * px + 3) / 4 * 4;  // floats; keeps the float4 planes 16-B aligned
+    BSM_TRY(c->planes.ensure((lab_off + 8 * px) * 4));
     Views v;
     float* base = c->planes.as<float>();
+    float4* lab4 = reinterpret_cast<float4*>(base + lab_off);
     v.gl = base;
     v.gr = base + px;
-    v.ll = base + 2 * px;
-    v.lr = base + 5 * px;
+    v.ll = lab4;
+    v.lr = lab4 + px;
     {
         Scope s(c, T_DESC);  // the conversion is accounted with the descriptor stage
         const int tb = 256;
         k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(d_left, px, c->d_rgb_gray.as<float>(),
-                                                                      c->d_rgb_lab.as<float>(), base, base + 2 * px);
+                                                                      c->d_rgb_lab.as<float>(), base, lab4);
         BSM_TRY(check_launch(c, "rgb_planes"));
         k_rgb_planes<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(d_right, px, c->d_rgb_gray.as<float>(),
                                                                       c->d_rgb_lab.as<float>(), base + px,
-                                                                      base + 5 * px);
+                                                                      lab4 + px);
         BSM_TRY(check_launch(c, "rgb_planes"));
     }
     return pipeline_device(c, v, W, H, 0, H, params, want_unmasked);
