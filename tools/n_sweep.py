@@ -18,7 +18,7 @@ from paper_1402_2020_b200.synth import WORKLOADS, workload_pair  # noqa: E402
 
 def main():
     key = sys.argv[1] if len(sys.argv) > 1 else "c2"
-    ns = [int(v) for v in sys.argv[2:]] or [512, 1024, 2048, 4096]
+    ns = [int(v) for v in sys.argv[2:]] or [512, 1024, 2048, 4096, 8192]
     w = WORKLOADS[key]
     import torch
     left, right = workload_pair(key)
