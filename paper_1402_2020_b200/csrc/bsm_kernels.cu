@@ -583,22 +583,30 @@ __global__ void __launch_bounds__(32, 16)
             }
         }
         __syncwarp();
+        // a = max(t[P], t[Q]) of 32 positions per chunk, transposed into bit
+        // planes: bits 31..8 first (the transposes' low-byte outputs are dead
+        // code), bits 7..0 only when the top 24 bits leave the tie unresolved
+        auto planes_of = [&](auto store) {
 #pragma unroll 1
-        for (int m = 0; m < MCH; ++m) {
-            uint32_t x[32];
+            for (int m = 0; m < MCH; ++m) {
+                uint32_t x[32];
 #pragma unroll
-            for (int t4 = 0; t4 < 8; ++t4) {
-                const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
-                x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
-                x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
-                x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
-                x[4 * t4 + 3] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
+                for (int t4 = 0; t4 < 8; ++t4) {
+                    const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                    const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                    x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
+                    x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
+                    x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
+                    x[4 * t4 + 3] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
+                }
+                transpose32(x);
+                store(m, x);
             }
-            transpose32(x);
+        };
+        planes_of([&](int m, const uint32_t (&x)[32]) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
-        }
+            for (int j = 8; j < 32; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
+        });
         __syncwarp();
         // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
         // the a <= T comparator fused in: where the threshold takes a 1, the
@@ -610,27 +618,57 @@ __global__ void __launch_bounds__(32, 16)
             lt[m] = 0u;
         }
         int kk = k;
+        uint32_t tbits = 0;  // threshold bits decided so far
+        auto rounds = [&](int hi, int lo) {
 #pragma unroll 1
-        for (int j = 31; j >= 0; --j) {
-            uint32_t pl[MCH], z[MCH], cnt = 0;
-#pragma unroll
-            for (int m = 0; m < MCH; ++m) {
-                pl[m] = planes[(j * MCH + m) * 32 + lane];
-                z[m] = eq[m] & ~pl[m];
-                cnt += __popc(z[m]);
-            }
-            const int zeros = int(__reduce_add_sync(full, cnt));
-            if (zeros >= kk) {
-#pragma unroll
-                for (int m = 0; m < MCH; ++m) eq[m] = z[m];
-            } else {
-                kk -= zeros;
+            for (int j = hi; j >= lo; --j) {
+                uint32_t pl[MCH], z[MCH], cnt = 0;
 #pragma unroll
                 for (int m = 0; m < MCH; ++m) {
-                    lt[m] |= z[m];
-                    eq[m] &= pl[m];
+                    pl[m] = planes[(j * MCH + m) * 32 + lane];
+                    z[m] = eq[m] & ~pl[m];
+                    cnt += __popc(z[m]);
+                }
+                const int zeros = int(__reduce_add_sync(full, cnt));
+                if (zeros >= kk) {
+#pragma unroll
+                    for (int m = 0; m < MCH; ++m) eq[m] = z[m];
+                } else {
+                    kk -= zeros;
+                    tbits |= 1u << j;
+#pragma unroll
+                    for (int m = 0; m < MCH; ++m) {
+                        lt[m] |= z[m];
+                        eq[m] &= pl[m];
+                    }
                 }
             }
+        };
+        rounds(31, 8);
+        // Every value is a slot key, so the positions still tied (top 24 bits
+        // equal to the threshold's) all hold the threshold itself when the
+        // slot keys with those top bits are one value: then eq is final.
+        // Otherwise (rare) the low byte is resolved on its own planes.
+        uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+        for (int j = lane; j < u; j += 32) {
+            const uint32_t v = tv[j];
+            if ((v >> 8) == (tbits >> 8)) {
+                mn = min(mn, v);
+                mx = max(mx, v);
+            }
+        }
+#ifdef BSM_MASKF_ALWAYS_LOW  // test hook: resolve the low byte for every pixel
+        if (true) {
+#else
+        if (__reduce_min_sync(full, mn) != __reduce_max_sync(full, mx)) {
+#endif
+            __syncwarp();
+            planes_of([&](int m, const uint32_t (&x)[32]) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
+            });
+            __syncwarp();
+            rounds(7, 0);
         }
 #pragma unroll
         for (int m = 0; m < MCH; ++m) {
