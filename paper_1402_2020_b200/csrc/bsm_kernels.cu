@@ -500,10 +500,21 @@ __global__ void __launch_bounds__(kDfTX* kDfTY)
     for (int w = 0; w < NW; ++w) {
         uint32_t acc[kDfPY] = {0u, 0u, 0u, 0u};
         const int cnt = min(32, max(0, n - 32 * w));
-        for (int k = 0; k < cnt; ++k) {
-            const int2 o = __ldg(offs + 32 * w + k);  // tile-relative (py*TW + px) of p and q
+        if (cnt == 32) {
+            // fully unrolled: static bit positions (predicated ORs)
 #pragma unroll
-            for (int j = 0; j < kDfPY; ++j) acc[j] |= uint32_t(t0[j * TW + o.x] > t0[j * TW + o.y]) << k;
+            for (int k = 0; k < 32; ++k) {
+                const int2 o = __ldg(offs + 32 * w + k);  // tile-relative (py*TW + px) of p and q
+#pragma unroll
+                for (int j = 0; j < kDfPY; ++j)
+                    if (t0[j * TW + o.x] > t0[j * TW + o.y]) acc[j] |= 1u << k;
+            }
+        } else {
+            for (int k = 0; k < cnt; ++k) {
+                const int2 o = __ldg(offs + 32 * w + k);
+#pragma unroll
+                for (int j = 0; j < kDfPY; ++j) acc[j] |= uint32_t(t0[j * TW + o.x] > t0[j * TW + o.y]) << k;
+            }
         }
 #pragma unroll
         for (int j = 0; j < kDfPY; ++j) {
@@ -516,10 +527,11 @@ __global__ void __launch_bounds__(kDfTX* kDfTY)
 // K2f: mask on a float Lab plane (descriptor.hpp:118-154, 64-76).  One warp
 // per CTA, kM3Px pixels per CTA, one pixel per pass.  The window SADs t[slot]
 // are kept as float bit patterns (non-negative floats order like u32); lane l
-// owns pairs 128l + 32m + t, forms a = max(t[P], t[Q]) for 32 pairs per chunk,
-// transposes the 32 words into 32 bit planes (5-stage in-register 32x32 bit
-// transpose), selects the k-th smallest MSB-first over 32 bits, and emits
-// bit = a <= T with a 32-plane comparator.
+// owns pairs S l + 32m + t, forms a = max(t[P], t[Q]) for 32 pairs per chunk,
+// transposes the 32 words into bit planes (5-stage in-register 32x32 bit
+// transpose) and selects the k-th smallest MSB-first with the a <= T
+// comparator fused in -- over key bits 31..8, and over the low byte only when
+// the threshold's tie is not a single slot key.
 __device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
     // afterwards x[j] bit t = (original x[t]) bit j
 #pragma unroll
