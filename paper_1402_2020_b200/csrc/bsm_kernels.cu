@@ -439,15 +439,16 @@ __global__ void __launch_bounds__(32, 16)
         __syncwarp();  // rho / rrows are rewritten by the next pass
     }
     __syncwarp();
+    // lane = (word offset w % 4, pixel j): 32-B row segments, stage reads
+    // independent across iterations; pad bits and pad words are zero
     const int rem = n & 31;
-    for (int idx = lane; idx < NW * kM3Px; idx += 32) {
-        const int w = idx / kM3Px, j = idx - w * kM3Px;
-        uint32_t v = 0;
-        if (w < G) {
-            v = stage[j * STG + w];
-            if (rem && w == G - 1) v &= (1u << rem) - 1u;
-        }
-        mask[(size_t(ly) * NW + w) * Wp + x0 + j] = v;
+    const uint32_t tail = rem ? (1u << rem) - 1u : ~0u;
+    const int jl = lane & (kM3Px - 1), wl = lane / kM3Px;
+    uint32_t* dst = mask + (size_t(ly) * NW + wl) * Wp + x0 + jl;
+#pragma unroll 4
+    for (int w = wl; w < NW; w += 32 / kM3Px, dst += size_t(32 / kM3Px) * Wp) {
+        const uint32_t v = stage[jl * STG + w];
+        *dst = w < G - 1 ? v : (w == G - 1 ? v & tail : 0u);
     }
 }
 
