@@ -5,8 +5,9 @@
 // Device layout (per view, W x H, n bits, NW = 2*ceil(n/64) u32 words):
 //   field[(y*NW + w)*Wp + x]   word-major ("bit-plane rows"), Wp = W rounded up
 //   to 128, so a row segment of one word is a contiguous, 16-B-aligned span:
-//   the cost kernel stages [K words x span] boxes with cp.async and every
-//   shared-memory read is a conflict-free 16-B lane-contiguous LDS.128.
+//   the cost kernel stages [K words x span] boxes by TMA (one tensor map per
+//   field, dims (Wp, NW, rows)) and every shared-memory read is a
+//   conflict-free 16-B lane-contiguous LDS.128.
 //   u32 word w of a pixel = bits 32w..32w+31 = the low/high half of the
 //   reference's u64 word w>>1 (bitstring.hpp:47-51).
 #include <cuda.h>
