@@ -557,11 +557,12 @@ __global__ void __launch_bounds__(32, 16)
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
                int NW, int Wp, uint32_t* __restrict__ mask, int half) {
     // Lab samples (float4 per pixel) are read through L1 (no shared tile):
-    // shared memory holds only the slot keys and the 16 KB of bit planes,
-    // for occupancy.
+    // shared memory holds only the slot keys and 24 rows of bit planes (the
+    // low byte's planes reuse the rows of bits 8..15), for occupancy.
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
-    uint32_t* planes = tv + rho_words;                    // [32 planes][MCH chunks][32 lanes]
+    uint32_t* planes = tv + rho_words;                    // [24 rows][MCH chunks][32 lanes]
+    auto prow = [](int b) { return b >= 8 ? b - 8 : b; };  // plane row of key bit b
     const int G = (n + 31) >> 5;
     const int lane = threadIdx.x;
     const int x0 = blockIdx.x * kM3Px;
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(32, 16)
         };
         planes_of([&](int m, const uint32_t (&x)[32]) {
 #pragma unroll
-            for (int j = 8; j < 32; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
+            for (int j = 8; j < 32; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
         });
         __syncwarp();
         // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(32, 16)
                 uint32_t pl[MCH], z[MCH], cnt = 0;
 #pragma unroll
                 for (int m = 0; m < MCH; ++m) {
-                    pl[m] = planes[(j * MCH + m) * 32 + lane];
+                    pl[m] = planes[(prow(j) * MCH + m) * 32 + lane];
                     z[m] = eq[m] & ~pl[m];
                     cnt += __popc(z[m]);
                 }
@@ -677,9 +678,9 @@ __global__ void __launch_bounds__(32, 16)
         if (__reduce_min_sync(full, mn) != __reduce_max_sync(full, mx)) {
 #endif
             __syncwarp();
-            planes_of([&](int m, const uint32_t (&x)[32]) {
+            planes_of([&](int m, const uint32_t (&x)[32]) {  // rows of bits 8..15 are dead now
 #pragma unroll
-                for (int j = 0; j < 8; ++j) planes[(j * MCH + m) * 32 + lane] = x[j];
+                for (int j = 0; j < 8; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
             });
             __syncwarp();
             rounds(7, 0);
@@ -1771,7 +1772,7 @@ int ensure_descf_table(bsm_ctx* c) {
     return BSM_OK;
 }
 
-size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(32) * c->mch * 32 * 4; }
+size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(24) * c->mch * 32 * 4; }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, int H, int ybeg, int rows,
