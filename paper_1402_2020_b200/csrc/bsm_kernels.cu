@@ -607,8 +607,15 @@ __global__ void __launch_bounds__(32, 16)
                 uint32_t x[32];
 #pragma unroll
                 for (int t4 = 0; t4 < 8; ++t4) {
-                    const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                    const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                    uint4 P, Q;
+                    if constexpr (MCH <= 4) {  // packed P | Q << 16 (p4 points at the packed table)
+                        P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                        Q = make_uint4(P.x >> 16, P.y >> 16, P.z >> 16, P.w >> 16);
+                        P = make_uint4(P.x & 0xFFFFu, P.y & 0xFFFFu, P.z & 0xFFFFu, P.w & 0xFFFFu);
+                    } else {
+                        P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                        Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                    }
                     x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
                     x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
                     x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
@@ -1796,7 +1803,8 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, in
         dim3 grid(Wp / kM3Px, rows);
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+            kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows,
+                                              c->d_pqb.as<uint4>() + (c->mch <= 4 ? 2 * kPqTable / 4 : 0),
                                               c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uxy.as<int32_t>(), c->mslots,
                                               round_up(c->mslots + 1, 4), c->NW, Wp, mask, c->half);
             return BSM_OK;
@@ -2151,8 +2159,12 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     // endpoints (k_mask4 / k_mask_f32): P table at [0, kPqTable), Q table at
     // [kPqTable, 2 kPqTable), lane-block order -- lane l, chunk m < MCH, t:
     // bit 32*MCH*l + 32m + t at uint4 [(m*8 + t/4)*32 + l], component t%4.
-    // Pads read the sentinel.
-    std::vector<uint32_t> pqb(2 * kPqTable, uint32_t(4 * c->mslots));
+    // Pads read the sentinel.  For MCH <= 4, k_mask_f32 reads the packed table
+    // at [2 kPqTable, 3 kPqTable): P | Q << 16 (mslots <= 2 * 4096 + 64 there,
+    // so byte offsets fit 16 bits) -- half the L1 footprint of the gathers.
+    if (c->mch <= 4 && 4 * c->mslots > 0xFFFF) return set_err(BSM_UNSUPPORTED, "bsm: rank-table offsets exceed 16 bits");
+    std::vector<uint32_t> pqb(3 * kPqTable, uint32_t(4 * c->mslots));
+    for (int i = 0; i < kPqTable; ++i) pqb[2 * kPqTable + i] = uint32_t(4 * c->mslots) * 65537u;
     for (int j = 0; j < n; ++j) {
         const int l = j / lane_pos, m = (j >> 5) % c->mch, t = j & 31;
         const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
@@ -2160,6 +2172,7 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
         const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
         pqb[at] = uint32_t(4 * rslot[size_t(a)]);
         pqb[kPqTable + at] = uint32_t(4 * rslot[size_t(b)]);
+        pqb[2 * kPqTable + at] = pqb[at] | (pqb[kPqTable + at] << 16);
     }
     BSM_TRY(c->d_pqb.ensure(pqb.size() * 4));
     BSM_CUDA(cudaMemcpy(c->d_pqb.p, pqb.data(), pqb.size() * 4, cudaMemcpyHostToDevice));
