@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(32, 16)
         };
         if (interior) {
             const float4* cp = lab4 + size_t(y) * W + x;
-            for (int j = lane; j < u; j += 32) {
+#pragma unroll 8
+            for (int j = lane; j < u; j += 32) {  // 8 window samples in flight per lane
                 const int e = __ldg(uxy + j);  // (dy << 16) | (dx & 0xFFFF)
                 tv[j] = __float_as_uint(sad(__ldg(cp + ((e >> 16) * W + int(int16_t(e & 0xFFFF))))));
             }
