@@ -24,21 +24,23 @@ def main():
     kargs = ["-k", "regex:" + kre] if kre else []
     rows = list(csv.reader(run([rep, "--page", "details", "--csv"] + kargs).splitlines()))
     hdr = rows[0]
-    ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
-    seen = {}
-    for r in rows[1:]:
-        if r[mi] in WANT and (r[ki], r[mi]) not in seen:
-            seen[(r[ki], r[mi])] = f"{r[vi]} {r[ui]}".strip()
-    kernels = sorted({k for k, _ in seen})
+    ii, ki, mi, vi, ui = (hdr.index(x) for x in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    seen, names = {}, {}
+    for r in rows[1:]:  # keyed by launch ID: one report may hold several launches
+        names[r[ii]] = r[ki]
+        if r[mi] in WANT and (r[ii], r[mi]) not in seen:
+            seen[(r[ii], r[mi])] = f"{r[vi]} {r[ui]}".strip()
     raw = list(csv.reader(run([rep, "--page", "raw", "--csv"] + kargs).splitlines()))
     h, units, vals = raw[0], raw[1], raw[2:]
-    for n, k in enumerate(kernels):
+    by_id = {v[h.index("ID")]: v for v in vals}
+    for lid in sorted(names, key=int):
+        k = names[lid]
         print(f"== {k[:110]}")
         for m in WANT:
-            if (k, m) in seen:
-                print(f"   {m:36s} {seen[(k, m)]}")
-        if n < len(vals):
-            v = vals[n]
+            if (lid, m) in seen:
+                print(f"   {m:36s} {seen[(lid, m)]}")
+        if lid in by_id:
+            v = by_id[lid]
             get = lambda name: float(v[h.index(name)].replace(",", "")) if name in h and v[h.index(name)] else None
             rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
             if rd is not None and wr is not None:
