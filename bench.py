@@ -401,6 +401,11 @@ def main():
             line["cpu_baseline"] = {"value": e / s / 1e6, "unit": "Mdisp-evals/s", "cores": threads,
                                     "kind": "reference",
                                     "sample": f"{args.ref_rows} rows x {W} x D={D} of the same pair, {libname}"}
+            # the paper's protocol is one thread: a smaller band
+            r1 = max(4, args.ref_rows // 8)
+            s1, e1, _ = cpu_reference_sample(args.workload, r1, 1, pairs_arr)
+            line["cpu_baseline"]["single_thread"] = {"value": e1 / s1 / 1e6, "cores": 1,
+                                                     "sample": f"{r1} rows x {W} x D={D}"}
         except Exception as ex:  # the checker is optional on a box without it
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:
