@@ -50,1357 +50,10 @@ constexpr int kCostStages = 3;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
-// ---------------------------------------------------------------------------
-// K1' -- descriptor, four pixels per thread.  Same contract as k_descriptor.
-// A thread owns pixels x..x+3 (x % 4 == 0) of two rows; per pair it reads the
-// 4 p-samples and the 4 q-samples as two aligned words each plus one PRMT
-// (the byte alignment is the same for every thread, so the selector is
-// warp-uniform), compares the 4 unsigned bytes with a borrow-free SWAR test,
-// and deposits the 4 result bits into byte lanes; every 32 pairs a 4x4 byte
-// transpose turns them into the 4 pixels' words, stored as one 16-B store.
-constexpr int kD2TX = 32, kD2TY = 8, kD2Rows = 2;  // CTA: 128 px x 16 rows
-
-__device__ __forceinline__ uint32_t bytes_gt(uint32_t p, uint32_t q) {
-    // bit 7 of each byte: p_b > q_b (unsigned).  d = (q|0x80) - (p&0x7F) has no
-    // inter-byte borrow; bit 7 of d is [q_lo >= p_lo]; then q >= p <=>
-    // (q7 & ~p7) | (~(q7 ^ p7) & d7), and p > q is its complement.
-    const uint32_t d = (q | 0x80808080u) - (p & 0x7F7F7F7Fu);
-    const uint32_t ge = (q & ~p) | (~(q ^ p) & d);
-    return ~ge & 0x80808080u;
-}
-
-__global__ void __launch_bounds__(kD2TX* kD2TY)
-    k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
-                  const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wp,
-                  uint32_t* __restrict__ desc) {
-    // tile: clamped bytes; t4[i] = bytes i..i+3 of the tile, so the 4 samples
-    // of a thread's 4 pixels at any offset are one aligned 32-bit load.
-    extern __shared__ __align__(16) uint32_t dsm[];
-    const int TH = kD2TY * kD2Rows + 2 * half;
-    const int NT = TWs * TH;
-    uint32_t* t4 = dsm;
-    uint8_t* tile = reinterpret_cast<uint8_t*>(dsm + NT);
-    const int tid = threadIdx.y * kD2TX + threadIdx.x;
-    const int gx0 = blockIdx.x * (kD2TX * 4) - half;
-    const int ly0 = blockIdx.y * kD2TY * kD2Rows;
-    const int gy0 = ybeg + ly0 - half;
-    for (int idx = tid; idx < NT; idx += kD2TX * kD2TY) {
-        const int r = idx / TWs, c = idx - r * TWs;
-        const int gx = min(max(gx0 + c, 0), W - 1);
-        const int gy = min(max(gy0 + r, 0), H - 1);
-        tile[idx] = __ldg(img + size_t(gy) * W + gx);
-    }
-    tile[NT] = tile[NT + 1] = tile[NT + 2] = 0;  // t4 tail (never sampled)
-    __syncthreads();
-    // phased layout: t4[ph * S4 + k] = bytes 4k+ph .. 4k+ph+3, so the windows a
-    // warp reads for one pair offset are 32 consecutive words (no conflicts)
-    const int S4 = NT >> 2;
-    for (int idx = tid; idx < NT; idx += kD2TX * kD2TY)
-        t4[(idx & 3) * S4 + (idx >> 2)] = uint32_t(tile[idx]) | (uint32_t(tile[idx + 1]) << 8) |
-                                          (uint32_t(tile[idx + 2]) << 16) | (uint32_t(tile[idx + 3]) << 24);
-    __syncthreads();
-    const int xq = blockIdx.x * (kD2TX * 4) + 4 * threadIdx.x;
-    const uint32_t* tb = t4 + ((threadIdx.y * kD2Rows + half) * TWs >> 2) + threadIdx.x;
-    const int rowW = TWs >> 2;
-    const int full = n >> 5;
-    // blockIdx.z splits the word range (small images: more CTAs than SMs)
-    const int wper = (NW + gridDim.z - 1) / gridDim.z;
-    const int wbeg = blockIdx.z * wper, wend = min(NW, wbeg + wper);
-    for (int w = wbeg; w < wend; ++w) {
-        uint32_t acc[kD2Rows][4];
-#pragma unroll
-        for (int r = 0; r < kD2Rows; ++r)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[r][b] = 0;
-        const int cnt = w < full ? 32 : (w == full ? (n & 31) : 0);
-        if (cnt == 32) {
-            // fully unrolled: acc[r][k >> 3] stays a static register choice
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int2 e = __ldg(ptab + 32 * w + k);  // tile-relative offsets of p and q
-#pragma unroll
-                for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t f = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]);  // bit 7 of byte j: pixel j
-                    // pair k -> bit (k & 7) of byte lane j of acc[k >> 3]
-                    acc[r][k >> 3] |= (f >> (7 - (k & 7)));
-                }
-            }
-        } else {
-            for (int k = 0; k < cnt; ++k) {
-                const int2 e = __ldg(ptab + 32 * w + k);
-#pragma unroll
-                for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t v = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]) >> (7 - (k & 7));
-                    switch (k >> 3) {
-                        case 0: acc[r][0] |= v; break;
-                        case 1: acc[r][1] |= v; break;
-                        case 2: acc[r][2] |= v; break;
-                        default: acc[r][3] |= v; break;
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < kD2Rows; ++r) {
-            // acc[b] byte j = bits 8b..8b+7 of pixel j  ->  4x4 byte transpose
-            const uint32_t t0 = __byte_perm(acc[r][0], acc[r][1], 0x5140), t1 = __byte_perm(acc[r][0], acc[r][1], 0x7362);
-            const uint32_t t2 = __byte_perm(acc[r][2], acc[r][3], 0x5140), t3 = __byte_perm(acc[r][2], acc[r][3], 0x7362);
-            uint4 o;
-            o.x = __byte_perm(t0, t2, 0x5410);
-            o.y = __byte_perm(t0, t2, 0x7632);
-            o.z = __byte_perm(t1, t3, 0x5410);
-            o.w = __byte_perm(t1, t3, 0x7632);
-            const int ly = ly0 + threadIdx.y * kD2Rows + r;
-            if (ly < rows) *reinterpret_cast<uint4*>(desc + (size_t(ly) * NW + w) * Wp + xq) = o;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2 -- mask: shared helpers of k_mask4 (one warp per CTA, kM3Px pixels per
-// CTA, two pixels per pass).
-constexpr int kM3Px = 8;
-// rank-gather index tables (u32 byte offsets): P table, then Q table, each
-// sized for MCH = 8 chunks (8192 positions)
-constexpr int kPqTable = 8192;
-
-__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t lds_u32(const uint32_t* base, uint32_t byte_off) {
-    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + byte_off);
-}
-
-// ---------------------------------------------------------------------------
-// K2'' -- mask on bit planes.  Lane l owns bit positions [S l, S l + S) in
-// MCH chunks of 32 (S = 32 MCH; MCH = 1, 2, 4, 8 for n <= 1024 .. 8192; the
-// pair at each position comes from the bank-balanced order, so every 32-lane
-// rank gather is one shared-memory wavefront); for two pixels per pass it
-//   1. gathers a = max(rhoP, rhoQ) of both pixels per pair (one u32 rank-table
-//      gather + VIMNMX.U16x2 serves both), packs each pixel's 32 chunk values
-//      into eight byte registers,
-//   2. transposes them into 8 bit planes held in registers (four 8x8 bit-matrix
-//      transposes and a 4x4 byte transpose): plane j, word m of lane l holds
-//      bit j of a for positions S l + 32m + t at bit t -- exactly the layout
-//      of output word MCH l + m (MCH = 8 forms one pixel's planes at a time),
-//   3. selects the k-th smallest a MSB-first on the planes (per bit: LOP3 +
-//      POPC per word, one REDUX; the two pixels in lockstep) with the a <= T
-//      comparator fused in, and stages one uint4 of output words per lane.
-// 8x8 bit-matrix transpose of the 8 bytes (lo: rows 0-3, hi: rows 4-7),
-// afterwards byte j bit k = input byte k bit j.  Three delta-swap stages on the
-// 32-bit halves (the first two stay inside a half; left shifts as multiplies
-// so they can issue on the FMA pipe).
-__device__ __forceinline__ void transpose8x8_32(uint32_t& lo, uint32_t& hi) {
-    uint32_t t;
-    t = (lo ^ (lo >> 7)) & 0x00AA00AAu;
-    lo = lo ^ t ^ (t * 128u);
-    t = (hi ^ (hi >> 7)) & 0x00AA00AAu;
-    hi = hi ^ t ^ (t * 128u);
-    t = (lo ^ (lo >> 14)) & 0x0000CCCCu;
-    lo = lo ^ t ^ (t * 16384u);
-    t = (hi ^ (hi >> 14)) & 0x0000CCCCu;
-    hi = hi ^ t ^ (t * 16384u);
-    t = (lo ^ (hi * 16u)) & 0xF0F0F0F0u;
-    lo ^= t;
-    hi ^= t >> 4;
-}
-
-// w[0..7]: 32 byte values (value t = byte t%4 of w[t/4]); planes[j] bit t = bit j of value t.
-__device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t (&pl)[8]) {
-    uint32_t lo[4], hi[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        lo[b] = w[2 * b];
-        hi[b] = w[2 * b + 1];
-        transpose8x8_32(lo[b], hi[b]);
-    }
-    // 4x4 byte transposes: plane j = byte j of block 0..3
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t* s = h ? hi : lo;
-        const uint32_t t0 = __byte_perm(s[0], s[1], 0x5140), t1 = __byte_perm(s[0], s[1], 0x7362);
-        const uint32_t t2 = __byte_perm(s[2], s[3], 0x5140), t3 = __byte_perm(s[2], s[3], 0x7362);
-        pl[4 * h + 0] = __byte_perm(t0, t2, 0x5410);
-        pl[4 * h + 1] = __byte_perm(t0, t2, 0x7632);
-        pl[4 * h + 2] = __byte_perm(t1, t3, 0x5410);
-        pl[4 * h + 3] = __byte_perm(t1, t3, 0x7632);
-    }
-}
-
-
-// MSB-first k-th-smallest selection over 8 bit planes (4 words per lane,
-// 128 values per lane, 4096 per warp) fused with the comparator: at a bit
-// where the threshold takes 1, the still-equal values with a 0 there are
-// strictly below it; the output words are (a <= T) = lt | eq.
-// Two selects in lockstep (the two pixels of a pass): the REDUX of one
-// overlaps the POPCs and the REDUX of the other.
-template <int MCH>
-__device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][MCH], const uint32_t (&pb)[8][MCH], int k,
-                                           uint32_t (&oa)[MCH], uint32_t (&ob)[MCH]) {
-    uint32_t ea[MCH], eb[MCH], la[MCH], lb[MCH];
-#pragma unroll
-    for (int m = 0; m < MCH; ++m) {
-        ea[m] = eb[m] = ~0u;
-        la[m] = lb[m] = 0u;
-    }
-    int ka = k, kb = k;
-#pragma unroll
-    for (int j = 7; j >= 0; --j) {
-        uint32_t za[MCH], zb[MCH];
-        uint32_t ca = 0, cb = 0;
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            za[m] = ea[m] & ~pa[j][m];
-            zb[m] = eb[m] & ~pb[j][m];
-            ca += __popc(za[m]);
-            cb += __popc(zb[m]);
-        }
-        const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
-        const int zbs = int(__reduce_add_sync(0xFFFFFFFFu, cb));
-        // warp-uniform choices; written as selects so both chains stay branch-free
-        const bool ha = zas < ka, hb = zbs < kb;
-        ka -= ha ? zas : 0;
-        kb -= hb ? zbs : 0;
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            la[m] |= ha ? za[m] : 0u;
-            ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
-            lb[m] |= hb ? zb[m] : 0u;
-            eb[m] = hb ? (eb[m] & pb[j][m]) : zb[m];
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < MCH; ++m) {
-        oa[m] = la[m] | ea[m];
-        ob[m] = lb[m] | eb[m];
-    }
-}
-
-// Stores MCH consecutive words (16-, 8- or 4-byte aligned).
-template <int MCH>
-__device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t (&w)[MCH]) {
-    if constexpr (MCH == 8) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(dst + 4) = make_uint4(w[4], w[5], w[6], w[7]);
-    } else if constexpr (MCH == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-    else if constexpr (MCH == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-    else dst[0] = w[0];
-}
-
-// One pixel's select (the split variant for MCH = 8, where two pixels' planes
-// would not fit the register budget).
-template <int MCH>
-__device__ __forceinline__ void select_le1(const uint32_t (&pa)[8][MCH], int k, uint32_t (&oa)[MCH]) {
-    uint32_t ea[MCH], la[MCH];
-#pragma unroll
-    for (int m = 0; m < MCH; ++m) {
-        ea[m] = ~0u;
-        la[m] = 0u;
-    }
-    int ka = k;
-#pragma unroll
-    for (int j = 7; j >= 0; --j) {
-        uint32_t za[MCH], ca = 0;
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            za[m] = ea[m] & ~pa[j][m];
-            ca += __popc(za[m]);
-        }
-        const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
-        const bool ha = zas < ka;
-        ka -= ha ? zas : 0;
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            la[m] |= ha ? za[m] : 0u;
-            ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < MCH; ++m) oa[m] = la[m] | ea[m];
-}
-
-// Output staging row stride (words) of k_mask4<MCH>: 32 MCH words per pixel +
-// 4 of padding (16-B aligned rows, conflict-free read-out).
-__host__ __device__ constexpr int mask4_stage_stride(int mch) { return 32 * mch + 4; }
-
-template <int MCH>
-__global__ void __launch_bounds__(32, 16)
-    k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
-            const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
-            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
-    extern __shared__ __align__(16) uint32_t dsm[];
-    uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
-    constexpr int STG = mask4_stage_stride(MCH);
-    uint32_t* stage = rho + rho_words;                    // [kM3Px][STG]
-    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * STG);  // 2 x 256
-    uint8_t* tile = rrows + 512;                                            // (2h+1) x TW
-    const int G = (n + 31) >> 5;
-    const int TH = 2 * half + 1;
-    const int lane = threadIdx.x;
-    const int x0 = blockIdx.x * kM3Px;
-    const int ly = blockIdx.y;
-    const int y = ybeg + ly;
-    // The tile starts at the word-aligned column a0 <= x0 - h; interior tiles of
-    // 4-byte-aligned rows load whole words, the rest bytes with clamping.
-    const int a0 = (x0 - half) & ~3, ay0 = y - half;
-    const int sh = x0 - half - a0;
-    if ((W & 3) == 0 && a0 >= 0 && a0 + TW <= W && ay0 >= 0 && ay0 + TH <= H) {
-        const int nw = TW >> 2;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(img + size_t(ay0) * W + a0);
-#pragma unroll 4
-        for (int idx = lane; idx < TH * nw; idx += 32) {
-            const int r = idx / nw;
-            reinterpret_cast<uint32_t*>(tile)[idx] = __ldg(src + size_t(r) * (W >> 2) + (idx - r * nw));
-        }
-    } else {
-#pragma unroll 4
-        for (int idx = lane; idx < TW * TH; idx += 32) {
-            const int r = idx / TW, c = idx - r * TW;
-            const int gx = min(max(a0 + c, 0), W - 1);
-            const int gy = min(max(ay0 + r, 0), H - 1);
-            tile[idx] = __ldg(img + size_t(gy) * W + gx);
-        }
-    }
-    if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
-    __syncwarp();
-
-    const int k = max(1, n / 4);
-    const int c0 = half * TW + sh + half;  // tile index of pixel x0
-    // rank rows of the next pass's two centre pixels, loaded one pass ahead
-    uint4 rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (lane >> 4)])) + (lane & 15));
-#pragma unroll 1
-    for (int q = 0; q < kM3Px; q += 2) {
-        const int cia = c0 + q, cib = cia + 1;
-        reinterpret_cast<uint4*>(rrows)[lane] = rr;
-        if (q + 2 < kM3Px)
-            rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[cia + 2 + (lane >> 4)])) + (lane & 15));
-        __syncwarp();
-        for (int j = lane; j < u; j += 32) {
-            const int o = __ldg(uoff + j);
-            rho[j] = uint32_t(rrows[tile[cia + o]]) | (uint32_t(rrows[256 + tile[cib + o]]) << 16);
-        }
-        __syncwarp();
-
-        // a = max(rhoP, rhoQ) of 32 positions of chunk m for both pixels, as
-        // byte registers wa (pixel A) and wb (pixel B)
-        auto gather = [&](int m, uint32_t(&wa)[8], uint32_t(&wb)[8]) {
-#pragma unroll
-            for (int t4 = 0; t4 < 8; ++t4) {
-                const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
-                const uint32_t v0 = vmax_u16x2(lds_u32(rho, P.x), lds_u32(rho, Q.x));
-                const uint32_t v1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
-                const uint32_t v2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
-                const uint32_t v3 = vmax_u16x2(lds_u32(rho, P.w), lds_u32(rho, Q.w));
-                const uint32_t x01 = __byte_perm(v0, v1, 0x6240);  // [A0 A1 B0 B1]
-                const uint32_t x23 = __byte_perm(v2, v3, 0x6240);  // [A2 A3 B2 B3]
-                wa[t4] = __byte_perm(x01, x23, 0x5410);
-                wb[t4] = __byte_perm(x01, x23, 0x7632);
-            }
-        };
-        if constexpr (MCH <= 4) {
-            uint32_t pa[8][MCH], pb[8][MCH];
-#pragma unroll
-            for (int m = 0; m < MCH; ++m) {
-                uint32_t wa[8], wb[8], ta[8], tb[8];
-                gather(m, wa, wb);
-                bytes_to_planes(wa, ta);
-                bytes_to_planes(wb, tb);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    pa[j][m] = ta[j];
-                    pb[j][m] = tb[j];
-                }
-            }
-            uint32_t oa[MCH], ob[MCH];
-            select_le2<MCH>(pa, pb, k, oa, ob);
-            store_words<MCH>(stage + q * STG + MCH * lane, oa);
-            store_words<MCH>(stage + (q + 1) * STG + MCH * lane, ob);
-        } else {
-            // one pixel's planes at a time: the gathers run twice
-#pragma unroll 1
-            for (int side = 0; side < 2; ++side) {
-                uint32_t pl[8][MCH];
-#pragma unroll
-                for (int m = 0; m < MCH; ++m) {
-                    uint32_t wa[8], wb[8], t[8];
-                    gather(m, wa, wb);
-                    bytes_to_planes(side ? wb : wa, t);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) pl[j][m] = t[j];
-                }
-                uint32_t o[MCH];
-                select_le1<MCH>(pl, k, o);
-                store_words<MCH>(stage + (q + side) * STG + MCH * lane, o);
-            }
-        }
-        __syncwarp();  // rho / rrows are rewritten by the next pass
-    }
-    __syncwarp();
-    // lane = (word offset w % 4, pixel j): 32-B row segments, stage reads
-    // independent across iterations; pad bits and pad words are zero
-    const int rem = n & 31;
-    const uint32_t tail = rem ? (1u << rem) - 1u : ~0u;
-    const int jl = lane & (kM3Px - 1), wl = lane / kM3Px;
-    uint32_t* dst = mask + (size_t(ly) * NW + wl) * Wp + x0 + jl;
-#pragma unroll 4
-    for (int w = wl; w < NW; w += 32 / kM3Px, dst += size_t(32 / kM3Px) * Wp) {
-        const uint32_t v = stage[jl * STG + w];
-        *dst = w < G - 1 ? v : (w == G - 1 ? v & tail : 0u);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Colour / float-plane path (compute_field on arbitrary GrayImage + LabImage,
-// run_pipeline on RGB).  Same contracts as K1/K2 with float planes.
-//
-// k_rgb_planes: interleaved RGB -> gray (f32) and Lab planes via the
-// host-built 2^24-entry conversion tables (bit-identical to the reference's
-// to_gray / to_lab, image.hpp:90-140).  Device Lab planes hold one float4
-// (L, a, b, 0) per pixel, so a window sample is one 16-byte load.
-__global__ void k_rgb_planes(const uint8_t* __restrict__ rgb, size_t n, const float* __restrict__ gtab,
-                             const float* __restrict__ ltab, float* __restrict__ gray, float4* __restrict__ lab4) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = (uint32_t(rgb[3 * i]) << 16) | (uint32_t(rgb[3 * i + 1]) << 8) | uint32_t(rgb[3 * i + 2]);
-    gray[i] = __ldg(gtab + k);
-    lab4[i] = make_float4(__ldg(ltab + 3 * size_t(k)), __ldg(ltab + 3 * size_t(k) + 1), __ldg(ltab + 3 * size_t(k) + 2),
-                          0.0f);
-}
-
-// Caller Lab planes (3 floats per pixel, the reference's LabImage layout) ->
-// device float4 planes.
-__global__ void k_lab3_to_lab4(const float* __restrict__ lab, size_t n, float4* __restrict__ lab4) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    lab4[i] = make_float4(lab[3 * i], lab[3 * i + 1], lab[3 * i + 2], 0.0f);
-}
-
-// K1f: descriptor bits I(p) > I(q) on a float gray plane (descriptor.hpp:95-105,
-// 214-230).  Thread per pixel column x 4 rows; clamped float tile.
-constexpr int kDfTX = 32, kDfTY = 8, kDfPY = 4;
-
-__global__ void __launch_bounds__(kDfTX* kDfTY)
-    k_descriptor_f32(const float* __restrict__ gray, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
-                     int n, int half, int NW, int Wp, uint32_t* __restrict__ desc) {
-    extern __shared__ __align__(16) float ftile[];
-    const int TW = kDfTX + 2 * half, TH = kDfTY * kDfPY + 2 * half;
-    const int tid = threadIdx.y * kDfTX + threadIdx.x;
-    const int gx0 = blockIdx.x * kDfTX - half;
-    const int ly0 = blockIdx.y * kDfTY * kDfPY;
-    const int gy0 = ybeg + ly0 - half;
-    for (int idx = tid; idx < TW * TH; idx += kDfTX * kDfTY) {
-        const int r = idx / TW, c = idx - r * TW;
-        ftile[idx] = __ldg(gray + size_t(min(max(gy0 + r, 0), H - 1)) * W + min(max(gx0 + c, 0), W - 1));
-    }
-    __syncthreads();
-    const int x = blockIdx.x * kDfTX + threadIdx.x;
-    const float* t0 = ftile + (threadIdx.y * kDfPY + half) * TW + threadIdx.x + half;
-    for (int w = 0; w < NW; ++w) {
-        uint32_t acc[kDfPY] = {0u, 0u, 0u, 0u};
-        const int cnt = min(32, max(0, n - 32 * w));
-        if (cnt == 32) {
-            // fully unrolled: static bit positions (predicated ORs)
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int2 o = __ldg(offs + 32 * w + k);  // tile-relative (py*TW + px) of p and q
-#pragma unroll
-                for (int j = 0; j < kDfPY; ++j)
-                    if (t0[j * TW + o.x] > t0[j * TW + o.y]) acc[j] |= 1u << k;
-            }
-        } else {
-            for (int k = 0; k < cnt; ++k) {
-                const int2 o = __ldg(offs + 32 * w + k);
-#pragma unroll
-                for (int j = 0; j < kDfPY; ++j) acc[j] |= uint32_t(t0[j * TW + o.x] > t0[j * TW + o.y]) << k;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kDfPY; ++j) {
-            const int ly = ly0 + threadIdx.y * kDfPY + j;
-            if (ly < rows) desc[(size_t(ly) * NW + w) * Wp + x] = acc[j];
-        }
-    }
-}
-
-// K2f: mask on a float Lab plane (descriptor.hpp:118-154, 64-76).  One warp
-// per CTA, kM3Px pixels per CTA, one pixel per pass.  The window SADs t[slot]
-// are kept as float bit patterns (non-negative floats order like u32); lane l
-// owns pairs S l + 32m + t, forms a = max(t[P], t[Q]) for 32 pairs per chunk,
-// transposes the 32 words into bit planes (5-stage in-register 32x32 bit
-// transpose) and selects the k-th smallest MSB-first with the a <= T
-// comparator fused in -- over key bits 31..8, and over the low byte only when
-// the threshold's tie is not a single slot key.
-__device__ __forceinline__ void transpose32(uint32_t (&x)[32]) {
-    // afterwards x[j] bit t = (original x[t]) bit j
-#pragma unroll
-    for (int sidx = 0; sidx < 5; ++sidx) {
-        const int sh = 16 >> sidx;
-        const uint32_t mk = sidx == 0 ? 0x0000FFFFu : sidx == 1 ? 0x00FF00FFu : sidx == 2 ? 0x0F0F0F0Fu
-                           : sidx == 3 ? 0x33333333u : 0x55555555u;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            if (i & sh) continue;
-            const uint32_t t = ((x[i] >> sh) ^ x[i + sh]) & mk;
-            x[i + sh] ^= t;
-            x[i] ^= t << sh;
-        }
-    }
-}
-
-template <int MCH>
-__global__ void __launch_bounds__(32, 16)
-    k_mask_f32(const float4* __restrict__ lab4, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
-               const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
-               int NW, int Wp, uint32_t* __restrict__ mask, int half) {
-    // Lab samples (float4 per pixel) are read through L1 (no shared tile):
-    // shared memory holds only the slot keys and 24 rows of bit planes (the
-    // low byte's planes reuse the rows of bits 8..15), for occupancy.
-    extern __shared__ __align__(16) uint32_t dsm[];
-    uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
-    uint32_t* planes = tv + rho_words;                    // [24 rows][MCH chunks][32 lanes]
-    auto prow = [](int b) { return b >= 8 ? b - 8 : b; };  // plane row of key bit b
-    const int G = (n + 31) >> 5;
-    const int lane = threadIdx.x;
-    const int x0 = blockIdx.x * kM3Px;
-    const int ly = blockIdx.y;
-    const int y = ybeg + ly;
-    if (lane == 0) tv[u] = 0xFFFFFFFFu;  // sentinel: larger than every SAD
-    // windows of all kM3Px pixels inside the view: no clamping
-    const bool interior = x0 - half >= 0 && x0 + kM3Px - 1 + half < W && y - half >= 0 && y + half < H;
-    const int k = max(1, n / 4);
-    const unsigned full = 0xFFFFFFFFu;
-    const int rem = n & 31;
-#pragma unroll 1
-    for (int px = 0; px < kM3Px; ++px) {
-        const int x = min(x0 + px, W - 1);  // pad columns repeat the last pixel (not stored)
-        const float4 cc = __ldg(lab4 + size_t(y) * W + x);
-        // lab_sad(centre, window pixel), image.hpp:144-146
-        auto sad = [&](const float4 o) {
-            return __fadd_rn(__fadd_rn(fabsf(__fsub_rn(cc.x, o.x)), fabsf(__fsub_rn(cc.y, o.y))),
-                             fabsf(__fsub_rn(cc.z, o.z)));
-        };
-        if (interior) {
-            const float4* cp = lab4 + size_t(y) * W + x;
-#pragma unroll 8
-            for (int j = lane; j < u; j += 32) {  // 8 window samples in flight per lane
-                const int e = __ldg(uxy + j);  // (dy << 16) | (dx & 0xFFFF)
-                tv[j] = __float_as_uint(sad(__ldg(cp + ((e >> 16) * W + int(int16_t(e & 0xFFFF))))));
-            }
-        } else {
-            for (int j = lane; j < u; j += 32) {
-                const int e = __ldg(uxy + j);
-                const int gx = min(max(x + int(int16_t(e & 0xFFFF)), 0), W - 1);
-                const int gy = min(max(y + (e >> 16), 0), H - 1);
-                tv[j] = __float_as_uint(sad(__ldg(lab4 + size_t(gy) * W + gx)));
-            }
-        }
-        __syncwarp();
-        // a = max(t[P], t[Q]) of 32 positions per chunk, transposed into bit
-        // planes: bits 31..8 first (the transposes' low-byte outputs are dead
-        // code), bits 7..0 only when the top 24 bits leave the tie unresolved
-        auto planes_of = [&](auto store) {
-#pragma unroll 1
-            for (int m = 0; m < MCH; ++m) {
-                uint32_t x[32];
-#pragma unroll
-                for (int t4 = 0; t4 < 8; ++t4) {
-                    uint4 P, Q;
-                    if constexpr (MCH <= 4) {  // packed P | Q << 16 (p4 points at the packed table)
-                        P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                        Q = make_uint4(P.x >> 16, P.y >> 16, P.z >> 16, P.w >> 16);
-                        P = make_uint4(P.x & 0xFFFFu, P.y & 0xFFFFu, P.z & 0xFFFFu, P.w & 0xFFFFu);
-                    } else {
-                        P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                        Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
-                    }
-                    x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
-                    x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
-                    x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
-                    x[4 * t4 + 3] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
-                }
-                transpose32(x);
-                store(m, x);
-            }
-        };
-        planes_of([&](int m, const uint32_t (&x)[32]) {
-#pragma unroll
-            for (int j = 8; j < 32; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
-        });
-        __syncwarp();
-        // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
-        // the a <= T comparator fused in: where the threshold takes a 1, the
-        // still-equal keys with a 0 there are strictly below it.
-        uint32_t eq[MCH], lt[MCH];
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            eq[m] = ~0u;
-            lt[m] = 0u;
-        }
-        int kk = k;
-        uint32_t tbits = 0;  // threshold bits decided so far
-        auto rounds = [&](int hi, int lo) {
-#pragma unroll 1
-            for (int j = hi; j >= lo; --j) {
-                uint32_t pl[MCH], z[MCH], cnt = 0;
-#pragma unroll
-                for (int m = 0; m < MCH; ++m) {
-                    pl[m] = planes[(prow(j) * MCH + m) * 32 + lane];
-                    z[m] = eq[m] & ~pl[m];
-                    cnt += __popc(z[m]);
-                }
-                const int zeros = int(__reduce_add_sync(full, cnt));
-                if (zeros >= kk) {
-#pragma unroll
-                    for (int m = 0; m < MCH; ++m) eq[m] = z[m];
-                } else {
-                    kk -= zeros;
-                    tbits |= 1u << j;
-#pragma unroll
-                    for (int m = 0; m < MCH; ++m) {
-                        lt[m] |= z[m];
-                        eq[m] &= pl[m];
-                    }
-                }
-            }
-        };
-        rounds(31, 8);
-        // Every value is a slot key, so the positions still tied (top 24 bits
-        // equal to the threshold's) all hold the threshold itself when the
-        // slot keys with those top bits are one value: then eq is final.
-        // Otherwise (rare) the low byte is resolved on its own planes.
-        uint32_t mn = 0xFFFFFFFFu, mx = 0u;
-        for (int j = lane; j < u; j += 32) {
-            const uint32_t v = tv[j];
-            if ((v >> 8) == (tbits >> 8)) {
-                mn = min(mn, v);
-                mx = max(mx, v);
-            }
-        }
-#ifdef BSM_MASKF_ALWAYS_LOW  // test hook: resolve the low byte for every pixel
-        if (true) {
-#else
-        if (__reduce_min_sync(full, mn) != __reduce_max_sync(full, mx)) {
-#endif
-            __syncwarp();
-            planes_of([&](int m, const uint32_t (&x)[32]) {  // rows of bits 8..15 are dead now
-#pragma unroll
-                for (int j = 0; j < 8; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
-            });
-            __syncwarp();
-            rounds(7, 0);
-        }
-#pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            const int w = MCH * lane + m;
-            if (w < NW) {
-                uint32_t v = lt[m] | eq[m];
-                if (w >= G) v = 0u;
-                else if (rem && w == G - 1) v &= (1u << rem) - 1u;
-                mask[(size_t(ly) * NW + w) * Wp + x0 + px] = v;
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// --- TMA staging helpers (cp.async.bulk.tensor + mbarrier) ----------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
-}
-// 3-D box (x, word, row) of a field into shared memory, completing on bar.
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int w, int y, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];\n" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(w), "r"(y), "r"(smem_addr(bar))
-        : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
-// (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
-// :68-75 (ties -> smaller d).  No cost volume is materialised.
-// CTA tile: 128 reference pixels of one row x 64 disparities; 8 warps, warp wi
-// owns disparities [d0 + 8wi, +8), lane l owns pixels [x0 + 4l, +4): a 4 x 8
-// register block of costs, so each staged word feeds 32 word-ops from 5
-// LDS.128 (ref desc, ref mask, a 12-word window of the other view).
-// Words stream through a 3-stage ring of K = 16 words filled by TMA: one
-// thread arms the stage's mbarrier and issues three tensor-box copies
-// ([K x 128] desc, [K x 128] mask, [K x 192] other-view span); columns and
-// words outside the field arrive zero-filled, so the load path carries no
-// per-thread predicates or address arithmetic.  The argmin key is
-// (cost << 16) | d (min cost, then smaller d); d-split CTAs merge with
-// atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
-template <bool RIGHT, bool MASKED>
-__global__ void __launch_bounds__(256, 2)
-    k_cost_wta(const __grid_constant__ CUtensorMap tm_ref, const __grid_constant__ CUtensorMap tm_mask,
-               const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
-               uint32_t* __restrict__ keys, uint32_t two) {
-    constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
-    constexpr int SA = K * T, SB = K * BW;
-    constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
-    constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * 4;
-    extern __shared__ __align__(128) uint32_t csm[];
-    uint32_t* red = csm + ST * STAGE;                                 // [8][T]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full, then [ST] empty
-    uint64_t* empty = bars + ST;
-
-    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    const int x0 = blockIdx.y * T;
-    const int y = blockIdx.z;
-    const int d0 = blockIdx.x * DC;
-    const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
-    const int nchunks = (NW + K - 1) / K;
-    const int xhi = min(x0 + T, W) - 1;
-    if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
-
-    if (tid == 0) {
-        for (int s = 0; s < ST; ++s) {
-            mbar_init(bars + s, 1);
-            mbar_init(empty + s, 8);  // one arrival per warp
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    auto load_stage = [&](int c, int st) {  // thread 0 only
-        uint32_t* s = csm + st * STAGE;
-        mbar_expect_tx(bars + st, STAGE_BYTES);
-        tma_load_3d(s, &tm_ref, x0, c * K, y, bars + st);
-        if constexpr (MASKED) tma_load_3d(s + SA, &tm_mask, x0, c * K, y, bars + st);
-        tma_load_3d(s + (MASKED ? 2 * SA : SA), &tm_oth, bbase, c * K, y, bars + st);
-    };
-    if (tid == 0)
-        for (int s = 0; s < ST && s < nchunks; ++s) load_stage(s, s);
-
-    uint32_t acc[4][8], ones[4][8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            acc[j][s] = 0;
-            ones[j][s] = 0;
-        }
-
-    const int xs = lane * 4;
-    const int ds = wi * 8;
-    const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
-    const bool busy = d0 + ds < D && (RIGHT ? x0 + d0 + ds < W : xhi >= d0 + ds);
-
-#pragma unroll 1
-    for (int c = 0; c < nchunks; ++c) {
-        mbar_wait(bars + c % ST, uint32_t(c / ST) & 1u);
-        if (busy) {
-        const uint32_t* sa = csm + (c % ST) * STAGE;
-        const uint32_t* sm = sa + SA;
-        const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
-#pragma unroll 1
-        for (int w = 0; w < K; w += 2) {
-            uint32_t a[2][4], m[2][4], b[2][12];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint4 a4 = *reinterpret_cast<const uint4*>(sa + (w + h) * T + xs);
-                uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(sm + (w + h) * T + xs);
-                const uint4 b0 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0);
-                const uint4 b1 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 4);
-                const uint4 b2 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 8);
-                a[h][0] = a4.x; a[h][1] = a4.y; a[h][2] = a4.z; a[h][3] = a4.w;
-                m[h][0] = m4.x; m[h][1] = m4.y; m[h][2] = m4.z; m[h][3] = m4.w;
-                b[h][0] = b0.x; b[h][1] = b0.y; b[h][2] = b0.z; b[h][3] = b0.w;
-                b[h][4] = b1.x; b[h][5] = b1.y; b[h][6] = b1.z; b[h][7] = b1.w;
-                b[h][8] = b2.x; b[h][9] = b2.y; b[h][10] = b2.z; b[h][11] = b2.w;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int s = 0; s < 8; ++s) {
-                    const int e = RIGHT ? j + s : j - s + 8;
-                    uint32_t q0 = a[0][j] ^ b[0][e];
-                    uint32_t q1 = a[1][j] ^ b[1][e];
-                    if constexpr (MASKED) {
-                        q0 &= m[0][j];
-                        q1 &= m[1][j];
-                    }
-                    const uint32_t o = ones[j][s];
-                    const uint32_t twos = (o & q0) | (o & q1) | (q0 & q1);
-                    ones[j][s] = o ^ q0 ^ q1;
-                    acc[j][s] = __popc(twos) * two + acc[j][s];
-                }
-        }
-        }
-        // release the slot; thread 0 refills it once all 8 warps are done
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + c % ST);
-        if (tid == 0 && c + ST < nchunks) {
-            mbar_wait(empty + c % ST, uint32_t(c / ST) & 1u);
-            load_stage(c + ST, c % ST);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int s = 0; s < 8; ++s) acc[j][s] += __popc(ones[j][s]);
-
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int x = x0 + xs + j;
-        uint32_t best = 0xFFFFFFFFu;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            const int d = d0 + ds + s;
-            const int xo = RIGHT ? x + d : x - d;
-            const bool ok = d < D && x < W && xo >= 0 && xo < W;
-            const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
-            if (ok && key < best) best = key;
-        }
-        red[wi * T + xs + j] = best;
-    }
-    __syncthreads();
-    if (tid < T) {
-        uint32_t best = red[tid];
-#pragma unroll
-        for (int w = 1; w < 8; ++w) best = min(best, red[w * T + tid]);
-        const int x = x0 + tid;
-        if (x < W && best != 0xFFFFFFFFu) {
-            if (gridDim.x == 1) keys[size_t(y) * W + x] = best;
-            else atomicMin(&keys[size_t(y) * W + x], best);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K5 -- left/right check on WTA keys.  refine.hpp:39-54: valid(x) <=>
-// xr = lround(x - dL) in [0, W) and |dL - dR(xr)| <= tol (inclusive, double).
-// Also emits the (all-valid) WTA maps as float when requested, the band-local
-// max_bin of the checked map (refine.hpp:68-72) and the list of invalid
-// pixels in the refine band [rb0, rb1).
-__global__ void k_lr_check_keys(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr, int W,
-                                int rows, double tol, float* __restrict__ chk_d, uint8_t* __restrict__ chk_v,
-                                float* __restrict__ left_d, float* __restrict__ right_d, int rb0, int rb1,
-                                int* __restrict__ counters, int* __restrict__ inv) {
-    const size_t total = size_t(rows) * W;
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool in = i < total;
-    int dl = 0;
-    bool ok = false;
-    int yy = 0;
-    if (in) {
-        yy = int(i / W);
-        const int x = int(i - size_t(yy) * W);
-        dl = int(kl[i] & 0xFFFFu);
-        const int xr = x - dl;
-        ok = xr >= 0 && xr < W;
-        if (ok) ok = fabs(double(dl) - double(kr[size_t(yy) * W + xr] & 0xFFFFu)) <= tol;
-        chk_d[i] = float(dl);
-        chk_v[i] = ok ? 1 : 0;
-        if (left_d) left_d[i] = float(dl);
-        if (right_d) right_d[i] = float(kr[i] & 0xFFFFu);
-    }
-    const unsigned full = 0xFFFFFFFFu;
-    const int mb = __reduce_max_sync(full, (in && ok) ? dl : 0);
-    const bool need = in && !ok && yy >= rb0 && yy < rb1;
-    const unsigned ballot = __ballot_sync(full, need);
-    const int lane = threadIdx.x & 31;
-    int base = 0;
-    if (lane == 0) {
-        atomicMax(&counters[0], mb);
-        if (ballot) base = atomicAdd(&counters[1], __popc(ballot));
-    }
-    base = __shfl_sync(full, base, 0);
-    if (need) inv[base + __popc(ballot & ((1u << lane) - 1u))] = int(i);
-}
-
-// lr_check on float maps (per-stage API, refine.hpp:39-54).
-__global__ void k_lr_check_float(const float* __restrict__ dl, const float* __restrict__ dr, int W, int H,
-                                 double tol, float* __restrict__ od, uint8_t* __restrict__ ov) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= size_t(W) * H) return;
-    const int y = int(i / W), x = int(i - size_t(y) * W);
-    const float d = dl[i];
-    const long long xr = llround(double(x) - double(d));
-    bool ok = xr >= 0 && xr < W;
-    if (ok) ok = fabs(double(d) - double(dr[size_t(y) * W + xr])) <= tol;
-    od[i] = d;
-    ov[i] = ok ? 1 : 0;
-}
-
-// ---------------------------------------------------------------------------
-// K6 -- bilateral voting refinement.  refine.hpp:62-111.  Warp per invalid
-// pixel.  Voters of one window row are examined 32 at a time (lane = column);
-// their bin lround(d) and weight (exact host table, refine.hpp:30-35) are
-// formed in parallel, then folded into the per-warp double bins strictly in
-// row-major voter order (the owner lane of a bin performs its adds in
-// sequence), so every bin sum is bit-identical to the reference's.  Argmax:
-// strict '>' from bin 0 == smallest bin among the maxima.
-__global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __restrict__ cv,
-                              const uint8_t* __restrict__ gray, int W, int rows, int radius,
-                              const double* __restrict__ wtab, int ncol, const int16_t* __restrict__ s2col,
-                              const int* __restrict__ counters, const int* __restrict__ inv,
-                              int nbins_cap, float* __restrict__ od, uint8_t* __restrict__ ov) {
-    extern __shared__ __align__(16) double sbins[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    double* bins = sbins + size_t(warp) * nbins_cap;
-    const int max_bin = counters[0];
-    const int n_inv = counters[1];
-    const unsigned full = 0xFFFFFFFFu;
-    for (int idx = blockIdx.x * nwarps + warp; idx < n_inv; idx += gridDim.x * nwarps) {
-        const int p = inv[idx];
-        const int y = p / W, x = p - y * W;
-        const int u = gray[p];
-        for (int b = lane; b <= max_bin; b += 32) bins[b] = 0.0;
-        __syncwarp();
-        const int y0 = max(0, y - radius), y1 = min(rows - 1, y + radius);
-        const int x0 = max(0, x - radius), x1 = min(W - 1, x + radius);
-        bool any = false;
-        for (int py = y0; py <= y1; ++py) {
-            const int dy2 = (py - y) * (py - y);
-            for (int cx = x0; cx <= x1; cx += 32) {
-                const int px = cx + lane;
-                const size_t j = size_t(py) * W + px;
-                const bool valid = px <= x1 && cv[j];
-                int bin = 0;
-                double wgt = 0.0;
-                if (valid) {
-                    bin = int(llround(double(cd[j])));
-                    const int v = gray[j];
-                    const int hi = max(u, v), lo = min(u, v);
-                    const int s = (px - x) * (px - x) + dy2;
-                    wgt = __ldg(wtab + (size_t(hi * (hi + 1) / 2 + lo) * ncol + s2col[s]));
-                }
-                unsigned m = __ballot_sync(full, valid);
-                any |= m != 0;
-                while (m) {
-                    const int i = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int b = __shfl_sync(full, bin, i);
-                    const double wv = __shfl_sync(full, wgt, i);
-                    if (lane == (b & 31)) bins[b] += wv;
-                }
-            }
-        }
-        __syncwarp();
-        if (!any) {
-            if (lane == 0) {
-                od[p] = 0.0f;
-                ov[p] = 0;
-            }
-            continue;
-        }
-        double bv = -1.0;
-        int bb = 0x7FFFFFFF;
-        for (int b = lane; b <= max_bin; b += 32)
-            if (bins[b] > bv) {
-                bv = bins[b];
-                bb = b;
-            }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov2 = __shfl_xor_sync(full, bv, o);
-            const int ob = __shfl_xor_sync(full, bb, o);
-            if (ov2 > bv || (ov2 == bv && ob < bb)) {
-                bv = ov2;
-                bb = ob;
-            }
-        }
-        if (lane == 0) {
-            od[p] = float(bb);
-            ov[p] = 1;
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K6' -- voting refinement, thread per invalid pixel (refine.hpp:62-111).
-// Each thread walks its clipped (2r+1)^2 window in row-major order and adds
-// every valid voter's exact weight to its own column of double bins in
-// shared memory ([bin][thread]: a lane always hits its own bank pair, so any
-// mix of bins is conflict-free).  Per bin the additions happen in the
-// reference's voter order, so the sums are bit-identical.  Voter data comes
-// pre-packed (k_make_vmap: bin | gray << 16 | valid << 24); the window offset
-// (dy, dx) is warp-uniform, so the distance column of the weight table is a
-// broadcast.  Used when the bins fit (nbins * 8 B * 32 threads); otherwise
-// the warp-per-pixel k_vote_refine runs.
-__global__ void k_make_vmap(const float* __restrict__ cd, const uint8_t* __restrict__ cv,
-                            const uint8_t* __restrict__ gray, size_t n, uint32_t* __restrict__ vmap) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t g = gray ? uint32_t(gray[i]) << 16 : 0u;
-    vmap[i] = cv[i] ? (g | (1u << 24) | uint32_t(llround(double(cd[i])))) : g;
-}
-
-// ---------------------------------------------------------------------------
-// K6'' -- voting refinement with device-computed weights.  vote_weight
-// (refine.hpp:30-35) = exp(-(double(lab_sad)/lc + sqrt(dx^2+dy^2)/le)):
-// lab_sad in float (same association), the divisions and the sum in IEEE
-// double, and exp by a restatement of glibc's e_exp.c (FMA build) whose
-// table and constants come from the host's libm and were validated bit for
-// bit against it (bsmh::glibc_exp_params).  sqrt(s)/le depends only on the
-// warp-uniform window offset and comes from a small host table.  Thread per
-// invalid pixel, own column of double bins in shared memory; per bin the adds
-// follow the reference's row-major voter order.
-struct ExpDev {
-    double invln2N, shift, negln2hiN, negln2loN, c2, c3, c4, c5;
-};
-
-__device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const unsigned long long* tab) {
-    // e_exp.c: |x| < 2^-54 -> 1 + x;  |x| >= 1024 -> 0 / inf;  512 <= |x| < 1024
-    // -> specialcase (the scale is built with a biased exponent).
-    const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
-    const unsigned abstop = unsigned(xb >> 52) & 0x7ffu;
-    bool special = false;
-    if (abstop - 0x3c9u >= 0x3fu) {
-        if (int(abstop) - 0x3c9 < 0) return 1.0 + x;
-        if (abstop >= 0x409u) return (xb >> 63) ? 0.0 : __longlong_as_double(0x7ff0000000000000ll);
-        special = true;
-    }
-    double kd = fma(x, p.invln2N, p.shift);
-    const unsigned long long ki = static_cast<unsigned long long>(__double_as_longlong(kd));
-    kd -= p.shift;
-    const double r = fma(kd, p.negln2loN, fma(kd, p.negln2hiN, x));
-    const unsigned idx = 2u * unsigned(ki & 127ull);
-    const unsigned long long top = ki << 45;
-    const double tail = __longlong_as_double(static_cast<long long>(tab[idx]));
-    unsigned long long sbits = tab[idx + 1] + top;
-    const double r2 = r * r;
-    const double tmp = fma(r2 * r2, fma(r, p.c5, p.c4), fma(fma(r, p.c3, p.c2), r2, tail + r));
-    if (!special) {
-        const double scale = __longlong_as_double(static_cast<long long>(sbits));
-        return fma(scale, tmp, scale);
-    }
-    if (!(ki & 0x80000000ull)) {  // k > 0 (x >= 512): overflow range
-        sbits -= 1009ull << 52;
-        const double scale = __longlong_as_double(static_cast<long long>(sbits));
-        return 0x1p1009 * __dadd_rn(scale, __dmul_rn(scale, tmp));
-    }
-    sbits += 1022ull << 52;  // k < 0: subnormal range, rounded once
-    const double scale = __longlong_as_double(static_cast<long long>(sbits));
-    const double st = __dmul_rn(scale, tmp);
-    double y = __dadd_rn(scale, st);
-    if (y < 1.0) {
-        const double hi = __dadd_rn(y, 1.0);
-        const double lo = __dadd_rn(__dsub_rn(scale, y), st);
-        const double l2 = __dadd_rn(__dadd_rn(__dsub_rn(1.0, hi), y), lo);
-        y = __dsub_rn(__dadd_rn(l2, hi), 1.0);
-        if (y == 0.0) y = 0.0;
-    }
-    return __dmul_rn(y, 0x1p-1022);
-}
-
-// K6d -- voting refinement, NP invalid pixels per warp (LPP = 32/NP lanes
-// each).  Per window row the LPP lanes of a pixel form the bins and weights of
-// LPP consecutive voters in parallel (weight from the exact host table, or
-// the device exp for Lab planes; the loads of a batch of CB chunks are issued
-// together), stage them, then fold them in voter order: lane sl owns the bins
-// b with (b % LPP) == sl, finds its entries of the chunk from ballots of the
-// valid flag and the residue bits, and walks them in order, keeping its
-// current bin's running sum in a register.  Per bin the additions are
-// therefore the reference's row-major sequence; the NP pixels fold side by
-// side.
-template <int NP, bool DEVEXP>
-__global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
-    const uint32_t* __restrict__ vmap, const float4* __restrict__ lab, const float* __restrict__ lab256, int W,
-    int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
-    const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
-    const int16_t* __restrict__ s2col, const int* __restrict__ counters, const int* __restrict__ inv, int nbins_cap,
-    float* __restrict__ od, uint8_t* __restrict__ ov, int* __restrict__ work) {
-    constexpr int LPP = 32 / NP;
-    extern __shared__ __align__(16) double fsm[];
-    unsigned long long* stab = reinterpret_cast<unsigned long long*>(fsm);  // 256 (DEVEXP)
-    float* slab = reinterpret_cast<float*>(stab + 256);                     // 768 (DEVEXP, gray)
-    const int nwarps = blockDim.x >> 5;
-    double* sw_all = reinterpret_cast<double*>(slab + 768);                 // [warps][32] staged weights
-    int* sb_all = reinterpret_cast<int*>(sw_all + nwarps * 32);             // [warps][32] staged bins
-    double* bins_all = reinterpret_cast<double*>(sb_all + nwarps * 32);     // [warps][NP][nbins_cap]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane / LPP, sl = lane % LPP;
-    if (DEVEXP) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) stab[i] = etab[i];
-        if (!lab)
-            for (int i = threadIdx.x; i < 768; i += blockDim.x) slab[i] = lab256[i];
-    }
-    __syncthreads();
-    double* sw = sw_all + warp * 32;
-    int* sbn = sb_all + warp * 32;
-    double* bins = bins_all + size_t(warp * NP + sub) * nbins_cap;
-    const unsigned full = 0xFFFFFFFFu;
-    const unsigned submask = (LPP == 32) ? full : (((1u << LPP) - 1u) << (sub * LPP));
-    const int max_bin = counters[0];
-    const int n_inv = counters[1];
-    // groups of NP pixels are taken from a work counter (*work == 0 at
-    // launch): the voter count varies per pixel, so a static stride leaves a tail
-    auto grab = [&]() {
-        int b = 0;
-        if (lane == 0) b = atomicAdd(work, NP);
-        return __shfl_sync(0xFFFFFFFFu, b, 0);
-    };
-    for (int base = grab(); base < n_inv; base = grab()) {  // warp-uniform loop
-        const int idx = base + sub;
-        const bool live = idx < n_inv;
-        const int p = live ? inv[idx] : 0;
-        const int y = p / W, x = p - y * W;
-        const uint32_t e0 = vmap[p];
-        const int u = int((e0 >> 16) & 0xFFu);
-        float lx0 = 0.f, lx1 = 0.f, lx2 = 0.f;
-        if (DEVEXP) {
-            if (lab) {
-                const float4 c = lab[p];
-                lx0 = c.x;
-                lx1 = c.y;
-                lx2 = c.z;
-            } else {
-                lx0 = slab[3 * u];
-                lx1 = slab[3 * u + 1];
-                lx2 = slab[3 * u + 2];
-            }
-        }
-        for (int b = sl; b <= max_bin; b += LPP) bins[b] = 0.0;
-        int cur = -1;
-        double acc = 0.0;
-        bool any = false;
-        const int tu = u * (u + 1) / 2;
-        // Per window row, the loads of CB chunks (LPP voters each) are issued
-        // together (vmap, then the weights), then the chunks fold in order:
-        // one L2 round trip per batch instead of one per chunk.
-        constexpr int CB = 6;
-        const int nch = (2 * radius + LPP) / LPP;  // ceil((2r + 1) / LPP)
-        for (int dy = -radius; dy <= radius; ++dy) {
-            const int py = y + dy;
-            const bool rowok = live && py >= 0 && py < rows;
-            const uint32_t* row = vmap + size_t(rowok ? py : 0) * W;
-            const int dy2 = dy * dy;
-            for (int c0 = 0; c0 < nch; c0 += CB) {
-                uint32_t ev[CB];
-#pragma unroll
-                for (int k = 0; k < CB; ++k) {
-                    const int dx = -radius + (c0 + k) * LPP + sl;
-                    const int px = x + dx;
-                    ev[k] = (rowok && dx <= radius && px >= 0 && px < W) ? __ldg(row + px) : 0u;
-                }
-                int bv[CB];
-                double wv[CB];
-#pragma unroll
-                for (int k = 0; k < CB; ++k) {
-                    const uint32_t e = ev[k];
-                    const int dx = -radius + (c0 + k) * LPP + sl;
-                    bv[k] = -1;
-                    wv[k] = 0.0;
-                    if (e & (1u << 24)) {
-                        bv[k] = int(e & 0xFFFFu);
-                        const int v = int((e >> 16) & 0xFFu);
-                        if (DEVEXP) {
-                            float l0, l1, l2;
-                            if (lab) {
-                                const float4 o = __ldg(lab + size_t(py) * W + x + dx);
-                                l0 = o.x;
-                                l1 = o.y;
-                                l2 = o.z;
-                            } else {
-                                l0 = slab[3 * v];
-                                l1 = slab[3 * v + 1];
-                                l2 = slab[3 * v + 2];
-                            }
-                            const float sad = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(lx0, l0)), fabsf(__fsub_rn(lx1, l1))),
-                                                        fabsf(__fsub_rn(lx2, l2)));
-                            const double arg = -(__ddiv_rn(double(sad), lc) + __ldg(e_over_le + dx * dx + dy2));
-                            wv[k] = exp_glibc(arg, ep, stab);
-                        } else {
-                            const int tri = v >= u ? (v * (v + 1) / 2 + u) : (tu + v);
-                            wv[k] = __ldg(wtab + size_t(tri) * ncol + s2col[dx * dx + dy2]);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < CB; ++k) {
-                    if (c0 + k >= nch) break;  // warp-uniform
-                    const int bin = bv[k];
-                    const double w = wv[k];
-                    // owner lane of bin b: b % LPP; the entries each owner
-                    // takes come from four ballots (valid + residue bits)
-                    const unsigned vb = __ballot_sync(full, bin >= 0) & submask;
-                    unsigned mine = vb >> (sub * LPP);
-#pragma unroll
-                    for (int kb = 0; (1 << kb) < LPP; ++kb) {
-                        const unsigned bk = __ballot_sync(full, (bin >> kb) & 1) >> (sub * LPP);
-                        mine &= ((sl >> kb) & 1) ? bk : ~bk;
-                    }
-                    any |= vb != 0u;
-                    sbn[lane] = bin;
-                    sw[lane] = w;
-                    __syncwarp();
-                    while (mine) {
-                        const int j = sub * LPP + __ffs(mine) - 1;
-                        mine &= mine - 1;
-                        const int b = sbn[j];
-                        if (b != cur) {
-                            if (cur >= 0) bins[cur] = acc;
-                            cur = b;
-                            acc = bins[b];
-                        }
-                        acc += sw[j];
-                    }
-                    __syncwarp();
-                }
-            }
-        }
-        if (cur >= 0) bins[cur] = acc;
-        __syncwarp();
-        // argmax: strict '>' from bin 0 == first bin holding the maximum
-        double bv = -1.0;
-        int bb = 0x7FFFFFFF;
-        for (int b = sl; b <= max_bin; b += LPP)
-            if (bins[b] > bv) {
-                bv = bins[b];
-                bb = b;
-            }
-#pragma unroll
-        for (int o = LPP / 2; o > 0; o >>= 1) {
-            const double ov2 = __shfl_xor_sync(full, bv, o);
-            const int ob = __shfl_xor_sync(full, bb, o);
-            if (ov2 > bv || (ov2 == bv && ob < bb)) {
-                bv = ov2;
-                bb = ob;
-            }
-        }
-        if (live && sl == 0) {
-            od[p] = any ? float(bb) : 0.0f;
-            ov[p] = any ? 1 : 0;
-        }
-        __syncwarp();
-    }
-}
-
-__global__ void k_exp_eval(const double* __restrict__ x, int n, ExpDev ep, const unsigned long long* __restrict__ tab,
-                           double* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = exp_glibc(x[i], ep, tab);
-}
-
-// ---------------------------------------------------------------------------
-// Layout converters for the per-stage API (reference AoS u64 <-> device SoA).
-__global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
-                             uint32_t* __restrict__ dst) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, w, x)
-    const size_t total = size_t(H) * NW * Wp;
-    if (i >= total) return;
-    const int x = int(i % Wp);
-    const size_t yw = i / Wp;
-    const int w = int(yw % NW), y = int(yw / NW);
-    dst[i] = x < W ? src[(size_t(y) * W + x) * NW + w] : 0u;
-}
-
-__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
-                             uint32_t* __restrict__ dst) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
-    const size_t total = size_t(H) * W * NW;
-    if (i >= total) return;
-    const int w = int(i % NW);
-    const size_t yx = i / NW;
-    const int x = int(yx % W), y = int(yx / W);
-    dst[i] = src[(size_t(y) * NW + w) * Wp + x];
-}
-
-// k_soa_to_aos with the pipeline's bit order undone: reference bit k of a
-// pixel's string is device bit pos[k].
-__global__ void k_soa_to_aos_perm(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
-                                  const int* __restrict__ pos, int n, uint32_t* __restrict__ dst) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
-    const size_t total = size_t(H) * W * NW;
-    if (i >= total) return;
-    const int w = int(i % NW);
-    const size_t yx = i / NW;
-    const int x = int(yx % W), y = int(yx / W);
-    uint32_t v = 0;
-    for (int b = 0; b < 32 && 32 * w + b < n; ++b) {
-        const int j = __ldg(pos + 32 * w + b);
-        v |= ((__ldg(src + (size_t(y) * NW + (j >> 5)) * Wp + x) >> (j & 31)) & 1u) << b;
-    }
-    dst[i] = v;
-}
-
-__global__ void k_keys_to_float(const uint32_t* __restrict__ keys, size_t n, float* __restrict__ out) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = float(keys[i] & 0xFFFFu);
-}
-
-// Roofline microbenchmarks of the cost kernel's inner loop (register-only,
-// 8 independent chains per thread, 2048 threads per SM):
-//   k_popc_peak: one word per LOP3 + POPC + IADD (the direct mix);
-//   k_csa_peak:  two words per 4 LOP3 + POPC + IMAD (the carry-save mix the
-//                kernel uses; balances the ALU and POPC pipes).
-__global__ void __launch_bounds__(512) k_popc_peak(uint32_t* out, uint32_t seed, int iters) {
-    uint32_t a[8], b[8], m[8], s[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        a[i] = seed * (threadIdx.x + i + 1);
-        b[i] = a[i] ^ (0x9e3779b9u * i);
-        m[i] = ~a[i] + i;
-        s[i] = 0;
-    }
-    for (int it = 0; it < iters; it++) {
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const uint32_t x = __popc((a[i] ^ b[i]) & m[i]);
-            s[i] += x;
-            b[i] += x;
-        }
-    }
-    uint32_t r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; i++) r += s[i];
-    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
-}
-
-__global__ void __launch_bounds__(512) k_csa_peak(uint32_t* out, uint32_t seed, int iters, uint32_t two) {
-    uint32_t a[8], b[8], m[8], o[8], s[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        a[i] = seed * (threadIdx.x + i + 1);
-        b[i] = (seed + 0x9e3779b9u) * (threadIdx.x * 7u + i + 3u);
-        m[i] = ~a[i] + i;
-        o[i] = 0;
-        s[i] = 0;
-    }
-    for (int it = 0; it < iters; it++) {
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const uint32_t x0 = (a[i] ^ s[i]) & m[i];
-            const uint32_t x1 = (b[i] ^ o[i]) & m[i];
-            const uint32_t t = (o[i] & x0) | (o[i] & x1) | (x0 & x1);
-            o[i] = o[i] ^ x0 ^ x1;
-            s[i] = __popc(t) * two + s[i];
-        }
-    }
-    uint32_t r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; i++) r += s[i] + o[i];
-    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
-}
+#include "kern_field.cuh"
+#include "kern_cost.cuh"
+#include "kern_refine.cuh"
+#include "kern_misc.cuh"
 
 }  // namespace
 

@@ -1,0 +1,189 @@
+// kern_cost.cuh -- K3: TMA staging helpers and the fused masked-Hamming cost +
+// winner-take-all kernel.  Part of bsm_kernels.cu's single translation unit.
+#pragma once
+
+// --- TMA staging helpers (cp.async.bulk.tensor + mbarrier) ----------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+// 3-D box (x, word, row) of a field into shared memory, completing on bar.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int w, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(w), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
+// (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
+// :68-75 (ties -> smaller d).  No cost volume is materialised.
+// CTA tile: 128 reference pixels of one row x 64 disparities; 8 warps, warp wi
+// owns disparities [d0 + 8wi, +8), lane l owns pixels [x0 + 4l, +4): a 4 x 8
+// register block of costs, so each staged word feeds 32 word-ops from 5
+// LDS.128 (ref desc, ref mask, a 12-word window of the other view).
+// Words stream through a 3-stage ring of K = 16 words filled by TMA: one
+// thread arms the stage's mbarrier and issues three tensor-box copies
+// ([K x 128] desc, [K x 128] mask, [K x 192] other-view span); columns and
+// words outside the field arrive zero-filled, so the load path carries no
+// per-thread predicates or address arithmetic.  The argmin key is
+// (cost << 16) | d (min cost, then smaller d); d-split CTAs merge with
+// atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
+template <bool RIGHT, bool MASKED>
+__global__ void __launch_bounds__(256, 2)
+    k_cost_wta(const __grid_constant__ CUtensorMap tm_ref, const __grid_constant__ CUtensorMap tm_mask,
+               const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
+               uint32_t* __restrict__ keys, uint32_t two) {
+    constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
+    constexpr int SA = K * T, SB = K * BW;
+    constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
+    constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * 4;
+    extern __shared__ __align__(128) uint32_t csm[];
+    uint32_t* red = csm + ST * STAGE;                                 // [8][T]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full, then [ST] empty
+    uint64_t* empty = bars + ST;
+
+    const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const int x0 = blockIdx.y * T;
+    const int y = blockIdx.z;
+    const int d0 = blockIdx.x * DC;
+    const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
+    const int nchunks = (NW + K - 1) / K;
+    const int xhi = min(x0 + T, W) - 1;
+    if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(bars + s, 1);
+            mbar_init(empty + s, 8);  // one arrival per warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto load_stage = [&](int c, int st) {  // thread 0 only
+        uint32_t* s = csm + st * STAGE;
+        mbar_expect_tx(bars + st, STAGE_BYTES);
+        tma_load_3d(s, &tm_ref, x0, c * K, y, bars + st);
+        if constexpr (MASKED) tma_load_3d(s + SA, &tm_mask, x0, c * K, y, bars + st);
+        tma_load_3d(s + (MASKED ? 2 * SA : SA), &tm_oth, bbase, c * K, y, bars + st);
+    };
+    if (tid == 0)
+        for (int s = 0; s < ST && s < nchunks; ++s) load_stage(s, s);
+
+    uint32_t acc[4][8], ones[4][8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            acc[j][s] = 0;
+            ones[j][s] = 0;
+        }
+
+    const int xs = lane * 4;
+    const int ds = wi * 8;
+    const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
+    const bool busy = d0 + ds < D && (RIGHT ? x0 + d0 + ds < W : xhi >= d0 + ds);
+
+#pragma unroll 1
+    for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(bars + c % ST, uint32_t(c / ST) & 1u);
+        if (busy) {
+        const uint32_t* sa = csm + (c % ST) * STAGE;
+        const uint32_t* sm = sa + SA;
+        const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
+#pragma unroll 1
+        for (int w = 0; w < K; w += 2) {
+            uint32_t a[2][4], m[2][4], b[2][12];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 a4 = *reinterpret_cast<const uint4*>(sa + (w + h) * T + xs);
+                uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(sm + (w + h) * T + xs);
+                const uint4 b0 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 4);
+                const uint4 b2 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 8);
+                a[h][0] = a4.x; a[h][1] = a4.y; a[h][2] = a4.z; a[h][3] = a4.w;
+                m[h][0] = m4.x; m[h][1] = m4.y; m[h][2] = m4.z; m[h][3] = m4.w;
+                b[h][0] = b0.x; b[h][1] = b0.y; b[h][2] = b0.z; b[h][3] = b0.w;
+                b[h][4] = b1.x; b[h][5] = b1.y; b[h][6] = b1.z; b[h][7] = b1.w;
+                b[h][8] = b2.x; b[h][9] = b2.y; b[h][10] = b2.z; b[h][11] = b2.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const int e = RIGHT ? j + s : j - s + 8;
+                    uint32_t q0 = a[0][j] ^ b[0][e];
+                    uint32_t q1 = a[1][j] ^ b[1][e];
+                    if constexpr (MASKED) {
+                        q0 &= m[0][j];
+                        q1 &= m[1][j];
+                    }
+                    const uint32_t o = ones[j][s];
+                    const uint32_t twos = (o & q0) | (o & q1) | (q0 & q1);
+                    ones[j][s] = o ^ q0 ^ q1;
+                    acc[j][s] = __popc(twos) * two + acc[j][s];
+                }
+        }
+        }
+        // release the slot; thread 0 refills it once all 8 warps are done
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + c % ST);
+        if (tid == 0 && c + ST < nchunks) {
+            mbar_wait(empty + c % ST, uint32_t(c / ST) & 1u);
+            load_stage(c + ST, c % ST);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) acc[j][s] += __popc(ones[j][s]);
+
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int x = x0 + xs + j;
+        uint32_t best = 0xFFFFFFFFu;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int d = d0 + ds + s;
+            const int xo = RIGHT ? x + d : x - d;
+            const bool ok = d < D && x < W && xo >= 0 && xo < W;
+            const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
+            if (ok && key < best) best = key;
+        }
+        red[wi * T + xs + j] = best;
+    }
+    __syncthreads();
+    if (tid < T) {
+        uint32_t best = red[tid];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) best = min(best, red[w * T + tid]);
+        const int x = x0 + tid;
+        if (x < W && best != 0xFFFFFFFFu) {
+            if (gridDim.x == 1) keys[size_t(y) * W + x] = best;
+            else atomicMin(&keys[size_t(y) * W + x], best);
+        }
+    }
+}
