@@ -1,0 +1,58 @@
+"""bench.py's contract on the CPU side: the reference arm (the compiled
+reference on host cores, the one leg that needs no GPU) and the clock sampler.
+The GPU leg's line is checked by the driver on the B200 (see profiles/)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+REF_SO = os.path.join(ROOT, "oracle", "_ref")
+
+
+def _bench(*args, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=600, env=e, cwd=ROOT)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SO), reason="oracle/_ref not built")
+@pytest.mark.parametrize("workload", ["c1", "c2"])
+def test_reference_arm_json_contract(workload):
+    r = _bench("--impl", "reference", "--workload", workload, "--steps", "2", "--warmup", "1", "--ref-rows", "4")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1  # one JSON line
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference"
+    assert d["metric"] == d["unit"] == "Mdisp-evals/s"
+    assert d["higher_is_better"] is True and d["steps"] == 2 and d["n_gpus"] == 1
+    assert d["value"] > 0 and d["vs_baseline"] is None
+    assert d["config"]["workload"].startswith(workload)
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"] and "sample" in cb
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_other_ranks_exit_quietly():
+    r = _bench("--impl", "reference", "--steps", "1", "--warmup", "0", env={"RANK": "1", "WORLD_SIZE": "2"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
+
+
+def test_clock_sampler_reports_without_a_gpu():
+    import bench
+    c = bench.ClockSampler(0)
+    with c:
+        pass
+    s = c.summary()
+    assert "reasons" in s and isinstance(s["reasons"], list)
+    assert "sm_mhz" in s and "sm_max_mhz" in s
