@@ -56,3 +56,21 @@ def test_clock_sampler_reports_without_a_gpu():
     s = c.summary()
     assert "reasons" in s and isinstance(s["reasons"], list)
     assert "sm_mhz" in s and "sm_max_mhz" in s
+
+
+@pytest.mark.gpu
+def test_gpu_line_json_contract():
+    r = _bench("--workload", "c1", "--steps", "3", "--warmup", "3", "--ref-rows", "4")
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "cpu_baseline", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 9 * 3  # descriptor, mask, WTA (x2 each), LR check, vmap, refine per step
+    rf = d["roofline"]
+    assert 0 < rf["frac"] <= 1.0 and rf["achieved"] > 0 and rf["peak"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] > 0
+    assert isinstance(d["clocks"]["reasons"], list)
