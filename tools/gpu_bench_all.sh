@@ -11,3 +11,5 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 echo "torchrun rc=$?"; cut -c1-300 gpurun_out/${TAG}_bench_torchrun.json
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_reference.json 2> gpurun_out/${TAG}_bench_reference.err
 echo "reference rc=$?"; cat gpurun_out/${TAG}_bench_reference.json
+timeout 900 python bench.py --impl reference --workload c2rgb --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_reference_c2rgb.json 2> gpurun_out/${TAG}_bench_reference_c2rgb.err
+echo "reference c2rgb rc=$?"; cut -c1-300 gpurun_out/${TAG}_bench_reference_c2rgb.json

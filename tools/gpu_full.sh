@@ -15,4 +15,9 @@ bash tools/gpu_prof.sh ${TAG} c2
 for K in k_cost_wta k_mask4 k_descriptor4 k_vote_refine_fold k_lr_check_keys; do
   python tools/summarize_ncu.py gpurun_out/${TAG}_${K}.ncu-rep >> gpurun_out/${TAG}_ncu_kernels_c2.txt 2>&1
 done
+# colour path: the three colour kernels of one c2-size RGB pipeline in one report
+timeout 300 python tools/profile_colour.py > gpurun_out/${TAG}_colour_plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_mask_f32|k_descriptor_f32|k_rgb_planes" -c 4 \
+      -o gpurun_out/${TAG}_colour python tools/profile_colour.py > gpurun_out/${TAG}_colour_ncu.log 2>&1; echo "ncu colour rc=$?"
+python tools/summarize_ncu.py gpurun_out/${TAG}_colour.ncu-rep > gpurun_out/${TAG}_ncu_kernels_c2rgb.txt 2>&1
 echo done
