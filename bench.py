@@ -3,26 +3,38 @@
 
 metric: Mdisp-evals/s = W*H*D per second (BASELINE.json), whole job.
 
-Default workload: BASELINE.json configs[1] (1392x1104, D=240, the largest
-single-pair config quoted for 1 GPU).  One step = one full run_pipeline of one
-stereo pair: descriptors + masks of both views, masked WTA in both
-directions, left/right check, voting refinement.  N > 1 (torchrun): every rank
-matches its own pair (independent units, weak scaling, no data-path
-collective -- the batch partition of configs[3]).
+Default workload: BASELINE.json configs[3] -- a batch of 64 synthetic
+1920x1080 pairs, D=192, the config the metric's "1/2/4/8 B200" is quoted on.
+One step = run_pipeline (descriptors + masks of both views, masked WTA in both
+directions, left/right check, voting refinement) of ALL 64 pairs; with N
+ranks (torchrun) rank r matches pairs shard_units(64, N, r) -- independent
+units, fixed total work (strong scaling), no data-path collective.
+`--workload c5` at N > 1 is the row-band partition of configs[4] (one NCCL
+all-gather of the refined bands); the single-pair configs (c1, c2, c3, c2rgb)
+run one pair per rank (replicas).
 
-  value   device-resident inputs, CUDA events on the library's stream per step
-          (L2 flushed by a 256 MiB write before each step, outside the events)
-  e2e     the public C-ABI call bsm_pipeline_u8 with pinned HOST buffers: the
-          H2D of both views and the D2H of the refined map (float + valid) are
-          inside the timed region
-  roofline  the dominant kernel (fused masked-Hamming cost + WTA) against the
-          measured POPC word-op rate of this GPU (it is POPC-issue bound, not
-          HBM bound -- see DESIGN.md); hbm_frac beside it
+  value   device-resident views (inputs in HBM before the timed region),
+          CUDA events on the library's stream; a 256 MiB L2 flush before each
+          step (outside the events)
+  e2e     the public C-ABI call a user makes (bsm_pipeline_batch_u8 for the
+          batch, bsm_pipeline_u8 / _rgb for one pair) with pinned HOST
+          buffers: the H2D of every view and the D2H of every refined map
+          (float + valid) are inside the timed region
+  roofline  the fused cost + WTA kernel (K3) against the nominal issue bound
+          of its integer pipes (ALU 64 LOP3 + XU 16 POPC per clk per SM: the
+          carry-save mix needs 2 LOP3 + 0.5 POPC per word-op, so 32 word-ops
+          per clk per SM); the live microbenchmark of that mix beside it;
+          `roofline_mask` does the same for the mask kernel (K2) against its
+          shared-memory gather floor
   cpu_baseline  the reference library compiled in place (oracle/_ref), all
-          host threads, on a bounded row band of the same workload
+          host threads, median of repeated runs on a row band of pair 0
+  cold_start  context creation + pattern upload + first pipeline (tables)
 
 --impl reference: the reference CPU implementation alone (rank 0), same
-metric, on a bounded row band per step.
+metric and config; the K timed steps tile pair 0 of the workload row-band by
+row-band (each band run through run_pipeline as its own image), so the run
+covers one whole frame; value = median over steps (time_pipeline's median,
+eval.hpp:144-159).
 """
 from __future__ import annotations
 
@@ -42,6 +54,8 @@ sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
+WORDOPS_PER_CLK_SM = 32  # ALU: 64 LOP3/clk/SM at 2 LOP3 per word-op; XU: 16 POPC/clk/SM at 0.5 per word-op
+WORKLOADS_CLI = ["c1", "c2", "c3", "c4", "c5", "c2rgb"]
 
 
 def env_int(k, d):
@@ -131,108 +145,207 @@ def in_bounds_evals(W, H, D):
     return H * (W * Dc - Dc * (Dc - 1) // 2)
 
 
-def cpu_reference_sample(workload, rows, threads, pairs_arr):
-    """Reference pipeline (oracle/_ref) on a row band of the workload's pair."""
-    import oracle
-    from paper_1402_2020_b200.synth import workload_pair
-    ref = oracle.Reference()
-    left, right = workload_pair(workload)
-    y0 = (left.shape[0] - rows) // 2
-    L = np.ascontiguousarray(left[y0:y0 + rows])
-    R = np.ascontiguousarray(right[y0:y0 + rows])
-    from paper_1402_2020_b200.synth import WORKLOADS
-    w = WORKLOADS[workload]
-    out = ref.pipeline(L, R, pairs_arr, 26, w.d_max, threads=threads, channels=3 if L.ndim == 3 else 1)
-    return out["seconds"], L.shape[1] * rows * w.d_max, os.path.basename(ref.path)
+# ---------------------------------------------------------------------------
+# CPU legs: the reference compiled in place (oracle/_ref); inputs come from the
+# generator compiled into that same library, so no product library is loaded.
+def cpu_info() -> dict:
+    model, mhz = None, []
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                elif ln.startswith("cpu MHz"):
+                    mhz.append(float(ln.split(":", 1)[1]))
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"nproc": usable, "cpu_count": os.cpu_count(), "model": model,
+            "mhz_median": statistics.median(mhz) if mhz else None}
+
+
+def ref_inputs(ref, key: str, index: int = 0):
+    from paper_1402_2020_b200.synth import workload_pair_with
+    return workload_pair_with(ref.synth_pair, key, index)
+
+
+def ref_band(ref, pairs_arr, left, right, y0, y1, d_max, threads):
+    """run_pipeline of rows [y0, y1) as their own image; (seconds, W*rows*D)."""
+    L = np.ascontiguousarray(left[y0:y1])
+    R = np.ascontiguousarray(right[y0:y1])
+    out = ref.pipeline(L, R, pairs_arr, 26, d_max, threads=threads, channels=3 if L.ndim == 3 else 1)
+    return out["seconds"], L.shape[1] * (y1 - y0) * d_max
+
+
+def split_rows(H: int, k: int):
+    k = max(1, min(k, H))
+    base, extra = divmod(H, k)
+    y = 0
+    for i in range(k):
+        h = base + (1 if i < extra else 0)
+        yield y, y + h
+        y += h
 
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, rank 0 only."""
-    rank = env_int("RANK", 0)
-    if rank != 0:
+    if env_int("RANK", 0) != 0:
         return 0
     import oracle
     from paper_1402_2020_b200.synth import WORKLOADS
     w = WORKLOADS[args.workload]
-    threads = os.cpu_count() or 1
-    pairs_arr = oracle.Reference().generate_pattern(4096, 26, 4.0, 42)
-    rows = args.ref_rows
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
-        cpu_reference_sample(args.workload, max(8, rows // 4), threads, pairs_arr)
-    secs, evals = 0.0, 0
-    for _ in range(args.steps):
-        s, e, lib = cpu_reference_sample(args.workload, rows, threads, pairs_arr)
-        secs += s
-        evals += e
-    v = evals / secs / 1e6
+    info = cpu_info()
+    threads = info["nproc"]
+    ref = oracle.Reference()
+    pairs_arr = ref.generate_pattern(4096, 26, 4.0, 42)
+    left, right = ref_inputs(ref, args.workload, 0)
+    H = left.shape[0]
+    if args.warmup > 0:  # page in the library and the thread pool on a small band
+        ref_band(ref, pairs_arr, left, right, 0, min(8, H), w.d_max, threads)
+    steps = max(1, args.steps)
+    bands = list(split_rows(H, steps))
+    secs, evals, tput = [], [], []
+    for i in range(steps):
+        y0, y1 = bands[i % len(bands)]
+        s, e = ref_band(ref, pairs_arr, left, right, y0, y1, w.d_max, threads)
+        secs.append(s)
+        evals.append(e)
+        tput.append(e / s / 1e6)
+    value = statistics.median(tput)
+    frame = sum(evals) / sum(secs) / 1e6
+    covered = sum(b[1] - b[0] for b in bands[:steps])
+    sample = (f"pair 0 of {w.name} ({w.width}x{H}, D={w.d_max}) split into {len(bands)} row bands, one band per "
+              f"step run through run_pipeline as its own image ({covered} of {H} rows covered); "
+              f"{os.path.basename(ref.path)}, {threads} threads")
     line = {
-        "impl": "reference", "metric": "Mdisp-evals/s", "value": v, "unit": "Mdisp-evals/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 popcount / f64 votes",
+        "impl": "reference", "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
+        "scaling": "strong" if (w.pairs > 1 or args.workload == "c5") else "weak", "vs_baseline": None,
+        "dtype": "u32 popcount / f64 votes",
         "data": ("synthetic colour views (synth.colour_pair)" if args.workload.endswith("rgb")
                  else "synthetic (BASELINE.json generator, SURVEY.md 8(d))"),
         "config": {"workload": w.name, "width": w.width, "height": w.height, "d_max": w.d_max, "n": 4096,
-                   "sample": f"{rows}-row band per step"},
-        "cpu_baseline": {"value": v, "unit": "Mdisp-evals/s", "cores": threads, "kind": "reference",
-                         "sample": f"{rows} rows x {w.width} x D={w.d_max} per step, {lib}"},
-        "e2e": {"value": v, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "pairs": w.pairs, "sample": "row bands of pair 0 tiling the frame, one per step",
+                   "same_config": True},
+        "cpu_baseline": {"value": value, "unit": "Mdisp-evals/s", "cores": threads, "kind": "reference",
+                         "sample": sample, "whole_frame_value": frame, "cpu": info,
+                         "statistic": "median over steps (eval.hpp:144-159 time_pipeline)"},
+        "e2e": {"value": value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def cpu_baseline_leg(args, w, pairs_arr):
+    """Bounded sample for the GPU arm's line (rank 0, N = 1): median of
+    `--ref-repeats` runs of a `--ref-rows` band of pair 0 on all host threads,
+    plus one run on one thread (the paper's protocol)."""
+    import oracle
+    info = cpu_info()
+    threads = info["nproc"]
+    ref = oracle.Reference()
+    left, right = ref_inputs(ref, args.workload, 0)
+    H = left.shape[0]
+    rows = min(args.ref_rows, H)
+    y0 = (H - rows) // 2
+    ref_band(ref, pairs_arr, left, right, y0, y0 + min(8, rows), w.d_max, threads)  # warm-up
+    tp = []
+    for _ in range(max(1, args.ref_repeats)):
+        s, e = ref_band(ref, pairs_arr, left, right, y0, y0 + rows, w.d_max, threads)
+        tp.append(e / s / 1e6)
+    r1 = max(2, rows // 16)
+    s1, e1 = ref_band(ref, pairs_arr, left, right, y0, y0 + r1, w.d_max, 1)
+    return {"value": statistics.median(tp), "unit": "Mdisp-evals/s", "cores": threads, "kind": "reference",
+            "sample": f"median of {len(tp)} runs of rows [{y0}, {y0 + rows}) x {w.width} x D={w.d_max} of pair 0, "
+                      f"{os.path.basename(ref.path)}",
+            "cpu": info, "single_thread": {"value": e1 / s1 / 1e6, "cores": 1,
+                                           "sample": f"{r1} rows x {w.width} x D={w.d_max}"}}
+
+
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c2rgb"])
-    ap.add_argument("--ref-rows", type=int, default=48)
+    ap.add_argument("--workload", default="c4", choices=WORKLOADS_CLI)
+    ap.add_argument("--pairs", type=int, default=0, help="batch size override (c4; default: the config's 64)")
+    ap.add_argument("--ref-rows", type=int, default=96)
+    ap.add_argument("--ref-repeats", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-only", action="store_true", help="few steps, no CPU leg (for ncu)")
+    ap.add_argument("--profile-only", action="store_true", help="value loop only (for ncu)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
-    import paper_1402_2020_b200 as bsm
-    from paper_1402_2020_b200.synth import WORKLOADS, workload_pair
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- cold start: context + pattern + first pipeline (tables built lazily) ----
+    t_cold = time.perf_counter()
+    import paper_1402_2020_b200 as bsm
+    from paper_1402_2020_b200._lib import bsm_maps, bsm_params, check, lib
+    from paper_1402_2020_b200.dist import band_rows, shard_units
+    from paper_1402_2020_b200.synth import WORKLOADS, workload_pair
+    t_import = time.perf_counter()
+    ctx = bsm.Context(local)
+    t_ctx = time.perf_counter()
     w = WORKLOADS[args.workload]
     W, H, D = w.width, w.height, w.d_max
-
-    ctx = bsm.Context(local)
     cfg = bsm.BsmConfig(d_max=D)
     pattern = bsm.generate_pattern(cfg=cfg)
     ctx.set_pattern(pattern)
-    # Partition (SURVEY.md 8(e)): configs[4] (c5, one frame) -> contiguous row
-    # bands with a vote-radius halo + one NCCL all-gather of the refined bands
-    # (strong scaling); every other workload -> rank r matches pair index r of
-    # the workload's seed sequence (independent units, weak scaling).
-    bands = args.workload == "c5" and world > 1
-    colour = args.workload.endswith("rgb")  # interleaved RGB views (colour path)
-    left, right = workload_pair(args.workload, index=0 if bands else rank)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    d_left = torch.from_numpy(left).to(dev)
-    d_right = torch.from_numpy(right).to(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    torch.cuda.synchronize()
-
-    from paper_1402_2020_b200._lib import check, lib, bsm_params
-    import ctypes as C
+    t_pat = time.perf_counter()
     p = bsm_params(D, cfg.lambda_c, cfg.lambda_e, cfg.lr_tolerance, cfg.vote_radius)
 
+    colour = args.workload.endswith("rgb")
+    bands = args.workload == "c5" and world > 1
+    n_total = (args.pairs or w.pairs) if w.pairs > 1 else 1
+    batch = w.pairs > 1
+    mine = list(shard_units(n_total, world, rank)) if batch else [0]
+    views = [workload_pair(args.workload, index=i) for i in mine]
+    px_view = W * H * (3 if colour else 1)
+    d_l = [torch.from_numpy(l).to(dev) for l, _ in views]
+    d_r = [torch.from_numpy(r).to(dev) for _, r in views]
+    d_od = [torch.empty((H, W), dtype=torch.float32, device=dev) for _ in views]
+    d_ov = [torch.empty((H, W), dtype=torch.uint8, device=dev) for _ in views]
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    vp = lambda ts: (C.c_void_p * max(1, len(ts)))(*[t.data_ptr() for t in ts])
+    dl_arr, dr_arr, od_arr, ov_arr = vp(d_l), vp(d_r), vp(d_od), vp(d_ov)
+
+    # first pipeline call (cold): the refine weight table and the other lazily
+    # built device tables are created here
+    t0 = time.perf_counter()
+    fn_dev = lib().bsm_pipeline_rgb_device if colour else lib().bsm_pipeline_u8_device
+    check(fn_dev(ctx.handle, C.c_void_p(d_l[0].data_ptr()), C.c_void_p(d_r[0].data_ptr()), W, H, C.byref(p), 0))
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    check(fn_dev(ctx.handle, C.c_void_p(d_l[0].data_ptr()), C.c_void_p(d_r[0].data_ptr()), W, H, C.byref(p), 0))
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    cold = {"import_ms": (t_import - t_cold) * 1e3, "ctx_create_ms": (t_ctx - t_import) * 1e3,
+            "set_pattern_ms": (t_pat - t_ctx) * 1e3, "first_pipeline_ms": (t1 - t0) * 1e3,
+            "warm_pipeline_ms": (t2 - t1) * 1e3,
+            "total_to_first_result_ms": (t1 - t_cold) * 1e3 - (t0 - t_pat) * 1e3}
+
     if bands:
-        from paper_1402_2020_b200.dist import band_rows
         y0, y1 = band_rows(H, world, rank)
         rows_max = -(-H // world)
         band_d = torch.zeros((rows_max, W), dtype=torch.float32, device=dev)
@@ -241,16 +354,16 @@ def main():
         all_v = [torch.empty_like(band_v) for _ in range(world)]
 
     def step_device():
-        if colour:
-            check(lib().bsm_pipeline_rgb_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
-                                                C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
+        if batch:
+            check(lib().bsm_pipeline_batch_u8_device(ctx.handle, len(mine), dl_arr, dr_arr, W, H, C.byref(p),
+                                                     od_arr, ov_arr))
             return
         if not bands:
-            check(lib().bsm_pipeline_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
-                                               C.c_void_p(d_right.data_ptr()), W, H, C.byref(p), 0))
+            check(fn_dev(ctx.handle, C.c_void_p(d_l[0].data_ptr()), C.c_void_p(d_r[0].data_ptr()), W, H,
+                         C.byref(p), 0))
             return
-        check(lib().bsm_pipeline_band_u8_device(ctx.handle, C.c_void_p(d_left.data_ptr()),
-                                                C.c_void_p(d_right.data_ptr()), W, H, y0, y1, C.byref(p)))
+        check(lib().bsm_pipeline_band_u8_device(ctx.handle, C.c_void_p(d_l[0].data_ptr()),
+                                                C.c_void_p(d_r[0].data_ptr()), W, H, y0, y1, C.byref(p)))
         check(lib().bsm_copy_result_device(ctx.handle, C.c_void_p(band_d.data_ptr()), C.c_void_p(band_v.data_ptr())))
         with torch.cuda.stream(stream):  # stream-ordered after the band kernels
             dist.all_gather(all_d, band_d)
@@ -261,13 +374,14 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # ---- warm-up (also builds the refine weight table once) ----
+    # ---- warm-up ----
     for _ in range(max(args.warmup, 1)):
         step_device()
     barrier()
 
     # ---- timed region: device-resident value ----
     evs = []
+    launches = 0
     with ClockSampler(local) as clocks:
         barrier()
         for _ in range(args.steps):
@@ -277,39 +391,72 @@ def main():
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 step_device()
+                launches += ctx.last_launch_count()
                 e1.record(stream)
             evs.append((e0, e1))
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
-    launches = ctx.last_launch_count()
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    units = W * H * D * (1 if bands else world) * args.steps
-    value = units / (total_ms * 1e-3) / 1e6
+    if batch:
+        units_step = W * H * D * n_total
+    elif bands:
+        units_step = W * H * D
+    else:
+        units_step = W * H * D * world
+    value = units_step * args.steps / (total_ms * 1e-3) / 1e6
+
+    line = {
+        "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong" if (batch or bands) else "weak", "vs_baseline": None,
+        "dtype": "u32 popcount / f64 votes",
+        "data": ("synthetic colour views (synth.colour_pair: configs[0] scene, three tone curves + noise)" if colour
+                 else "synthetic (BASELINE.json generator, SURVEY.md 8(d))"),
+        "config": {"workload": w.name, "width": W, "height": H, "d_max": D, "n": 4096,
+                   "pairs_per_step": n_total if batch else (1 if bands else world),
+                   "pairs_per_rank": len(mine) if batch else 1,
+                   "parallelism": (f"pairs sharded {n_total}/{world} per rank (no data-path collective)" if batch
+                                   else (f"row bands x{world} + NCCL all-gather" if bands
+                                         else (f"replicas x{world}" if world > 1 else "1 pair"))),
+                   "l2": "256 MiB flush before every step (outside events); per-pair working set 2-9 GB >> L2"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if args.profile_only:
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
 
     # ---- e2e through the public C ABI with pinned host buffers ----
-    h_left = torch.from_numpy(left).pin_memory()
-    h_right = torch.from_numpy(right).pin_memory()
-    h_rd = torch.empty((H, W), dtype=torch.float32).pin_memory()
-    h_rv = torch.empty((H, W), dtype=torch.uint8).pin_memory()
-    maps = bsm._lib.bsm_maps(h_rd.data_ptr(), h_rv.data_ptr(), None, None, None, None, None)
-
+    h_l = [torch.from_numpy(l).pin_memory() for l, _ in views]
+    h_r = [torch.from_numpy(r).pin_memory() for _, r in views]
+    h_d = [torch.empty((H, W), dtype=torch.float32).pin_memory() for _ in views]
+    h_v = [torch.empty((H, W), dtype=torch.uint8).pin_memory() for _ in views]
+    hl_arr, hr_arr, hd_arr, hv_arr = vp(h_l), vp(h_r), vp(h_d), vp(h_v)
     if bands:
         h_all_d = torch.empty((world * rows_max, W), dtype=torch.float32).pin_memory()
         h_all_v = torch.empty((world * rows_max, W), dtype=torch.uint8).pin_memory()
+    maps = bsm_maps(h_d[0].data_ptr(), h_v[0].data_ptr(), None, None, None, None, None)
 
     def step_e2e():
+        if batch:
+            check(lib().bsm_pipeline_batch_u8(ctx.handle, len(mine), hl_arr, hr_arr, W, H, C.byref(p), hd_arr,
+                                              hv_arr))
+            return
         if not bands:
             fn = lib().bsm_pipeline_rgb if colour else lib().bsm_pipeline_u8
-            check(fn(ctx.handle, C.c_void_p(h_left.data_ptr()), C.c_void_p(h_right.data_ptr()),
-                     W, H, C.byref(p), 0, C.byref(maps)))
+            check(fn(ctx.handle, C.c_void_p(h_l[0].data_ptr()), C.c_void_p(h_r[0].data_ptr()), W, H, C.byref(p), 0,
+                     C.byref(maps)))
             return
         with torch.cuda.stream(stream):
-            d_left.copy_(h_left, non_blocking=True)
-            d_right.copy_(h_right, non_blocking=True)
+            d_l[0].copy_(h_l[0], non_blocking=True)
+            d_r[0].copy_(h_r[0], non_blocking=True)
         step_device()
         with torch.cuda.stream(stream):
             h_all_d.copy_(torch.cat(all_d), non_blocking=True)
@@ -318,94 +465,103 @@ def main():
 
     step_e2e()
     barrier()
-    e2e_ms = []
+    e2e_ms, e2e_wall = [], []
     for _ in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        tw = time.perf_counter()
         step_e2e()
         e1.record(stream)
         e1.synchronize()
+        e2e_wall.append((time.perf_counter() - tw) * 1e3)
         e2e_ms.append(e0.elapsed_time(e1))
     barrier()
     te = torch.tensor([float(sum(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = units / (float(te.item()) * 1e-3) / 1e6
+    e2e_value = units_step * args.steps / (float(te.item()) * 1e-3) / 1e6
+    if batch:
+        h2d, d2h = 2 * px_view * len(mine), 5 * W * H * len(mine)
+    elif bands:
+        h2d, d2h = 2 * px_view, 5 * world * rows_max * W
+    else:
+        h2d, d2h = 2 * px_view, 5 * W * H
+    line["e2e"] = {"value": e2e_value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": float(te.item()) / args.steps,
+                   "host_wall_ms_per_step": float(np.mean(e2e_wall)),
+                   "call": ("bsm_pipeline_batch_u8" if batch else ("bsm_pipeline_band_u8_device + NCCL all-gather"
+                                                                   if bands else
+                                                                   ("bsm_pipeline_rgb" if colour else
+                                                                    "bsm_pipeline_u8")))}
 
-    # ---- per-kernel device time (events on the library's stream) ----
+    # ---- per-stage device time of one pair (events on the library's stream) ----
     ctx.set_profiling(True)
     prof = {}
-    nprof = max(3, min(args.steps, 10))
-    for _ in range(nprof):
+    for _ in range(max(3, min(args.steps, 8))):
         flush.fill_(1)
         torch.cuda.synchronize()
-        step_device()
+        if bands:
+            check(lib().bsm_pipeline_band_u8_device(ctx.handle, C.c_void_p(d_l[0].data_ptr()),
+                                                    C.c_void_p(d_r[0].data_ptr()), W, H, y0, y1, C.byref(p)))
+        else:
+            check(fn_dev(ctx.handle, C.c_void_p(d_l[0].data_ptr()), C.c_void_p(d_r[0].data_ptr()), W, H,
+                         C.byref(p), 0))
         for k, v in ctx.last_timings().items():
             prof.setdefault(k, []).append(v)
     ctx.set_profiling(False)
     prof_ms = {k: float(np.mean(v)) for k, v in prof.items() if np.mean(v) > 0}
-    popc_peak, csa_peak = ctx.measure_word_peaks()  # word-ops/s, this GPU, live
+    popc_peak, csa_peak = ctx.measure_word_peaks()  # live microbenchmarks, word-ops/s
 
-    if bands:  # fields / WTA / check cover the band plus the vote-radius halo
-        hr = min(H, y1 + cfg.vote_radius) - max(0, y0 - cfg.vote_radius)
-        evals_dir = in_bounds_evals(W, hr, D)
-    else:
-        evals_dir = in_bounds_evals(W, H, D)
-    wta_ms = (prof_ms.get("wta_left", 0) + prof_ms.get("wta_right", 0)) / 2
-    achieved = evals_dir * (4096 // 32) / (wta_ms * 1e-3)  # u32 masked-xor-popcount word-ops / s
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
     peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
+    clk = line["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    pipe_peak = WORDOPS_PER_CLK_SM * sms * clk * 1e6  # nominal word-ops/s
+    rows_c = (min(H, y1 + cfg.vote_radius) - max(0, y0 - cfg.vote_radius)) if bands else H
+    evals_dir = in_bounds_evals(W, rows_c, D)
+    wta_ms = prof_ms.get("wta", 0.0) + prof_ms.get("wta_left", 0.0) + prof_ms.get("wta_right", 0.0)
+    achieved = 2 * evals_dir * (4096 // 32) / (wta_ms * 1e-3)  # both directions per launch set
     hbm_peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-    alg_bytes = W * (hr if bands else H) * (3 * 4096 // 8 + 4)  # ref desc + ref mask + other desc, + key
+    alg_bytes = 2 * W * rows_c * (3 * 4096 // 8 + 4)  # per direction: ref desc + ref mask + other desc, + key
     hbm_ach = alg_bytes / (wta_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.workload)
-
-    line = {
-        "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if bands else "weak", "vs_baseline": None,
-        "dtype": "u32 popcount / f64 votes",
-        "data": ("synthetic colour views (synth.colour_pair: configs[0] scene, three tone curves + noise)" if colour
-                 else "synthetic (BASELINE.json generator, SURVEY.md 8(d))"),
-        "config": {"workload": w.name, "width": W, "height": H, "d_max": D, "n": 4096,
-                   "pairs_per_step": 1 if bands else world,
-                   "parallelism": (f"row bands x{world} + NCCL all-gather" if bands
-                                   else (f"pairs x{world}" if world > 1 else "1 pair")),
-                   "l2": "256 MiB flush before every step (outside events); working set 3.2 GB >> L2"},
-        "e2e": {"value": e2e_value, "unit": "Mdisp-evals/s", "h2d_bytes_per_step": 2 * W * H * (3 if colour else 1),
-                "d2h_bytes_per_step": 5 * (world * rows_max if bands else H) * W,
-                "ms_per_step": float(te.item()) / args.steps},
-        "gpu_launches": launches * args.steps,
-        "roofline": {"bound": "int-pipes (LOP3+POPC)",
-                     "kernel": "k_cost_wta (fused masked Hamming + WTA, per direction)",
-                     "achieved": achieved / 1e9, "peak": csa_peak / 1e9, "unit": "Gword-ops/s",
-                     "frac": achieved / csa_peak, "traffic": traffic,
-                     "peak_source": "live register-only microbenchmark of the kernel's carry-save instruction mix "
-                                    "(2 words per 4 LOP3 + POPC + IMAD: ALU and POPC pipes balanced) on this GPU",
-                     "popc_only_peak": popc_peak / 1e9, "frac_of_popc_only": achieved / popc_peak,
-                     "kernel_ms": wta_ms, "alg_word_ops_per_launch": evals_dir * 128,
-                     "hbm_achieved_gbs": hbm_ach, "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_ach / hbm_peak},
-        "stage_ms": prof_ms,
-        "clocks": clocks.summary(),
+    line["roofline"] = {
+        "bound": "int-pipes (ALU LOP3 + XU POPC)", "kernel": "k_cost_wta (fused masked Hamming + WTA, both "
+                                                               "directions)",
+        "achieved": achieved / 1e9, "peak": pipe_peak / 1e9, "unit": "Gword-ops/s", "frac": achieved / pipe_peak,
+        "traffic": traffic,
+        "peak_source": f"nominal: {WORDOPS_PER_CLK_SM} word-ops/clk/SM (64 LOP3/clk/SM at 2 per word-op = 16 "
+                       f"POPC/clk/SM at 0.5 per word-op) x {sms} SMs x {clk:.0f} MHz",
+        "achievable_peak": csa_peak / 1e9, "frac_of_achievable": achieved / csa_peak,
+        "achievable_source": "live register-only microbenchmark of the kernel's carry-save instruction mix",
+        "popc_only_peak": popc_peak / 1e9,
+        "kernel_ms": wta_ms, "alg_word_ops": 2 * evals_dir * 128,
+        "unit_def": "word-op = one u32 (a^b)&m + popcount; 128 per in-bounds (x, y, d, direction)",
+        "hbm_achieved_gbs": hbm_ach, "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_ach / hbm_peak,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
+    mask_ms = prof_ms.get("mask", 0.0)
+    if mask_ms > 0 and not colour:
+        # K2: 2 rank gathers per pair and pixel, u16x2-packed for two pixels:
+        # n / 32 conflict-free wavefronts per pixel; the LSU serves 1 per clk per SM
+        wf = 2 * W * rows_c * (4096 // 32)  # both views
+        wf_peak = sms * clk * 1e6
+        line["roofline_mask"] = {"bound": "lsu (shared-memory gather wavefronts)", "kernel": "k_mask4 (both views)",
+                                 "achieved": wf / (mask_ms * 1e-3) / 1e9, "peak": wf_peak / 1e9,
+                                 "unit": "Gwavefronts/s", "frac": wf / (mask_ms * 1e-3) / wf_peak,
+                                 "kernel_ms": mask_ms,
+                                 "unit_def": "n/32 = 128 rank-gather wavefronts per pixel (2 per pair, two pixels "
+                                             "per u32)"}
+    line["stage_ms"] = prof_ms
+    line["cold_start"] = cold
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            pairs_arr = pattern.pairs
-            threads = os.cpu_count() or 1
-            s, e, libname = cpu_reference_sample(args.workload, args.ref_rows, threads, pairs_arr)
-            line["cpu_baseline"] = {"value": e / s / 1e6, "unit": "Mdisp-evals/s", "cores": threads,
-                                    "kind": "reference",
-                                    "sample": f"{args.ref_rows} rows x {W} x D={D} of the same pair, {libname}"}
-            # the paper's protocol is one thread: a smaller band
-            r1 = max(4, args.ref_rows // 8)
-            s1, e1, _ = cpu_reference_sample(args.workload, r1, 1, pairs_arr)
-            line["cpu_baseline"]["single_thread"] = {"value": e1 / s1 / 1e6, "cores": 1,
-                                                     "sample": f"{r1} rows x {W} x D={D}"}
+            line["cpu_baseline"] = cpu_baseline_leg(args, w, pattern.pairs)
         except Exception as ex:  # the checker is optional on a box without it
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:

@@ -129,8 +129,26 @@ int bsm_rgb24_tables(float* gray16M, float* lab48M);
 int bsm_pipeline_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int W, int H,
                     const bsm_params* params, int want_unmasked, bsm_maps* out);
 
+/* run_pipeline(...).refined (pipeline.hpp:25-56) of a batch of grayscale pairs
+ * (BASELINE configs[3]), host buffers: lefts[i] / rights[i] are W x H views,
+ * refined_d[i] / refined_v[i] receive pair i's refined map (either array, or
+ * any entry, may be NULL).  Uploads, compute and downloads of consecutive pairs
+ * overlap (two device slots, separate copy streams); returns when every map
+ * has landed.  Pinned host buffers make the copies asynchronous. */
+int bsm_pipeline_batch_u8(bsm_ctx* ctx, int n_pairs, const uint8_t* const* lefts, const uint8_t* const* rights,
+                          int W, int H, const bsm_params* params, float* const* refined_d,
+                          uint8_t* const* refined_v);
+/* Device-resident batch: d_lefts / d_rights / d_refined_* are host arrays of
+ * DEVICE pointers; work is queued on bsm_stream() and not synchronised. */
+int bsm_pipeline_batch_u8_device(bsm_ctx* ctx, int n_pairs, const uint8_t* const* d_lefts,
+                                 const uint8_t* const* d_rights, int W, int H, const bsm_params* params,
+                                 float* const* d_refined_d, uint8_t* const* d_refined_v);
+
 /* Device-resident variant: left/right are device pointers; results stay on the
- * device in context-owned buffers (read them with bsm_fetch_maps). */
+ * device in context-owned buffers (read them with bsm_fetch_maps).
+ * Device inputs must be complete when the context's stream reaches the call:
+ * produce them on bsm_stream(), synchronise, or call bsm_stream_wait() with
+ * the producing stream first.  Device pointers must be 4-byte aligned. */
 int bsm_pipeline_u8_device(bsm_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int W, int H,
                            const bsm_params* params, int want_unmasked);
 int bsm_fetch_maps(bsm_ctx* ctx, bsm_maps* out);
@@ -152,10 +170,38 @@ int bsm_result_device(bsm_ctx* ctx, const float** refined_d, const uint8_t** ref
 /* Stream-ordered device-to-device copy of those rows into caller buffers. */
 int bsm_copy_result_device(bsm_ctx* ctx, float* dst_d, uint8_t* dst_v);
 
+/* Multi-GPU partitions over NCCL; one process (and one
+ * context) per GPU.  Rank 0 makes an id with bsm_comm_unique_id and hands the
+ * 128 bytes to the other ranks out of band (MPI, a file, torch.distributed);
+ * every rank then calls bsm_comm_create with its rank.  NCCL is loaded at run
+ * time (libnccl.so.2); NCCL failures return BSM_NCCL_ERROR. */
+typedef struct bsm_comm bsm_comm;
+int bsm_comm_unique_id(uint8_t* id128);
+int bsm_comm_create(bsm_ctx* ctx, const uint8_t* id128, int world, int rank, bsm_comm** out);
+int bsm_comm_destroy(bsm_comm* comm);
+/* One frame (BASELINE configs[4]) partitioned into contiguous row bands:
+ * every rank passes the full views, computes its band with a local
+ * vote-radius halo (no exchange) and receives the whole refined map through
+ * one NCCL all-gather of the bands; bit-identical to run_pipeline(...).refined
+ * for every world size (parallel.hpp:12-14). */
+int bsm_pipeline_frame_bands_u8(bsm_ctx* ctx, bsm_comm* comm, const uint8_t* left, const uint8_t* right, int W,
+                                int H, const bsm_params* params, float* refined_d, uint8_t* refined_v);
+/* A batch of pairs (BASELINE configs[3]) sharded by pair: rank r computes the
+ * contiguous shard [r*n/world ...) (sizes differ by at most one; only that
+ * shard's lefts[i] / rights[i] are read) and the refined maps of ALL pairs
+ * land in refined_d[i] / refined_v[i] on rank `root` (ncclSend / ncclRecv;
+ * other ranks' output arrays may be NULL). */
+int bsm_pipeline_pairs_sharded_u8(bsm_ctx* ctx, bsm_comm* comm, int n_pairs, const uint8_t* const* lefts,
+                                  const uint8_t* const* rights, int W, int H, const bsm_params* params, int root,
+                                  float* const* refined_d, uint8_t* const* refined_v);
+
 /* Instrumentation.  bsm_stream returns the cudaStream_t the context launches
  * on.  When profiling is enabled, bsm_last_timings reports the device time (ms)
  * of the last pipeline's kernels, in the order of bsm_timing_names. */
 int bsm_stream(bsm_ctx* ctx, void** stream);
+/* Order the context's stream after all work queued so far on `stream` (a
+ * cudaStream_t of the caller, NULL = the legacy default stream). */
+int bsm_stream_wait(bsm_ctx* ctx, void* stream);
 int bsm_set_profiling(bsm_ctx* ctx, int enable);
 int bsm_last_timings(bsm_ctx* ctx, float* ms, int max, int* count);
 const char* bsm_timing_names(void);

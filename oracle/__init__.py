@@ -264,6 +264,17 @@ class Reference(_Lib):
         lp = np.ascontiguousarray(lp, np.float32)
         return self.f("vote_weight", [_P, _P, _I, _I, _D, _D], C.c_double)(_p(lx), _p(lp), dx, dy, lc, le)
 
+    def synth_pair(self, config, seed, width, height):
+        """(left, right) uint8 views of a BASELINE synthetic pair (the generator
+        compiled into this library, so callers load no product library)."""
+        left = np.empty((height, width), np.uint8)
+        right = np.empty((height, width), np.uint8)
+        rc = self.f("synth_pair", [_I, C.c_uint64, _I, _I, _P, _P, _P])(
+            int(config), int(seed), int(width), int(height), _p(left), _p(right), None)
+        if rc:
+            raise ValueError("synth_pair: bad arguments")
+        return left, right
+
     def pipeline(self, left, right, pairs, window, d_max, lc=9.0, le=16.0, tol=1.0, radius=20, threads=1,
                  want_unmasked=False, channels=1):
         left = np.ascontiguousarray(left, np.uint8)

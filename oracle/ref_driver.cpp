@@ -260,3 +260,11 @@ int ref_pipeline(const uint8_t* left, const uint8_t* right, int channels, int W,
 }
 
 }  // extern "C"
+
+// The BASELINE synthetic pair generator (paper_1402_2020_b200/csrc/synth.cpp,
+// input generation only) compiled into this test library as ref_synth_pair, so
+// that the reference arm of bench.py builds its inputs without loading any
+// product library.
+#define bsm_synth_pair ref_synth_pair
+#include "../paper_1402_2020_b200/csrc/synth.cpp"
+#undef bsm_synth_pair

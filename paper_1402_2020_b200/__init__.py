@@ -34,7 +34,7 @@ from ._lib import (
 __all__ = [
     "BsmConfig", "SamplingPattern", "DisparityMap", "PipelineResult", "Context",
     "generate_pattern", "gray_lab_lut", "to_gray_lab", "compute_field", "wta", "lr_check",
-    "vote_refine", "run_pipeline", "run_pipeline_band", "default_context",
+    "vote_refine", "run_pipeline", "run_pipeline_band", "run_pipeline_batch", "default_context",
     "BsmError", "InvalidArgument", "DimensionMismatch", "CudaError", "Unsupported",
     "GENERATOR_NAME",
 ]
@@ -140,6 +140,8 @@ class Context:
         self._pattern_key = None
 
     def close(self) -> None:
+        for comm in list(self.__dict__.get("_comms", {}).values()):  # NCCL communicators first
+            comm.close()
         if getattr(self, "_h", None):
             lib().bsm_ctx_destroy(self._h)
             self._h = None
@@ -473,3 +475,33 @@ def run_pipeline_band(left, right, cfg: BsmConfig, y0: int, y1: int,
     check(lib().bsm_pipeline_band_u8(ctx.handle, _ptr(L), _ptr(R), W, H, int(y0), int(y1), C.byref(p),
                                      _ptr(rd), _ptr(rv)))
     return DisparityMap(rd, rv)
+
+
+def _ptr_array(arrays):
+    return (C.c_void_p * max(len(arrays), 1))(*[a.ctypes.data for a in arrays])
+
+
+def run_pipeline_batch(pairs, cfg: BsmConfig, pattern: Optional[SamplingPattern] = None,
+                       ctx: Optional[Context] = None) -> list:
+    """run_pipeline(...).refined of every (left, right) grayscale pair of a batch
+    (BASELINE configs[3]; pipeline.hpp:25-56 per pair).  One C-ABI call
+    (bsm_pipeline_batch_u8) overlaps each pair's upload and download with its
+    neighbours' compute.  All pairs share one shape."""
+    views = [(_u8(l, "left"), _u8(r, "right")) for l, r in pairs]
+    if not views:
+        return []
+    H, W = views[0][0].shape
+    for L, R in views:
+        if L.shape != R.shape or L.shape != (H, W):
+            raise DimensionMismatch("pipeline: left/right dimensions differ")
+    cfg.validate()
+    if pattern is None:
+        pattern = generate_pattern(cfg=cfg)
+    ctx = ctx or default_context()
+    ctx.set_pattern(pattern)
+    outs = [(np.empty((H, W), np.float32), np.empty((H, W), np.uint8)) for _ in views]
+    p = _params(cfg)
+    check(lib().bsm_pipeline_batch_u8(ctx.handle, len(views), _ptr_array([v[0] for v in views]),
+                                      _ptr_array([v[1] for v in views]), W, H, C.byref(p),
+                                      _ptr_array([o[0] for o in outs]), _ptr_array([o[1] for o in outs])))
+    return [DisparityMap(d, v) for d, v in outs]

@@ -102,7 +102,15 @@ _SIGS = {
     "bsm_pipeline_band_u8_device": [_P, _P, _P, _I, _I, _I, _I, C.POINTER(bsm_params)],
     "bsm_result_device": [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "bsm_copy_result_device": [_P, _P, _P],
+    "bsm_pipeline_batch_u8": [_P, _I, _P, _P, _I, _I, C.POINTER(bsm_params), _P, _P],
+    "bsm_pipeline_batch_u8_device": [_P, _I, _P, _P, _I, _I, C.POINTER(bsm_params), _P, _P],
+    "bsm_comm_unique_id": [_P],
+    "bsm_comm_create": [_P, _P, _I, _I, C.POINTER(C.c_void_p)],
+    "bsm_comm_destroy": [_P],
+    "bsm_pipeline_frame_bands_u8": [_P, _P, _P, _P, _I, _I, C.POINTER(bsm_params), _P, _P],
+    "bsm_pipeline_pairs_sharded_u8": [_P, _P, _I, _P, _P, _I, _I, C.POINTER(bsm_params), _I, _P, _P],
     "bsm_stream": [_P, C.POINTER(C.c_void_p)],
+    "bsm_stream_wait": [_P, _P],
     "bsm_set_profiling": [_P, _I],
     "bsm_last_timings": [_P, _P, _I, C.POINTER(C.c_int)],
     "bsm_last_launch_count": [_P, C.POINTER(C.c_int)],

@@ -19,7 +19,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/bsm_cuda.h"
@@ -130,6 +132,11 @@ struct bsm_ctx {
     int ev_used[T_COUNT] = {};
     int launches = 0;
     DevBuf popc_out;
+    // batch pipelining (bsm_pipeline_batch_u8): two slots of input views and
+    // refined maps, an H2D and a D2H copy stream ordered by events
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    DevBuf bimg[2][2], bout_d[2], bout_v[2];
+    cudaEvent_t ev_in[2] = {}, ev_free[2] = {}, ev_done[2] = {}, ev_out[2] = {};
 };
 
 namespace {
@@ -621,6 +628,33 @@ int sync(bsm_ctx* c) {
     return BSM_OK;
 }
 
+// Copy streams, events and the two slots of views / refined maps used to
+// overlap pair i's compute with pair i+1's upload and pair i-1's download.
+int ensure_batch(bsm_ctx* c, size_t px) {
+    if (!c->s_h2d) {
+        BSM_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        BSM_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+        for (int s = 0; s < 2; ++s)
+            for (cudaEvent_t* e : {&c->ev_in[s], &c->ev_free[s], &c->ev_done[s], &c->ev_out[s]})
+                BSM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    for (int s = 0; s < 2; ++s) {
+        BSM_TRY(c->bimg[s][0].ensure(px));
+        BSM_TRY(c->bimg[s][1].ensure(px));
+        BSM_TRY(c->bout_d[s].ensure(px * 4));
+        BSM_TRY(c->bout_v[s].ensure(px));
+    }
+    return BSM_OK;
+}
+
+int check_batch_ptrs(int n_pairs, const void* const* a, const void* const* b) {
+    if (n_pairs < 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: n_pairs must be >= 0");
+    if (n_pairs > 0 && (!a || !b)) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image array");
+    for (int i = 0; i < n_pairs; ++i)
+        if (!a[i] || !b[i]) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    return BSM_OK;
+}
+
 int check_dims(int W, int H) {
     if (W < 1 || H < 1) return set_err(BSM_INVALID_ARGUMENT, "bsm: image dimensions must be >= 1");
     if (int64_t(W) * H > (int64_t(1) << 31) - 1)
@@ -705,6 +739,16 @@ int bsm_ctx_destroy(bsm_ctx* c) {
                       &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
                       &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
     for (DevBuf* b : bufs) b->release();
+    for (int s = 0; s < 2; ++s) {
+        c->bimg[s][0].release();
+        c->bimg[s][1].release();
+        c->bout_d[s].release();
+        c->bout_v[s].release();
+        for (cudaEvent_t e : {c->ev_in[s], c->ev_free[s], c->ev_done[s], c->ev_out[s]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (int t = 0; t < T_COUNT; ++t)
         for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
             if (c->ev[t][s][0]) cudaEventDestroy(c->ev[t][s][0]);
@@ -1047,6 +1091,82 @@ int bsm_pipeline_band_u8(bsm_ctx* c, const uint8_t* left, const uint8_t* right, 
     return sync(c);
 }
 
+// run_pipeline(...).refined (pipeline.hpp:25-56) of every pair of a batch
+// (BASELINE configs[3]).  Pair i's views are uploaded on the H2D stream while
+// pair i-1 computes, and its refined map is downloaded on the D2H stream
+// while pair i+1 computes; two slots of device views / maps alternate.
+int bsm_pipeline_batch_u8(bsm_ctx* c, int n_pairs, const uint8_t* const* lefts, const uint8_t* const* rights, int W,
+                          int H, const bsm_params* params, float* const* refined_d, uint8_t* const* refined_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    BSM_TRY(check_batch_ptrs(n_pairs, reinterpret_cast<const void* const*>(lefts),
+                             reinterpret_cast<const void* const*>(rights)));
+    if (n_pairs == 0) return BSM_OK;
+    const size_t px = size_t(W) * H;
+    BSM_TRY(ensure_batch(c, px));
+    for (int i = 0; i < n_pairs; ++i) {
+        const int s = i & 1;
+        if (i >= 2) BSM_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_free[s], 0));  // slot views consumed
+        BSM_CUDA(cudaMemcpyAsync(c->bimg[s][0].p, lefts[i], px, cudaMemcpyHostToDevice, c->s_h2d));
+        BSM_CUDA(cudaMemcpyAsync(c->bimg[s][1].p, rights[i], px, cudaMemcpyHostToDevice, c->s_h2d));
+        BSM_CUDA(cudaEventRecord(c->ev_in[s], c->s_h2d));
+        BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
+        BSM_TRY(pipeline_device(c, u8views(c->bimg[s][0].as<uint8_t>(), c->bimg[s][1].as<uint8_t>()), W, H, 0, H,
+                                params, false));
+        BSM_CUDA(cudaEventRecord(c->ev_free[s], c->stream));
+        if (i >= 2) BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out[s], 0));  // slot map downloaded
+        BSM_CUDA(cudaMemcpyAsync(c->bout_d[s].p, c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
+        BSM_CUDA(cudaMemcpyAsync(c->bout_v[s].p, c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
+        BSM_CUDA(cudaEventRecord(c->ev_done[s], c->stream));
+        BSM_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_done[s], 0));
+        if (refined_d && refined_d[i])
+            BSM_CUDA(cudaMemcpyAsync(refined_d[i], c->bout_d[s].p, px * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+        if (refined_v && refined_v[i])
+            BSM_CUDA(cudaMemcpyAsync(refined_v[i], c->bout_v[s].p, px, cudaMemcpyDeviceToHost, c->s_d2h));
+        BSM_CUDA(cudaEventRecord(c->ev_out[s], c->s_d2h));
+    }
+    BSM_CUDA(cudaStreamSynchronize(c->s_d2h));
+    return sync(c);
+}
+
+// Device-resident batch: views and refined maps are device buffers (arrays of
+// device pointers held on the host); stream-ordered on bsm_stream(), no sync.
+int bsm_pipeline_batch_u8_device(bsm_ctx* c, int n_pairs, const uint8_t* const* d_lefts,
+                                 const uint8_t* const* d_rights, int W, int H, const bsm_params* params,
+                                 float* const* d_refined_d, uint8_t* const* d_refined_v) {
+    BSM_TRY(begin_call(c));
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(check_dims(W, H));
+    BSM_TRY(validate_params(params));
+    BSM_TRY(check_batch_ptrs(n_pairs, reinterpret_cast<const void* const*>(d_lefts),
+                             reinterpret_cast<const void* const*>(d_rights)));
+    const size_t px = size_t(W) * H;
+    for (int i = 0; i < n_pairs; ++i) {
+        BSM_TRY(pipeline_device(c, u8views(d_lefts[i], d_rights[i]), W, H, 0, H, params, false));
+        if (d_refined_d && d_refined_d[i])
+            BSM_CUDA(cudaMemcpyAsync(d_refined_d[i], c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
+        if (d_refined_v && d_refined_v[i])
+            BSM_CUDA(cudaMemcpyAsync(d_refined_v[i], c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return BSM_OK;
+}
+
+// Make the context's stream wait for all work queued so far on `stream` (a
+// cudaStream_t of the caller, e.g. the one that produced device inputs).
+int bsm_stream_wait(bsm_ctx* c, void* stream) {
+    if (!c) return set_err(BSM_INVALID_ARGUMENT, "bsm: null context");
+    BSM_CUDA(cudaSetDevice(c->device));
+    cudaEvent_t e;
+    BSM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaError_t r = cudaEventRecord(e, static_cast<cudaStream_t>(stream));
+    if (r == cudaSuccess) r = cudaStreamWaitEvent(c->stream, e, 0);
+    cudaEventDestroy(e);
+    if (r != cudaSuccess) return set_err(BSM_CUDA_ERROR, std::string("CUDA: stream wait: ") + cudaGetErrorString(r));
+    return BSM_OK;
+}
+
 int bsm_device_exp(bsm_ctx* c, const double* x, int n, double* out) {
     BSM_TRY(begin_call(c));
     if (!x || !out || n < 0) return set_err(BSM_INVALID_ARGUMENT, "bsm: bad arguments");
@@ -1322,3 +1442,5 @@ int bsm_measure_word_peaks(bsm_ctx* c, double* popc_words_per_s, double* csa_wor
 }
 
 }  // extern "C"
+
+#include "bsm_dist.cuh"

@@ -1,32 +1,41 @@
 """Multi-GPU partitions of the matching path (one process per GPU).
 
-Two partitions:
+Two partitions, both implemented in the C ABI over
+NCCL (include/bsm_cuda.h "Multi-GPU", csrc/bsm_dist.cuh); this module is the
+thin Python caller:
 
 * batch of pairs (BASELINE configs[3]): pairs are independent units, sharded
-  contiguously over ranks; no data-path collective; results are gathered to
-  one rank only at the end (``gather_pairs``).
-* one large frame (configs[4]): contiguous row bands.  Every rank holds both
-  full views and computes its band with a vote-radius halo of redundant rows
-  (``run_pipeline_band``), so the only exchange is the final all-gather of
-  the refined bands.  A band-local ``max_bin`` is safe: bins above it are 0
-  for every pixel of the band and cannot win the strict-'>' argmax
-  (refine.hpp:102-105).
+  contiguously over ranks (``shard_units``); no data-path collective; the
+  refined maps are gathered to one root rank at the end
+  (``bsm_pipeline_pairs_sharded_u8``: ncclSend / ncclRecv).
+* one large frame (configs[4]): contiguous row bands (``band_rows``).  Every
+  rank holds both full views and computes its band with a vote-radius halo of
+  redundant rows, so the only exchange is the final all-gather of the refined
+  bands (``bsm_pipeline_frame_bands_u8``: ncclAllGather).  A band-local
+  ``max_bin`` is safe: bins above it are 0 for every pixel of the band and
+  cannot win the strict-'>' argmax (refine.hpp:102-105).
 
-Rendezvous/plumbing is ``torch.distributed`` (NCCL over NVLink on GPUs, gloo
-for the CPU tests).  The compute of a unit is injectable so the partition and
-gather logic can be tested on CPU against the checker.
+``torch.distributed`` is the plumbing: it carries the NCCL unique id from rank
+0 to the others.  With a non-NCCL process group (gloo: several processes
+sharing one GPU in the tests, or hosts without NCCL) the same per-rank compute
+runs through the C ABI (``run_pipeline_band`` / ``run_pipeline_batch``) and
+the bands / maps travel through the group's own all-gather instead.
 """
 from __future__ import annotations
 
-from typing import Callable, List, Optional, Sequence, Tuple
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from . import BsmConfig, DisparityMap, SamplingPattern, run_pipeline, run_pipeline_band
+from . import (BsmConfig, Context, DisparityMap, SamplingPattern, _params, _ptr_array, _u8, default_context,
+               generate_pattern, run_pipeline_band, run_pipeline_batch)
+from ._lib import DimensionMismatch, check, lib
 
 
 def band_rows(height: int, world: int, rank: int) -> Tuple[int, int]:
-    """Contiguous row band [y0, y1) of `rank`; band sizes differ by at most 1."""
+    """Contiguous row band [y0, y1) of `rank`; band sizes differ by at most 1
+    (the same formula as csrc/bsm_dist.cuh band_of)."""
     if not (0 <= rank < world):
         raise ValueError("rank out of range")
     base, extra = divmod(height, world)
@@ -40,19 +49,60 @@ def shard_units(n_units: int, world: int, rank: int) -> range:
     return range(y0, y1)
 
 
-def _device_for(backend: str):
-    import torch
-    if backend == "nccl":
-        return torch.device("cuda", torch.cuda.current_device())
-    return torch.device("cpu")
+class Comm:
+    """A bsm_comm (NCCL communicator bound to a context) for this rank of a
+    torch.distributed group; the NCCL unique id travels through the group."""
+
+    def __init__(self, ctx: Optional[Context] = None, group=None):
+        import torch.distributed as dist
+        self.ctx = ctx or default_context()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            check(lib().bsm_comm_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        check(lib().bsm_comm_create(self.ctx.handle, uid, self.world, self.rank, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bsm_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _is_nccl(group) -> bool:
+    import torch.distributed as dist
+    return dist.get_backend(group) == "nccl"
+
+
+def _comm_for(ctx: Context, group) -> Comm:
+    cache = ctx.__dict__.setdefault("_comms", {})
+    key = id(group)
+    if key not in cache:
+        cache[key] = Comm(ctx, group)
+    return cache[key]
 
 
 def allgather_bands(band: DisparityMap, height: int, group=None) -> DisparityMap:
-    """All-gather row bands (equal-or-off-by-one heights) into the full map."""
+    """All-gather row bands (equal-or-off-by-one heights) into the full map
+    through the group's own collective (the non-NCCL path)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    dev = _device_for(dist.get_backend(group))
+    dev = torch.device("cuda", torch.cuda.current_device()) if _is_nccl(group) else torch.device("cpu")
     W = band.width
     rows_max = -(-height // world)
     d = torch.zeros((rows_max, W), dtype=torch.float32, device=dev)
@@ -72,35 +122,14 @@ def allgather_bands(band: DisparityMap, height: int, group=None) -> DisparityMap
     return DisparityMap(out_d, out_v)
 
 
-def run_frame_bands(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern] = None, group=None,
-                    compute_band: Optional[Callable] = None) -> DisparityMap:
-    """run_pipeline(...).refined of one frame, row-band partitioned over the group."""
-    import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    H = np.asarray(left).shape[0]
-    y0, y1 = band_rows(H, world, rank)
-    fn = compute_band or (lambda L, R, c, a, b, p: run_pipeline_band(L, R, c, a, b, pattern=p))
-    band = fn(left, right, cfg, y0, y1, pattern)
-    return allgather_bands(band, H, group)
-
-
-def run_pairs_sharded(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], cfg: BsmConfig,
-                      pattern: Optional[SamplingPattern] = None, group=None,
-                      compute_pair: Optional[Callable] = None) -> List[Tuple[int, DisparityMap]]:
-    """Refined maps of this rank's shard of a batch of pairs (no collective)."""
-    import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    fn = compute_pair or (lambda L, R, c, p: run_pipeline(L, R, c, p, outputs="refined").refined)
-    return [(i, fn(pairs[i][0], pairs[i][1], cfg, pattern)) for i in shard_units(len(pairs), world, rank)]
-
-
 def gather_pairs(results: List[Tuple[int, DisparityMap]], n_units: int, shape: Tuple[int, int], dst: int = 0,
                  group=None) -> Optional[List[DisparityMap]]:
-    """Gather every rank's (index, map) results to rank `dst` (None elsewhere)."""
+    """Gather every rank's (index, map) results to rank `dst` (None elsewhere)
+    through the group's own collective (the non-NCCL path)."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    dev = _device_for(dist.get_backend(group))
+    dev = torch.device("cuda", torch.cuda.current_device()) if _is_nccl(group) else torch.device("cpu")
     H, W = shape
     per = max(len(shard_units(n_units, world, r)) for r in range(world))
     d = torch.zeros((per, H, W), dtype=torch.float32, device=dev)
@@ -119,3 +148,65 @@ def gather_pairs(results: List[Tuple[int, DisparityMap]], n_units: int, shape: T
         for k, i in enumerate(shard_units(n_units, world, r)):
             out[i] = DisparityMap(ds[r][k].cpu().numpy(), vs[r][k].cpu().numpy())
     return out  # type: ignore[return-value]
+
+
+def run_frame_bands(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern] = None, group=None,
+                    ctx: Optional[Context] = None) -> DisparityMap:
+    """run_pipeline(...).refined of one frame, row-band partitioned over the
+    group; every rank returns the whole refined map."""
+    import torch.distributed as dist
+    L, R = _u8(left, "left"), _u8(right, "right")
+    if L.shape != R.shape:
+        raise DimensionMismatch("pipeline: left/right dimensions differ")
+    cfg.validate()
+    pattern = pattern or generate_pattern(cfg=cfg)
+    ctx = ctx or default_context()
+    H, W = L.shape
+    if _is_nccl(group):
+        ctx.set_pattern(pattern)
+        comm = _comm_for(ctx, group)
+        d = np.empty((H, W), np.float32)
+        v = np.empty((H, W), np.uint8)
+        p = _params(cfg)
+        check(lib().bsm_pipeline_frame_bands_u8(ctx.handle, comm.handle, L.ctypes.data, R.ctypes.data, W, H,
+                                                C.byref(p), d.ctypes.data, v.ctypes.data))
+        return DisparityMap(d, v)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    y0, y1 = band_rows(H, world, rank)
+    band = run_pipeline_band(L, R, cfg, y0, y1, pattern=pattern, ctx=ctx)
+    return allgather_bands(band, H, group)
+
+
+def run_pairs_sharded(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], cfg: BsmConfig,
+                      pattern: Optional[SamplingPattern] = None, group=None, ctx: Optional[Context] = None,
+                      root: int = 0) -> Optional[List[DisparityMap]]:
+    """run_pipeline(...).refined of every pair of a batch, pairs sharded over
+    the group; the list of all maps on rank `root`, None on the others.  Only
+    this rank's shard of `pairs` is read."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n = len(pairs)
+    mine = shard_units(n, world, rank)
+    cfg.validate()
+    pattern = pattern or generate_pattern(cfg=cfg)
+    ctx = ctx or default_context()
+    views = {i: (_u8(pairs[i][0], "left"), _u8(pairs[i][1], "right")) for i in mine}
+    shapes = {v[0].shape for v in views.values()} | {v[1].shape for v in views.values()}
+    if len(shapes) > 1:
+        raise DimensionMismatch("pipeline: left/right dimensions differ")
+    H, W = np.asarray(pairs[0][0]).shape
+    if _is_nccl(group):
+        ctx.set_pattern(pattern)
+        comm = _comm_for(ctx, group)
+        blank = np.zeros((1, 1), np.uint8)
+        lefts = [views[i][0] if i in views else blank for i in range(n)]
+        rights = [views[i][1] if i in views else blank for i in range(n)]
+        outs = ([(np.empty((H, W), np.float32), np.empty((H, W), np.uint8)) for _ in range(n)]
+                if rank == root else None)
+        p = _params(cfg)
+        check(lib().bsm_pipeline_pairs_sharded_u8(
+            ctx.handle, comm.handle, n, _ptr_array(lefts), _ptr_array(rights), W, H, C.byref(p), root,
+            _ptr_array([o[0] for o in outs]) if outs else None, _ptr_array([o[1] for o in outs]) if outs else None))
+        return [DisparityMap(d, v) for d, v in outs] if outs else None
+    maps = run_pipeline_batch([views[i] for i in mine], cfg, pattern=pattern, ctx=ctx)
+    return gather_pairs(list(zip(mine, maps)), n, (H, W), dst=root, group=group)

@@ -73,16 +73,23 @@ def workload_pair(key: str, index: int = 0, with_gt: bool = False):
     return synth_pair(w.config, w.seed + index, w.width, w.height, with_gt)
 
 
-def colour_pair(height: int, width: int, seed: int = 1):
+def colour_pair(height: int, width: int, seed: int = 1, gen=None):
     """(left, right) (H, W, 3) uint8 RGB views of a synthetic colour pair.
 
     The scene geometry is synth_pair's (configs[0] builder, disparities
     below 60); each view's gray
     level is mapped through three different tone curves and perturbed by
     independent per-channel noise, so r, g and b differ everywhere and the
-    colour conversion is exercised on genuinely colour input.
+    colour conversion is exercised on genuinely colour input.  `gen` replaces
+    synth_pair (same signature) -- the reference arm passes the generator
+    compiled into oracle/_ref.
     """
-    left, right = synth_pair(0, seed, width, height)
+    left, right = (gen or synth_pair)(0, seed, width, height)
+    return colour_views(left, right, seed)
+
+
+def colour_views(left, right, seed: int):
+    """Colour views of a gray pair: three tone curves + per-channel noise."""
     v = np.arange(256, dtype=np.float64)
     luts = np.stack([v, 255.0 * np.sqrt(v / 255.0), 255.0 - 0.8 * v]).round().astype(np.int32)
     rng = np.random.default_rng(seed)
@@ -91,3 +98,11 @@ def colour_pair(height: int, width: int, seed: int = 1):
         c = np.stack([luts[k][img] for k in range(3)], axis=-1) + rng.integers(-6, 7, size=img.shape + (3,))
         out.append(np.clip(c, 0, 255).astype(np.uint8))
     return out[0], out[1]
+
+
+def workload_pair_with(gen, key: str, index: int = 0):
+    """workload_pair through another generator with synth_pair's signature."""
+    w = WORKLOADS[key]
+    if key.endswith("rgb"):
+        return colour_pair(w.height, w.width, seed=w.seed + index, gen=gen)
+    return gen(w.config, w.seed + index, w.width, w.height)
