@@ -1,8 +1,11 @@
 // bsm/descriptor.hpp -- DescriptorField and the descriptor/mask API
 // (reference descriptor.hpp:18-239).  compute_field runs on the GPU
-// (bsm_compute_field_u8: kernels k_descriptor + k_mask3); the single-pixel
-// compute_descriptor / compute_mask are answered from the same device field
-// so they agree with it by construction.
+// (bsm_compute_field_u8 / _f32: kernels k_descriptor4 + k_mask4, or
+// k_descriptor_f32 + k_mask_f32 for float planes, any n <= 8192).  The
+// single-pixel compute_descriptor / compute_mask (descriptor.hpp:174-196) cost
+// O(n): the clamped (2h+1)^2 window around the pixel is gathered on the host
+// into a tile whose centre samples exactly what the pixel samples, and the
+// same kernels run on that tile.
 #pragma once
 
 #include <algorithm>
@@ -78,7 +81,7 @@ inline DescriptorField field_u8(const std::vector<uint8_t>& img, int W, int H, c
     throw_status(bsm_compute_field_u8(ctx.get(), img.data(), W, H, f.descriptor_data(), f.mask_data()));
     return f;
 }
-// Arbitrary float planes (colour views): the float-plane kernels (n <= 4096).
+// Arbitrary float planes (colour views): the float-plane kernels (any n <= 8192).
 inline DescriptorField field_f32(const float* gray, const float* lab, int W, int H, const SamplingPattern& pat) {
     static_assert(sizeof(Lab) == 3 * sizeof(float), "Lab must be three packed floats");
     Context& ctx = context();
@@ -100,26 +103,49 @@ inline DescriptorField compute_field(const GrayImage& gray, const LabImage& lab,
     return detail::field_u8(*u8, gray.width, gray.height, pat);
 }
 
+namespace detail {
+// The (2h+1) x (2h+1) window around (x, y) with the reference's border clamp
+// (clamp_coord, image.hpp:148-150): tile(u, v) = img(clamp(x-h+u), clamp(y-h+v)).
+// Every sample of the tile's centre pixel lies inside the tile, so its
+// descriptor and mask equal the pixel's in the full image.
+template <typename T>
+std::vector<T> window_tile(const std::vector<T>& img, int W, int H, int x, int y, int half) {
+    const int side = 2 * half + 1;
+    std::vector<T> t(std::size_t(side) * side);
+    for (int v = 0; v < side; ++v) {
+        const int yy = std::clamp(y - half + v, 0, H - 1);
+        for (int u = 0; u < side; ++u) t[std::size_t(v) * side + u] = img[std::size_t(yy) * W + std::clamp(x - half + u, 0, W - 1)];
+    }
+    return t;
+}
+}  // namespace detail
+
 inline BitString compute_descriptor(const GrayImage& gray, const SamplingPattern& pat, int x, int y) {
     if (x < 0 || x >= gray.width || y < 0 || y >= gray.height)
         throw InvalidArgument("compute_descriptor: pixel outside image");
-    const auto u8 = detail::u8_from_planes(&gray, nullptr);
+    const int h = pat.half_window(), side = 2 * h + 1;
+    GrayImage tile(side, side);
+    tile.values = detail::window_tile(gray.values, gray.width, gray.height, x, y, h);
+    const auto u8 = detail::u8_from_planes(&tile, nullptr);
     if (!u8) {
-        const std::vector<float> lab(gray.values.size() * 3, 0.0f);  // the mask is not read
-        return detail::field_f32(gray.values.data(), lab.data(), gray.width, gray.height, pat).descriptor_at(x, y);
+        const std::vector<float> lab(tile.values.size() * 3, 0.0f);  // the mask is not read
+        return detail::field_f32(tile.values.data(), lab.data(), side, side, pat).descriptor_at(h, h);
     }
-    return detail::field_u8(*u8, gray.width, gray.height, pat).descriptor_at(x, y);
+    return detail::field_u8(*u8, side, side, pat).descriptor_at(h, h);
 }
 
 inline BitString compute_mask(const LabImage& lab, const SamplingPattern& pat, int x, int y) {
     if (x < 0 || x >= lab.width || y < 0 || y >= lab.height)
         throw InvalidArgument("compute_mask: pixel outside image");
-    const auto u8 = detail::u8_from_planes(nullptr, &lab);
+    const int h = pat.half_window(), side = 2 * h + 1;
+    LabImage tile(side, side);
+    tile.values = detail::window_tile(lab.values, lab.width, lab.height, x, y, h);
+    const auto u8 = detail::u8_from_planes(nullptr, &tile);
     if (!u8) {
-        const std::vector<float> gray(lab.values.size(), 0.0f);  // the descriptor is not read
-        return detail::field_f32(gray.data(), &lab.values[0].l, lab.width, lab.height, pat).mask_at(x, y);
+        const std::vector<float> gray(tile.values.size(), 0.0f);  // the descriptor is not read
+        return detail::field_f32(gray.data(), &tile.values[0].l, side, side, pat).mask_at(h, h);
     }
-    return detail::field_u8(*u8, lab.width, lab.height, pat).mask_at(x, y);
+    return detail::field_u8(*u8, side, side, pat).mask_at(h, h);
 }
 
 }  // namespace bsm

@@ -38,6 +38,7 @@ public:
     // Upload the pattern when it differs from the resident one.
     void use_pattern(const std::vector<int16_t>& flat, int n, int window) {
         if (n == n_ && window == window_ && flat == flat_) return;
+        n_ = 0;  // a failed upload leaves the context without a pattern
         throw_status(bsm_set_pattern(ctx_, flat.data(), n, window));
         flat_ = flat;
         n_ = n;

@@ -5,9 +5,13 @@
 // path consumes grayscale views through bit-exact 256-entry tables.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <optional>
+#include <utility>
 #include <vector>
 
 #include "../bsm_cuda.h"
@@ -113,7 +117,25 @@ inline std::optional<std::vector<uint8_t>> gray_view(const RgbImage& img) {
 struct GrayTables {
     float gray[256];
     float lab[768];
-    GrayTables() { throw_status(bsm_gray_lab_lut(gray, lab)); }
+    // (L, a, b) bit patterns of the 256 gray Lab values, sorted, with the gray
+    // level: a Lab pixel's level by binary search instead of a 256-entry scan
+    std::vector<std::pair<std::array<uint32_t, 3>, int>> lab_index;
+    GrayTables() {
+        throw_status(bsm_gray_lab_lut(gray, lab));
+        for (int c = 0; c < 256; ++c) lab_index.push_back({key(&lab[3 * c]), c});
+        std::sort(lab_index.begin(), lab_index.end());
+    }
+    static std::array<uint32_t, 3> key(const float* p) {
+        std::array<uint32_t, 3> k;
+        std::memcpy(k.data(), p, 12);
+        return k;
+    }
+    int lab_level(const float* p) const {  // smallest gray level with exactly this Lab, or -1
+        const auto k = key(p);
+        auto it = std::lower_bound(lab_index.begin(), lab_index.end(), std::make_pair(k, -1));
+        if (it == lab_index.end() || it->first != k) return -1;
+        return it->second;
+    }
 };
 
 inline const GrayTables& gray_tables() {
@@ -143,8 +165,13 @@ inline std::optional<std::vector<uint8_t>> u8_from_planes(const GrayImage* gray,
         if (lab) {
             const Lab& p = lab->values[i];
             if (k < 0) {
-                for (int c = 0; c < 256 && k < 0; ++c)
-                    if (t.lab[3 * c] == p.l && t.lab[3 * c + 1] == p.a && t.lab[3 * c + 2] == p.b) k = c;
+                const float q[3] = {p.l, p.a, p.b};
+                if (q[0] == 0.0f || q[1] == 0.0f || q[2] == 0.0f) {  // -0.0 == 0.0: compare by value
+                    for (int c = 0; c < 256 && k < 0; ++c)
+                        if (t.lab[3 * c] == p.l && t.lab[3 * c + 1] == p.a && t.lab[3 * c + 2] == p.b) k = c;
+                } else {
+                    k = t.lab_level(q);
+                }
                 if (k < 0) return std::nullopt;
             } else if (t.lab[3 * k] != p.l || t.lab[3 * k + 1] != p.a || t.lab[3 * k + 2] != p.b) {
                 return std::nullopt;

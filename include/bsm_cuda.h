@@ -205,6 +205,10 @@ int bsm_stream_wait(bsm_ctx* ctx, void* stream);
 int bsm_set_profiling(bsm_ctx* ctx, int enable);
 int bsm_last_timings(bsm_ctx* ctx, float* ms, int max, int* count);
 const char* bsm_timing_names(void);
+/* Test hook: with BSM_GUARD=1 in the environment when the first context is
+ * created, every device buffer is bracketed by 4 KiB guards (and its payload
+ * pre-filled) with 0xA5; this reports how many guard bytes changed. */
+int bsm_debug_check_guards(bsm_ctx* ctx, long long* damaged, int* enabled);
 /* Kernel launches issued by the last pipeline call. */
 int bsm_last_launch_count(bsm_ctx* ctx, int* count);
 /* Measured masked-XOR-popcount word-op throughput of this device (words/s),

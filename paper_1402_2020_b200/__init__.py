@@ -163,6 +163,7 @@ class Context:
         key = (pattern.window, pairs.tobytes())
         if key == self._pattern_key:
             return
+        self._pattern_key = None  # a failed upload leaves the context without a pattern
         check(lib().bsm_set_pattern(self.handle, _ptr(pairs), int(pairs.shape[0]), int(pattern.window)))
         self._pattern_key = key
 
@@ -190,6 +191,12 @@ class Context:
         v = C.c_double()
         check(lib().bsm_measure_popc_peak(self.handle, C.byref(v)))
         return float(v.value)
+
+    def debug_check_guards(self) -> tuple:
+        """(damaged guard bytes, guard mode on) -- see bsm_debug_check_guards."""
+        n, on = C.c_longlong(), C.c_int()
+        check(lib().bsm_debug_check_guards(self.handle, C.byref(n), C.byref(on)))
+        return int(n.value), bool(on.value)
 
     def set_refine_mode(self, mode: int) -> None:
         """-1 auto, 2 warp per pixel + host weight table, 3 ordered fold + table, 4 fold + device exp."""

@@ -111,6 +111,7 @@ _SIGS = {
     "bsm_pipeline_pairs_sharded_u8": [_P, _P, _I, _P, _P, _I, _I, C.POINTER(bsm_params), _I, _P, _P],
     "bsm_stream": [_P, C.POINTER(C.c_void_p)],
     "bsm_stream_wait": [_P, _P],
+    "bsm_debug_check_guards": [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_int)],
     "bsm_set_profiling": [_P, _I],
     "bsm_last_timings": [_P, _P, _I, C.POINTER(C.c_int)],
     "bsm_last_launch_count": [_P, C.POINTER(C.c_int)],

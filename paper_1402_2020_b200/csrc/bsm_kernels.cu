@@ -3,11 +3,12 @@
 // kernel's roofline, and the reference function (file:line) it replaces.
 //
 // Device layout (per view, W x H, n bits, NW = 2*ceil(n/64) u32 words):
-//   field[(y*NW + w)*Wp + x]   word-major ("bit-plane rows"), Wp = W rounded up
-//   to 128, so a row segment of one word is a contiguous, 16-B-aligned span:
-//   the cost kernel stages [K words x span] boxes by TMA (one tensor map per
-//   field, dims (Wp, NW, rows)) and every shared-memory read is a
-//   conflict-free 16-B lane-contiguous LDS.128.
+//   field[w*P + y*Wq + x]   word planes ("bit-plane images"), Wq = W rounded up
+//   to 4, P = rows*Wq rounded up to 32: for a fixed word the pixels of all rows
+//   are one contiguous run, so the cost kernel tiles pixels over the flat
+//   index y*Wq + x (no padding of rows to a tile multiple) and stages
+//   [K words x span] boxes by TMA (one 2-D tensor map per field, dims (P, NW));
+//   every shared-memory read is a conflict-free 16-B lane-contiguous LDS.128.
 //   u32 word w of a pixel = bits 32w..32w+31 = the low/high half of the
 //   reference's u64 word w>>1 (bitstring.hpp:47-51).
 #include <cuda.h>
@@ -18,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -51,6 +53,12 @@ constexpr int kCostK = 16;           // u32 words per pipeline stage
 constexpr int kCostStages = 3;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+// Field plane geometry: row pitch and plane size (u32 words) of `rows` rows.
+inline int field_pitch(int W) { return round_up(W, 4); }
+inline size_t field_plane(int W, int rows) {
+    const size_t p = size_t(std::max(rows, 1)) * size_t(field_pitch(W));
+    return (p + 31) / 32 * 32;
+}
 
 #include "kern_field.cuh"
 #include "kern_cost.cuh"
@@ -61,28 +69,54 @@ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // ===========================================================================
 // Context.
-enum Timing { T_H2D, T_DESC, T_MASK, T_WTA_L, T_WTA_R, T_WTA_U, T_LR, T_REFINE, T_D2H, T_COUNT };
-static const char* kTimingNames = "h2d,descriptor,mask,wta_left,wta_right,wta_unmasked,lr_check,refine,d2h";
+enum Timing { T_H2D, T_DESC, T_MASK, T_WTA, T_WTA_U, T_LR, T_REFINE, T_D2H, T_COUNT };
+static const char* kTimingNames = "h2d,descriptor,mask,wta,wta_unmasked,lr_check,refine,d2h";
+
+// Debug guard mode (environment BSM_GUARD=1 when the first context is
+// created; compute-sanitizer is not available on the GPU pool): every device
+// buffer gets kGuard bytes of 0xA5 before and after it, and its payload starts
+// as 0xA5 too, so out-of-bounds writes show up in bsm_debug_check_guards and
+// reads of never-written memory change results against the reference.
+constexpr size_t kGuard = 4096;
+bool g_guard = false;
 
 struct DevBuf {
     void* p = nullptr;
+    void* base = nullptr;
     size_t cap = 0;
     int ensure(size_t bytes) {
         if (bytes <= cap) return BSM_OK;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMalloc: ") + cudaGetErrorString(e));
+        release();
+        const size_t extra = g_guard ? 2 * kGuard : 0;
+        cudaError_t e = cudaMalloc(&base, bytes + extra);
+        if (e != cudaSuccess) {
+            base = nullptr;
+            return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMalloc: ") + cudaGetErrorString(e));
+        }
+        if (g_guard && (e = cudaMemset(base, 0xA5, bytes + extra)) != cudaSuccess)
+            return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMemset: ") + cudaGetErrorString(e));
+        p = static_cast<char*>(base) + (g_guard ? kGuard : 0);
         cap = bytes;
         return BSM_OK;
     }
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
     void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
+        if (base) cudaFree(base);
+        p = base = nullptr;
         cap = 0;
+    }
+    // number of guard bytes that no longer hold 0xA5 (0 outside guard mode)
+    size_t damaged() const {
+        if (!g_guard || !base) return 0;
+        std::vector<uint8_t> h(kGuard);
+        size_t bad = 0;
+        for (int side = 0; side < 2; ++side) {
+            const char* g = static_cast<const char*>(base) + (side ? kGuard + cap : 0);
+            if (cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return kGuard;
+            for (uint8_t v : h) bad += v != 0xA5;
+        }
+        return bad;
     }
 };
 
@@ -131,6 +165,7 @@ struct bsm_ctx {
     cudaEvent_t ev[T_COUNT][kEvPerSlot][2] = {};
     int ev_used[T_COUNT] = {};
     int launches = 0;
+    int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction
     DevBuf popc_out;
     // batch pipelining (bsm_pipeline_batch_u8): two slots of input views and
     // refined maps, an H2D and a D2H copy stream ordered by events
@@ -140,6 +175,15 @@ struct bsm_ctx {
 };
 
 namespace {
+
+std::vector<DevBuf*> ctx_bufs(bsm_ctx* c) {
+    return {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pqb, &c->d_uoff,
+            &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col, &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr,
+            &c->fmr, &c->keys_l, &c->keys_r, &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d,
+            &c->rw_d, &c->un_d, &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0,
+            &c->aux1, &c->aux2, &c->aux3, &c->popc_out, &c->bimg[0][0], &c->bimg[0][1], &c->bimg[1][0],
+            &c->bimg[1][1], &c->bout_d[0], &c->bout_d[1], &c->bout_v[0], &c->bout_v[1]};
+}
 
 struct Scope {  // brackets one pipeline stage with events when profiling
     bsm_ctx* c;
@@ -223,8 +267,26 @@ int ensure_mask_offsets(bsm_ctx* c, int TW) {
     return BSM_OK;
 }
 
+// Bytes of the exact grayscale weight table W[tri(u, v)][col(dx^2 + dy^2)]
+// (32,896 gray pairs x distinct squared distances within the radius).
+constexpr size_t kWeightTableCap = size_t(256) << 20;
+size_t weight_table_bytes(int radius) {
+    std::vector<uint8_t> seen(size_t(2) * radius * radius + 1, 0);
+    size_t ncol = 0;
+    for (int dy = 0; dy <= radius; ++dy)
+        for (int dx = 0; dx <= radius; ++dx) {
+            uint8_t& f = seen[size_t(dx * dx + dy * dy)];
+            ncol += f == 0;
+            f = 1;
+        }
+    return size_t(256 * 257 / 2) * ncol * sizeof(double);
+}
+
 int ensure_weight_table(bsm_ctx* c, double lc, double le, int radius) {
     if (c->wt_radius == radius && c->wt_lc == lc && c->wt_le == le) return BSM_OK;
+    if (weight_table_bytes(radius) > kWeightTableCap)
+        return set_err(BSM_UNSUPPORTED, "bsm: vote_radius " + std::to_string(radius) +
+                                            " needs a weight table above 256 MiB and the device exp is unavailable");
     std::vector<double> w;
     std::vector<int16_t> s2col;
     int ncol = 0;
@@ -257,7 +319,8 @@ size_t mask4_smem(const bsm_ctx* c) {
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
 int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
-    const int Wp = round_up(W, 128);
+    const int Wp = round_up(W, 128), Wq = field_pitch(W);
+    const size_t P = field_plane(W, rows);
     BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
@@ -271,19 +334,19 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
                                                                     int(grid.x * grid.y))));
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<int2>(),
-                                                                    c->n, c->half, TWs, c->NW, Wp, desc);
+                                                                    c->n, c->half, TWs, c->NW, Wq, P, desc);
         BSM_TRY(check_launch(c, "descriptor"));
     }
     {
         Scope s(c, T_MASK);
         const size_t sm4 = mask4_smem(c);
-        dim3 grid3(Wp / kM3Px, rows);
+        dim3 grid3((Wq + kM3Px - 1) / kM3Px, rows);
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
             kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
                                                 c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<int32_t>(),
                                                 c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
-                                                c->half, mask4_tw(c->half), c->NW, Wp, mask);
+                                                c->half, mask4_tw(c->half), c->NW, Wq, P, mask);
             return BSM_OK;
         };
         // chunks of 32 positions per lane: the work scales with n
@@ -297,8 +360,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
 }
 
 // WTA keys of rows [0, rows) of device fields (SoA); keys: rows x W.
-// Tensor map of a device field [rows][NW][Wp] u32 for TMA boxes of box_x
-// columns x kCostK words x 1 row; out-of-range boxes read zeros.
+// Tensor map of a device field [NW][P] u32 for TMA boxes of box_x pixels x
+// kCostK words; out-of-range boxes read zeros.
 int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int rows, int box_x) {
     static PFN_cuTensorMapEncodeTiled encode = nullptr;
     if (!encode) {
@@ -309,38 +372,55 @@ int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int
             return set_err(BSM_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
     }
-    const int Wp = round_up(W, 128);
-    const cuuint64_t dims[3] = {cuuint64_t(Wp), cuuint64_t(NW), cuuint64_t(std::max(rows, 1))};
-    const cuuint64_t strides[2] = {cuuint64_t(Wp) * 4, cuuint64_t(NW) * Wp * 4};
-    const cuuint32_t box[3] = {cuuint32_t(box_x), cuuint32_t(kCostK), 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(field), dims, strides, box,
+    const size_t P = field_plane(W, rows);
+    const cuuint64_t dims[2] = {cuuint64_t(P), cuuint64_t(NW)};
+    const cuuint64_t strides[1] = {cuuint64_t(P) * 4};
+    const cuuint32_t box[2] = {cuuint32_t(box_x), cuuint32_t(kCostK)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(field), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(BSM_CUDA_ERROR, "CUDA: cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     return BSM_OK;
 }
 
-int wta_device(bsm_ctx* c, const uint32_t* dref, const uint32_t* mref, const uint32_t* doth, int W, int rows,
-               int d_max, bool right, bool masked, uint32_t* keys, int timing) {
+// K3 over device fields.  Direction 0 (left reference, x - d): ref = (dl, ml),
+// other = dr, keys -> keys_l; direction 1 (right reference, x + d): ref =
+// (dr, mr), other = dl, keys -> keys_r.  both: one launch for the two
+// directions; otherwise only direction `dir`.  ml/mr == nullptr: unmasked.
+int wta_device(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_t* dr, const uint32_t* mr, int W,
+               int rows, int d_max, bool both, int dir, bool masked, uint32_t* keys_l, uint32_t* keys_r, int timing) {
     Scope s(c, timing);
-    const int Wp = round_up(W, 128);
+    const int Wq = field_pitch(W);
     const int dz = (d_max + kCostDisp - 1) / kCostDisp;
-    if (dz > 1) BSM_CUDA(cudaMemsetAsync(keys, 0xFF, size_t(rows) * W * 4, c->stream));
-    dim3 grid(dz, Wp / kCostTile, rows);
+    const bool use_l = both || dir == 0, use_r = both || dir == 1;
+    if (dz > 1) {
+        if (use_l) BSM_CUDA(cudaMemsetAsync(keys_l, 0xFF, size_t(rows) * W * 4, c->stream));
+        if (use_r) BSM_CUDA(cudaMemsetAsync(keys_r, 0xFF, size_t(rows) * W * 4, c->stream));
+    }
+    const long long tiles = (static_cast<long long>(rows) * Wq + kCostTile - 1) / kCostTile;
+    if (tiles > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel grid");
+    if (dz * (both ? 2 : 1) > 65535) return set_err(BSM_UNSUPPORTED, "bsm: d_max too large for the cost kernel grid");
+    dim3 grid(unsigned(tiles), unsigned(dz * (both ? 2 : 1)));
     const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
-    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 16;  // + full/empty mbarriers
-    CUtensorMap tr, tmk, to;
-    BSM_TRY(field_tensor_map(&tr, dref, W, c->NW, rows, kCostTile));
-    BSM_TRY(field_tensor_map(&tmk, mref ? mref : dref, W, c->NW, rows, kCostTile));
-    BSM_TRY(field_tensor_map(&to, doth, W, c->NW, rows, kCostTile + kCostDisp));
+    const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 16 + kCostStages * 4;
+    CUtensorMap lr, lm, lo, rr, rm, ro;  // unused slots are copies of a valid map
+    const uint32_t* ml_ = ml ? ml : dl;
+    const uint32_t* mr_ = mr ? mr : dr;
+    BSM_TRY(field_tensor_map(&lr, use_l ? dl : dr, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&lm, use_l ? ml_ : mr_, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, kCostTile + kCostDisp));
+    BSM_TRY(field_tensor_map(&rr, use_r ? dr : dl, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&rm, use_r ? mr_ : ml_, W, c->NW, rows, kCostTile));
+    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, kCostTile + kCostDisp));
     auto launch = [&](auto kern) -> int {
         BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<grid, 256, sm, c->stream>>>(tr, tmk, to, W, rows, c->NW, d_max, keys, 2u);
+        kern<<<grid, 256, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, rows, c->NW, d_max, dz, both ? 0 : dir,
+                                           keys_l, keys_r, 2u);
         return BSM_OK;
     };
-    if (right) BSM_TRY(masked ? launch(k_cost_wta<true, true>) : launch(k_cost_wta<true, false>));
-    else BSM_TRY(masked ? launch(k_cost_wta<false, true>) : launch(k_cost_wta<false, false>));
+    if (c->k3_variant & 1) BSM_TRY(masked ? launch(k_cost_wta<true, false>) : launch(k_cost_wta<false, false>));
+    else BSM_TRY(masked ? launch(k_cost_wta<true, true>) : launch(k_cost_wta<false, true>));
     return check_launch(c, "cost_wta");
 }
 
@@ -366,6 +446,9 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
     const int tb = 256;
     int mode = c->refine_mode >= 0 ? c->refine_mode : (lab ? 4 : 3);
     if (lab && mode != 4) mode = 4;  // Lab planes: the weight table only covers gray pairs
+    // large radii: the exact table would exceed 256 MiB (3 GB at radius 180),
+    // so the gray path evaluates the weights with the device exp instead
+    if (!lab && mode != 4 && c->exp_ok && weight_table_bytes(radius) > kWeightTableCap) mode = 4;
     if (mode == 4 && !c->exp_ok) {
         if (lab) return set_err(BSM_UNSUPPORTED, "bsm: colour refine needs the device exp (" + c->exp_why + ")");
         mode = 3;
@@ -445,29 +528,30 @@ size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, int H, int ybeg, int rows,
                      uint32_t* desc, uint32_t* mask) {
-    const int Wp = round_up(W, 128);
+    const int Wq = field_pitch(W);
+    const size_t P = field_plane(W, rows);
     BSM_TRY(ensure_descf_table(c));
     BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
         const int TW = kDfTX + 2 * c->half, TH = kDfTY * kDfPY + 2 * c->half;
         const size_t sm = size_t(TW) * TH * 4;
-        dim3 grid(Wp / kDfTX, (rows + kDfTY * kDfPY - 1) / (kDfTY * kDfPY));
+        dim3 grid((Wq + kDfTX - 1) / kDfTX, (rows + kDfTY * kDfPY - 1) / (kDfTY * kDfPY));
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         k_descriptor_f32<<<grid, dim3(kDfTX, kDfTY), sm, c->stream>>>(gray, W, H, ybeg, rows, c->d_descf.as<int2>(),
-                                                                      c->n, c->half, c->NW, Wp, desc);
+                                                                      c->n, c->half, c->NW, Wq, P, desc);
         BSM_TRY(check_launch(c, "descriptor_f32"));
     }
     {
         Scope s(c, T_MASK);
         const size_t sm = maskf_smem(c);
-        dim3 grid(Wp / kM3Px, rows);
+        dim3 grid((Wq + kM3Px - 1) / kM3Px, rows);
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows,
                                               c->d_pqb.as<uint4>() + (c->mch <= 4 ? 2 * kPqTable / 4 : 0),
                                               c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uxy.as<int32_t>(), c->mslots,
-                                              round_up(c->mslots + 1, 4), c->NW, Wp, mask, c->half);
+                                              round_up(c->mslots + 1, 4), c->NW, Wq, P, mask, c->half);
             return BSM_OK;
         };
         BSM_TRY(c->mch == 1   ? launch(k_mask_f32<1>)
@@ -510,8 +594,7 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
     const int r0 = std::max(0, out0 - p->vote_radius);
     const int r1 = std::min(H, out0 + out_rows + p->vote_radius);
     const int rows = r1 - r0;
-    const int Wp = round_up(W, 128);
-    const size_t fbytes = size_t(rows) * c->NW * Wp * 4;
+    const size_t fbytes = field_plane(W, rows) * c->NW * 4;
     const size_t px = size_t(rows) * W;
     BSM_TRY(c->fdl.ensure(fbytes));
     BSM_TRY(c->fml.ensure(fbytes));
@@ -537,13 +620,21 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
         BSM_TRY(field_device_f32(c, v.gl, v.ll, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
         BSM_TRY(field_device_f32(c, v.gr, v.lr, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
     }
-    BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(), W, rows, p->d_max,
-                       false, true, c->keys_l.as<uint32_t>(), T_WTA_L));
-    BSM_TRY(wta_device(c, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>(), c->fdl.as<uint32_t>(), W, rows, p->d_max,
-                       true, true, c->keys_r.as<uint32_t>(), T_WTA_R));
+    if (c->k3_variant & 2) {  // one launch per direction
+        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 0, true, c->keys_l.as<uint32_t>(),
+                           c->keys_r.as<uint32_t>(), T_WTA));
+        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 1, true, c->keys_l.as<uint32_t>(),
+                           c->keys_r.as<uint32_t>(), T_WTA));
+    } else {
+        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, true, 0, true, c->keys_l.as<uint32_t>(),
+                           c->keys_r.as<uint32_t>(), T_WTA));
+    }
     if (want_unmasked)
-        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), nullptr, c->fdr.as<uint32_t>(), W, rows, p->d_max, false, false,
-                           c->keys_u.as<uint32_t>(), T_WTA_U));
+        BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), nullptr, c->fdr.as<uint32_t>(), nullptr, W, rows, p->d_max, false,
+                           0, false, c->keys_u.as<uint32_t>(), nullptr, T_WTA_U));
     {
         Scope s(c, T_LR);
         BSM_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
@@ -659,6 +750,7 @@ int check_dims(int W, int H) {
     if (W < 1 || H < 1) return set_err(BSM_INVALID_ARGUMENT, "bsm: image dimensions must be >= 1");
     if (int64_t(W) * H > (int64_t(1) << 31) - 1)
         return set_err(BSM_UNSUPPORTED, "bsm: images above 2^31 pixels are outside this build's envelope");
+    if (H > 65535) return set_err(BSM_UNSUPPORTED, "bsm: images taller than 65535 rows are outside this build's envelope");
     return BSM_OK;
 }
 
@@ -685,8 +777,14 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     BSM_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10)
         return set_err(BSM_CUDA_ERROR, std::string("CUDA: built for sm_100a, device is ") + prop.name);
+    {
+        const char* g = std::getenv("BSM_GUARD");
+        static bool once = (g_guard = g && g[0] == '1', true);
+        (void)once;
+    }
     bsm_ctx* c = new bsm_ctx();
     c->device = device;
+    if (const char* v = std::getenv("BSM_K3_VARIANT")) c->k3_variant = std::atoi(v);
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
@@ -734,16 +832,8 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
 int bsm_ctx_destroy(bsm_ctx* c) {
     if (!c) return BSM_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->d_pos, &c->d_descf, &c->d_rgb_gray, &c->d_rgb_lab, &c->planes, &c->d_desc4, &c->d_pqb, &c->d_uoff, &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col,
-                      &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr, &c->fmr, &c->keys_l, &c->keys_r,
-                      &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d, &c->rw_d, &c->un_d,
-                      &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0, &c->aux1, &c->aux2, &c->aux3, &c->popc_out};
-    for (DevBuf* b : bufs) b->release();
+    for (DevBuf* b : ctx_bufs(c)) b->release();
     for (int s = 0; s < 2; ++s) {
-        c->bimg[s][0].release();
-        c->bimg[s][1].release();
-        c->bout_d[s].release();
-        c->bout_v[s].release();
         for (cudaEvent_t e : {c->ev_in[s], c->ev_free[s], c->ev_done[s], c->ev_out[s]})
             if (e) cudaEventDestroy(e);
     }
@@ -790,7 +880,9 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
         if (pairs[i] < -half || pairs[i] > half)
             return set_err(BSM_INVALID_ARGUMENT, "pattern: offset outside window");
     BSM_CUDA(cudaSetDevice(c->device));
-    c->n = n;
+    // any failure below leaves the context without a pattern (n = 0), never
+    // with a half-updated one; c->n is set last
+    c->n = 0;
     c->window = window;
     c->half = half;
     c->NW = 2 * ((n + 63) / 64);
@@ -879,19 +971,21 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     c->uoff_tw = -1;
     if (mask4_smem(c) > 200 * 1024 || maskf_smem(c) > 200 * 1024)
         return set_err(BSM_UNSUPPORTED, "bsm: pattern too large for shared-memory staging");
+    c->n = n;  // committed: every table above is consistent with this pattern
     return BSM_OK;
 }
 
 // Device SoA field -> reference AoS words in c->aux0 (bit order restored).
 static int soa_to_aos(bsm_ctx* c, const uint32_t* src, int W, int H) {
-    const int Wp = round_up(W, 128), tb = 256;
+    const int Wq = field_pitch(W), tb = 256;
+    const size_t P = field_plane(W, H);
     const size_t aos = size_t(H) * W * c->NW;
     if (c->permuted)
-        k_soa_to_aos_perm<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wp,
+        k_soa_to_aos_perm<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wq, P,
                                                                               c->d_pos.as<int>(), c->n,
                                                                               c->aux0.as<uint32_t>());
     else
-        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wp,
+        k_soa_to_aos<<<unsigned((aos + tb - 1) / tb), tb, 0, c->stream>>>(src, W, H, c->NW, Wq, P,
                                                                          c->aux0.as<uint32_t>());
     return check_launch(c, "soa_to_aos");
 }
@@ -901,8 +995,7 @@ int bsm_compute_field_u8(bsm_ctx* c, const uint8_t* img, int W, int H, uint64_t*
     BSM_TRY(check_pattern(c));
     BSM_TRY(check_dims(W, H));
     if (!img) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
-    const int Wp = round_up(W, 128);
-    const size_t fbytes = size_t(H) * c->NW * Wp * 4;
+    const size_t fbytes = field_plane(W, H) * c->NW * 4;
     BSM_TRY(upload_views(c, img, nullptr, W, H));
     BSM_TRY(c->fdl.ensure(fbytes));
     BSM_TRY(c->fml.ensure(fbytes));
@@ -931,8 +1024,9 @@ int bsm_wta(bsm_ctx* c, const uint64_t* desc_ref, const uint64_t* mask_ref, cons
     const int NW = 2 * ((n + 63) / 64);
     const int savedNW = c->NW;
     c->NW = NW;
-    const int Wp = round_up(W, 128);
-    const size_t aos = size_t(H) * W * NW, soa = size_t(H) * NW * Wp;
+    const int Wq = field_pitch(W);
+    const size_t P = field_plane(W, H);
+    const size_t aos = size_t(H) * W * NW, soa = size_t(NW) * P;
     int rc = BSM_OK;
     do {
         if ((rc = c->aux0.ensure(aos * 4)) != BSM_OK) break;
@@ -950,14 +1044,19 @@ int bsm_wta(bsm_ctx* c, const uint64_t* desc_ref, const uint64_t* mask_ref, cons
                 rc = set_err(BSM_CUDA_ERROR, "CUDA: field upload failed");
                 break;
             }
-            k_aos_to_soa<<<unsigned((soa + tb - 1) / tb), tb, 0, c->stream>>>(c->aux0.as<uint32_t>(), W, H, NW, Wp,
+            k_aos_to_soa<<<unsigned((soa + tb - 1) / tb), tb, 0, c->stream>>>(c->aux0.as<uint32_t>(), W, H, NW, Wq, P,
                                                                             dsts[k]->as<uint32_t>());
             rc = check_launch(c, "aos_to_soa");
             if (rc == BSM_OK) rc = sync(c);  // aux0 is reused by the next upload
         }
         if (rc != BSM_OK) break;
-        rc = wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(), W, H, d_max,
-                        right_ref != 0, use_mask != 0, c->keys_l.as<uint32_t>(), right_ref ? T_WTA_R : T_WTA_L);
+        // the reference field is fdl (+ fml) whichever the direction
+        rc = right_ref ? wta_device(c, c->fdr.as<uint32_t>(), nullptr, c->fdl.as<uint32_t>(),
+                                    use_mask ? c->fml.as<uint32_t>() : nullptr, W, H, d_max, false, 1, use_mask != 0,
+                                    nullptr, c->keys_l.as<uint32_t>(), T_WTA)
+                       : wta_device(c, c->fdl.as<uint32_t>(), use_mask ? c->fml.as<uint32_t>() : nullptr,
+                                    c->fdr.as<uint32_t>(), nullptr, W, H, d_max, false, 0, use_mask != 0,
+                                    c->keys_l.as<uint32_t>(), nullptr, T_WTA);
         if (rc != BSM_OK) break;
         const size_t px = size_t(H) * W;
         k_keys_to_float<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->keys_l.as<uint32_t>(), px,
@@ -1153,6 +1252,19 @@ int bsm_pipeline_batch_u8_device(bsm_ctx* c, int n_pairs, const uint8_t* const* 
     return BSM_OK;
 }
 
+// Guard mode (BSM_GUARD=1): damaged guard bytes over every device buffer of
+// the context after its queued work completes; *enabled = guard mode on.
+int bsm_debug_check_guards(bsm_ctx* c, long long* damaged, int* enabled) {
+    if (!c || !damaged) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    BSM_CUDA(cudaSetDevice(c->device));
+    BSM_CUDA(cudaStreamSynchronize(c->stream));
+    long long bad = 0;
+    for (DevBuf* b : ctx_bufs(c)) bad += (long long)b->damaged();
+    *damaged = bad;
+    if (enabled) *enabled = g_guard ? 1 : 0;
+    return BSM_OK;
+}
+
 // Make the context's stream wait for all work queued so far on `stream` (a
 // cudaStream_t of the caller, e.g. the one that produced device inputs).
 int bsm_stream_wait(bsm_ctx* c, void* stream) {
@@ -1288,8 +1400,7 @@ int bsm_compute_field_f32(bsm_ctx* c, const float* gray, const float* lab, int W
     BSM_TRY(check_dims(W, H));
     if (!gray || !lab) return set_err(BSM_INVALID_ARGUMENT, "bsm: null plane");
     const size_t px = size_t(W) * H;
-    const int Wp = round_up(W, 128);
-    const size_t fbytes = size_t(H) * c->NW * Wp * 4;
+    const size_t fbytes = field_plane(W, H) * c->NW * 4;
     BSM_TRY(c->planes.ensure(px * 32));
     float* g = c->planes.as<float>();
     float* l3 = g + px;

@@ -27,67 +27,89 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
 }
-// 3-D box (x, word, row) of a field into shared memory, completing on bar.
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int w, int y, uint64_t* bar) {
+// 2-D box (pixel, word) of a field into shared memory, completing on bar.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int p, int w, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];\n" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(w), "r"(y), "r"(smem_addr(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(p), "r"(w), "r"(smem_addr(bar))
         : "memory");
+}
+// Arrival on a shared-memory counter with CTA-scope acquire-release ordering;
+// returns the previous value.
+__device__ __forceinline__ uint32_t smem_arrive_count(uint32_t* ctr) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_addr(ctr)) : "memory");
+    return old;
 }
 
 // ---------------------------------------------------------------------------
 // K3 -- fused masked Hamming cost + winner-take-all.  matcher.hpp:80-113
 // (wta), :24-29/bitstring.hpp:73-88 (masked_hamming), :35-38 (other_column),
 // :68-75 (ties -> smaller d).  No cost volume is materialised.
-// CTA tile: 128 reference pixels of one row x 64 disparities; 8 warps, warp wi
-// owns disparities [d0 + 8wi, +8), lane l owns pixels [x0 + 4l, +4): a 4 x 8
-// register block of costs, so each staged word feeds 32 word-ops from 5
-// LDS.128 (ref desc, ref mask, a 12-word window of the other view).
+//
+// Pixels are tiled over the flat index p = y * Wq + x of the field planes
+// (Wq = W rounded up to 4), so a 128-pixel tile may cover the end of one row
+// and the start of the next: no lane idles on padding to a tile multiple, and
+// a correspondence p -+ d is valid exactly when x -+ d stays inside the row.
+// CTA tile: 128 reference pixels x 64 disparities; 8 warps, warp wi owns
+// disparities [d0 + 8wi, +8), lane l owns pixels [p0 + 4l, +4) (one row: Wq and
+// p0 + 4l are multiples of 4): a 4 x 8 register block of costs, so each staged
+// word feeds 32 word-ops from 5 LDS.128 (ref desc, ref mask, a 12-word window
+// of the other view).
 // Words stream through a 3-stage ring of K = 16 words filled by TMA: one
 // thread arms the stage's mbarrier and issues three tensor-box copies
-// ([K x 128] desc, [K x 128] mask, [K x 192] other-view span); columns and
+// ([K x 128] desc, [K x 128] mask, [K x 192] other-view span); pixels and
 // words outside the field arrive zero-filled, so the load path carries no
-// per-thread predicates or address arithmetic.  The argmin key is
-// (cost << 16) | d (min cost, then smaller d); d-split CTAs merge with
-// atomicMin.  Out-of-image correspondences are skipped (matcher.hpp:100).
-template <bool RIGHT, bool MASKED>
-__global__ void __launch_bounds__(256, 2)
-    k_cost_wta(const __grid_constant__ CUtensorMap tm_ref, const __grid_constant__ CUtensorMap tm_mask,
-               const __grid_constant__ CUtensorMap tm_oth, int W, int rows, int NW, int D,
-               uint32_t* __restrict__ keys, uint32_t two) {
+// per-thread predicates or address arithmetic.  Each warp, once done with a
+// slot, arrives on the slot's counter (acquire-release, CTA scope); the LAST
+// of the 8 warps refills it, so no warp waits for the others between stages.
+// Warps whose (pixel, d) block has no in-range correspondence skip the
+// arithmetic; CTAs with none exit.  The argmin key is (cost << 16) | d (min
+// cost, then smaller d); d-split CTAs merge with atomicMin.  Out-of-image
+// correspondences are skipped (matcher.hpp:100).
+// One launch covers both directions (blockIdx.y = direction x d-block).
+template <bool RIGHT, bool MASKED, bool LASTREFILL>
+__device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const CUtensorMap* tm_mask,
+                                              const CUtensorMap* tm_oth, int W, int Wq, int npix, int NW, int D,
+                                              int d0, bool split, uint32_t* __restrict__ keys, uint32_t two) {
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
     constexpr int SA = K * T, SB = K * BW;
     constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
     constexpr uint32_t STAGE_BYTES = uint32_t(STAGE) * 4;
     extern __shared__ __align__(128) uint32_t csm[];
     uint32_t* red = csm + ST * STAGE;                                 // [8][T]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full, then [ST] empty
-    uint64_t* empty = bars + ST;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * T);         // [ST] full barriers
+    uint64_t* empty = bars + ST;                                       // [ST] empty barriers (!LASTREFILL)
+    uint32_t* ctr = reinterpret_cast<uint32_t*>(bars + 2 * ST);        // [ST] slot-release counters
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    const int x0 = blockIdx.y * T;
-    const int y = blockIdx.z;
-    const int d0 = blockIdx.x * DC;
-    const int bbase = RIGHT ? x0 + d0 : x0 - d0 - DC;
+    const int p0 = blockIdx.x * T;
+    const int bbase = RIGHT ? p0 + d0 : p0 - d0 - DC;
     const int nchunks = (NW + K - 1) / K;
-    const int xhi = min(x0 + T, W) - 1;
-    if (d0 >= D || (RIGHT ? x0 + d0 >= W : xhi < d0)) return;
+    // this lane's 4 pixels: row yl, columns xl .. xl + 3
+    const int pl = p0 + lane * 4;
+    const int yl = pl / Wq, xl = pl - yl * Wq;
+    const bool lane_in = pl < npix && xl < W;
+    const int ds = wi * 8, dlo = d0 + ds;
+    const bool any = lane_in && dlo < D && (RIGHT ? xl + dlo < W : min(xl + 3, W - 1) >= dlo);
+    const bool busy = __any_sync(0xFFFFFFFFu, any);
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(bars + s, 1);
             mbar_init(empty + s, 8);  // one arrival per warp
+            ctr[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
-    auto load_stage = [&](int c, int st) {  // thread 0 only
+    if (!__syncthreads_or(busy)) return;  // no in-range correspondence in the whole tile
+    auto load_stage = [&](int c, int st) {
         uint32_t* s = csm + st * STAGE;
         mbar_expect_tx(bars + st, STAGE_BYTES);
-        tma_load_3d(s, &tm_ref, x0, c * K, y, bars + st);
-        if constexpr (MASKED) tma_load_3d(s + SA, &tm_mask, x0, c * K, y, bars + st);
-        tma_load_3d(s + (MASKED ? 2 * SA : SA), &tm_oth, bbase, c * K, y, bars + st);
+        tma_load_2d(s, tm_ref, p0, c * K, bars + st);
+        if constexpr (MASKED) tma_load_2d(s + SA, tm_mask, p0, c * K, bars + st);
+        tma_load_2d(s + (MASKED ? 2 * SA : SA), tm_oth, bbase, c * K, bars + st);
     };
     if (tid == 0)
         for (int s = 0; s < ST && s < nchunks; ++s) load_stage(s, s);
@@ -102,15 +124,14 @@ __global__ void __launch_bounds__(256, 2)
         }
 
     const int xs = lane * 4;
-    const int ds = wi * 8;
     const int c0 = RIGHT ? xs + ds : xs - ds + DC - 8;
-    const bool busy = d0 + ds < D && (RIGHT ? x0 + d0 + ds < W : xhi >= d0 + ds);
 
 #pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
-        mbar_wait(bars + c % ST, uint32_t(c / ST) & 1u);
+        const int st = c % ST;
+        mbar_wait(bars + st, uint32_t(c / ST) & 1u);
         if (busy) {
-        const uint32_t* sa = csm + (c % ST) * STAGE;
+        const uint32_t* sa = csm + st * STAGE;
         const uint32_t* sm = sa + SA;
         const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
 #pragma unroll 1
@@ -148,12 +169,17 @@ __global__ void __launch_bounds__(256, 2)
                 }
         }
         }
-        // release the slot; thread 0 refills it once all 8 warps are done
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + c % ST);
-        if (tid == 0 && c + ST < nchunks) {
-            mbar_wait(empty + c % ST, uint32_t(c / ST) & 1u);
-            load_stage(c + ST, c % ST);
+        if constexpr (LASTREFILL) {
+            // release the slot; the last of the 8 warps refills it
+            if (lane == 0 && c + ST < nchunks && (smem_arrive_count(ctr + st) & 7u) == 7u) load_stage(c + ST, st);
+        } else {
+            // release the slot; thread 0 refills it once all 8 warps are done
+            if (lane == 0) mbar_arrive(empty + st);
+            if (tid == 0 && c + ST < nchunks) {
+                mbar_wait(empty + st, uint32_t(c / ST) & 1u);
+                load_stage(c + ST, st);
+            }
         }
     }
 #pragma unroll
@@ -163,13 +189,12 @@ __global__ void __launch_bounds__(256, 2)
 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int x = x0 + xs + j;
+        const int x = xl + j;
         uint32_t best = 0xFFFFFFFFu;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            const int d = d0 + ds + s;
-            const int xo = RIGHT ? x + d : x - d;
-            const bool ok = d < D && x < W && xo >= 0 && xo < W;
+            const int d = dlo + s;
+            const bool ok = lane_in && x < W && d < D && (RIGHT ? x + d < W : x >= d);
             const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
             if (ok && key < best) best = key;
         }
@@ -180,10 +205,32 @@ __global__ void __launch_bounds__(256, 2)
         uint32_t best = red[tid];
 #pragma unroll
         for (int w = 1; w < 8; ++w) best = min(best, red[w * T + tid]);
-        const int x = x0 + tid;
-        if (x < W && best != 0xFFFFFFFFu) {
-            if (gridDim.x == 1) keys[size_t(y) * W + x] = best;
+        const int p = p0 + tid;
+        const int y = p / Wq, x = p - y * Wq;
+        if (p < npix && x < W && best != 0xFFFFFFFFu) {
+            if (!split) keys[size_t(y) * W + x] = best;
             else atomicMin(&keys[size_t(y) * W + x], best);
         }
     }
+}
+
+// blockIdx.x: pixel tile; blockIdx.y: d-block (+ dz for the second direction
+// when both run in this launch).  dir0: direction of blockIdx.y < dz
+// (0 = left reference, x - d; 1 = right reference, x + d).  The left-reference
+// maps / keys are l_*, keys_l; the right-reference ones r_*, keys_r.
+template <bool MASKED, bool LASTREFILL>
+__global__ void __launch_bounds__(256, 2)
+    k_cost_wta(const __grid_constant__ CUtensorMap l_ref, const __grid_constant__ CUtensorMap l_mask,
+               const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_ref,
+               const __grid_constant__ CUtensorMap r_mask, const __grid_constant__ CUtensorMap r_oth, int W, int Wq,
+               int rows, int NW, int D, int dz, int dir0, uint32_t* __restrict__ keys_l,
+               uint32_t* __restrict__ keys_r, uint32_t two) {
+    const int by = int(blockIdx.y);
+    const bool second = by >= dz;
+    const int dir = dir0 ^ (second ? 1 : 0);
+    const int d0 = (second ? by - dz : by) * kCostDisp;
+    if (dir)
+        cost_wta_tile<true, MASKED, LASTREFILL>(&r_ref, &r_mask, &r_oth, W, Wq, rows * Wq, NW, D, d0, dz > 1, keys_r, two);
+    else
+        cost_wta_tile<false, MASKED, LASTREFILL>(&l_ref, &l_mask, &l_oth, W, Wq, rows * Wq, NW, D, d0, dz > 1, keys_l, two);
 }

@@ -24,7 +24,7 @@ __device__ __forceinline__ uint32_t bytes_gt(uint32_t p, uint32_t q) {
 
 __global__ void __launch_bounds__(kD2TX* kD2TY)
     k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
-                  const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wp,
+                  const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wq, size_t P,
                   uint32_t* __restrict__ desc) {
     // tile: clamped bytes; t4[i] = bytes i..i+3 of the tile, so the 4 samples
     // of a thread's 4 pixels at any offset are one aligned 32-bit load.
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
             o.z = __byte_perm(t1, t3, 0x5410);
             o.w = __byte_perm(t1, t3, 0x7632);
             const int ly = ly0 + threadIdx.y * kD2Rows + r;
-            if (ly < rows) *reinterpret_cast<uint4*>(desc + (size_t(ly) * NW + w) * Wp + xq) = o;
+            if (ly < rows && xq < Wq) *reinterpret_cast<uint4*>(desc + size_t(w) * P + size_t(ly) * Wq + xq) = o;
         }
     }
 }
@@ -283,7 +283,7 @@ template <int MCH>
 __global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
-            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wp, uint32_t* __restrict__ mask) {
+            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
     constexpr int STG = mask4_stage_stride(MCH);
@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(32, 16)
     // 4-byte-aligned rows load whole words, the rest bytes with clamping.
     const int a0 = (x0 - half) & ~3, ay0 = y - half;
     const int sh = x0 - half - a0;
-    if ((W & 3) == 0 && a0 >= 0 && a0 + TW <= W && ay0 >= 0 && ay0 + TH <= H) {
+    if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(img) & 3) == 0 && a0 >= 0 && a0 + TW <= W && ay0 >= 0 &&
+        ay0 + TH <= H) {
         const int nw = TW >> 2;
         const uint32_t* src = reinterpret_cast<const uint32_t*>(img + size_t(ay0) * W + a0);
 #pragma unroll 4
@@ -398,9 +399,10 @@ __global__ void __launch_bounds__(32, 16)
     const int rem = n & 31;
     const uint32_t tail = rem ? (1u << rem) - 1u : ~0u;
     const int jl = lane & (kM3Px - 1), wl = lane / kM3Px;
-    uint32_t* dst = mask + (size_t(ly) * NW + wl) * Wp + x0 + jl;
+    if (x0 + jl >= Wq) return;
+    uint32_t* dst = mask + size_t(wl) * P + size_t(ly) * Wq + x0 + jl;
 #pragma unroll 4
-    for (int w = wl; w < NW; w += 32 / kM3Px, dst += size_t(32 / kM3Px) * Wp) {
+    for (int w = wl; w < NW; w += 32 / kM3Px, dst += size_t(32 / kM3Px) * P) {
         const uint32_t v = stage[jl * STG + w];
         *dst = w < G - 1 ? v : (w == G - 1 ? v & tail : 0u);
     }
@@ -438,7 +440,7 @@ constexpr int kDfTX = 32, kDfTY = 8, kDfPY = 4;
 
 __global__ void __launch_bounds__(kDfTX* kDfTY)
     k_descriptor_f32(const float* __restrict__ gray, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
-                     int n, int half, int NW, int Wp, uint32_t* __restrict__ desc) {
+                     int n, int half, int NW, int Wq, size_t P, uint32_t* __restrict__ desc) {
     extern __shared__ __align__(16) float ftile[];
     const int TW = kDfTX + 2 * half, TH = kDfTY * kDfPY + 2 * half;
     const int tid = threadIdx.y * kDfTX + threadIdx.x;
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(kDfTX* kDfTY)
 #pragma unroll
         for (int j = 0; j < kDfPY; ++j) {
             const int ly = ly0 + threadIdx.y * kDfPY + j;
-            if (ly < rows) desc[(size_t(ly) * NW + w) * Wp + x] = acc[j];
+            if (ly < rows && x < Wq) desc[size_t(w) * P + size_t(ly) * Wq + x] = acc[j];
         }
     }
 }
@@ -508,7 +510,7 @@ template <int MCH>
 __global__ void __launch_bounds__(32, 16)
     k_mask_f32(const float4* __restrict__ lab4, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
-               int NW, int Wp, uint32_t* __restrict__ mask, int half) {
+               int NW, int Wq, size_t P, uint32_t* __restrict__ mask, int half) {
     // Lab samples (float4 per pixel) are read through L1 (no shared tile):
     // shared memory holds only the slot keys and 24 rows of bit planes (the
     // low byte's planes reuse the rows of bits 8..15), for occupancy.
@@ -649,11 +651,11 @@ __global__ void __launch_bounds__(32, 16)
 #pragma unroll
         for (int m = 0; m < MCH; ++m) {
             const int w = MCH * lane + m;
-            if (w < NW) {
+            if (w < NW && x0 + px < Wq) {
                 uint32_t v = lt[m] | eq[m];
                 if (w >= G) v = 0u;
                 else if (rem && w == G - 1) v &= (1u << rem) - 1u;
-                mask[(size_t(ly) * NW + w) * Wp + x0 + px] = v;
+                mask[size_t(w) * P + size_t(ly) * Wq + x0 + px] = v;
             }
         }
         __syncwarp();

@@ -5,18 +5,20 @@
 
 // ---------------------------------------------------------------------------
 // Layout converters for the per-stage API (reference AoS u64 <-> device SoA).
-__global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+// Device field layout (see bsm_kernels.cu): word plane w at w * P, pixel
+// (x, y) of a plane at y * Wq + x (Wq = W rounded up to 4, P >= H * Wq).
+__global__ void k_aos_to_soa(const uint32_t* __restrict__ src, int W, int H, int NW, int Wq, size_t P,
                              uint32_t* __restrict__ dst) {
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, w, x)
-    const size_t total = size_t(H) * NW * Wp;
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (w, p)
+    const size_t total = size_t(NW) * P;
     if (i >= total) return;
-    const int x = int(i % Wp);
-    const size_t yw = i / Wp;
-    const int w = int(yw % NW), y = int(yw / NW);
-    dst[i] = x < W ? src[(size_t(y) * W + x) * NW + w] : 0u;
+    const size_t p = i % P;
+    const int w = int(i / P);
+    const int x = int(p % Wq), y = int(p / Wq);
+    dst[i] = (x < W && y < H) ? src[(size_t(y) * W + x) * NW + w] : 0u;
 }
 
-__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+__global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int NW, int Wq, size_t P,
                              uint32_t* __restrict__ dst) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
     const size_t total = size_t(H) * W * NW;
@@ -24,12 +26,12 @@ __global__ void k_soa_to_aos(const uint32_t* __restrict__ src, int W, int H, int
     const int w = int(i % NW);
     const size_t yx = i / NW;
     const int x = int(yx % W), y = int(yx / W);
-    dst[i] = src[(size_t(y) * NW + w) * Wp + x];
+    dst[i] = src[size_t(w) * P + size_t(y) * Wq + x];
 }
 
 // k_soa_to_aos with the pipeline's bit order undone: reference bit k of a
 // pixel's string is device bit pos[k].
-__global__ void k_soa_to_aos_perm(const uint32_t* __restrict__ src, int W, int H, int NW, int Wp,
+__global__ void k_soa_to_aos_perm(const uint32_t* __restrict__ src, int W, int H, int NW, int Wq, size_t P,
                                   const int* __restrict__ pos, int n, uint32_t* __restrict__ dst) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over (y, x, w)
     const size_t total = size_t(H) * W * NW;
@@ -40,7 +42,7 @@ __global__ void k_soa_to_aos_perm(const uint32_t* __restrict__ src, int W, int H
     uint32_t v = 0;
     for (int b = 0; b < 32 && 32 * w + b < n; ++b) {
         const int j = __ldg(pos + 32 * w + b);
-        v |= ((__ldg(src + (size_t(y) * NW + (j >> 5)) * Wp + x) >> (j & 31)) & 1u) << b;
+        v |= ((__ldg(src + size_t(j >> 5) * P + size_t(y) * Wq + x) >> (j & 31)) & 1u) << b;
     }
     dst[i] = v;
 }

@@ -31,9 +31,20 @@ def default_pairs(ref):
 
 
 @pytest.fixture(scope="session")
-def ctx():
+def _session_ctx():
     import paper_1402_2020_b200 as bsm
     return bsm.Context(0)
+
+
+@pytest.fixture
+def ctx(_session_ctx):
+    """The session's device context; under BSM_GUARD=1 (guarded device
+    buffers, see bsm_debug_check_guards) every test that used it must leave
+    all guard bytes intact."""
+    yield _session_ctx
+    if os.environ.get("BSM_GUARD") == "1":
+        damaged, on = _session_ctx.debug_check_guards()
+        assert on and damaged == 0, f"{damaged} guard bytes overwritten"
 
 
 def random_u8(h, w, seed):

@@ -113,8 +113,15 @@ static int gpu_run(const char* lpath, const char* rpath, int W, int H, int D, co
     CHECK(rw == res.right_wta);
     CHECK(chk == res.checked);
     CHECK(ref == res.refined);
-    CHECK(compute_descriptor(to_gray(left), pat, 3, 2) == fl.descriptor_at(3, 2));
-    CHECK(compute_mask(to_lab(left), pat, W - 1, H - 1) == fl.mask_at(W - 1, H - 1));
+    // single-pixel API (descriptor.hpp:174-196, O(n) window tiles) == the field,
+    // at corners, borders and the interior
+    const GrayImage gl = to_gray(left);
+    const LabImage ll = to_lab(left);
+    const int px[][2] = {{0, 0}, {W - 1, 0}, {0, H - 1}, {W - 1, H - 1}, {W / 2, H / 2}, {1, H / 2}, {W / 2, 1}, {3, 2}};
+    for (const auto& q : px) {
+        CHECK(compute_descriptor(gl, pat, q[0], q[1]) == fl.descriptor_at(q[0], q[1]));
+        CHECK(compute_mask(ll, pat, q[0], q[1]) == fl.mask_at(q[0], q[1]));
+    }
     std::ofstream o(out, std::ios::binary);
     for (const DisparityMap* m : {&res.refined, &res.left_wta, &res.right_wta, &res.checked, &*res.unmasked}) {
         o.write(reinterpret_cast<const char*>(m->disparity.data()), std::streamsize(m->disparity.size() * 4));
