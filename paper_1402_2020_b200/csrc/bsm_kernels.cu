@@ -165,7 +165,10 @@ struct bsm_ctx {
     cudaEvent_t ev[T_COUNT][kEvPerSlot][2] = {};
     int ev_used[T_COUNT] = {};
     int launches = 0;
-    int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction
+    int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
+    int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
+                     // bit 2 d-block-major CTA order, bit 3 groups of
+                     // 2 x SMs tiles
     DevBuf popc_out;
     // batch pipelining (bsm_pipeline_batch_u8): two slots of input views and
     // refined maps, an H2D and a D2H copy stream ordered by events
@@ -388,6 +391,18 @@ int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int
 // other = dr, keys -> keys_l; direction 1 (right reference, x + d): ref =
 // (dr, mr), other = dl, keys -> keys_r.  both: one launch for the two
 // directions; otherwise only direction `dir`.  ml/mr == nullptr: unmasked.
+// Tiles per CTA-order group of the cost kernel (see k_cost_wta).  Tile-major
+// (1) by default: measured on B200, it reads less DRAM
+// than the tile's words (the two directions and neighbouring d-blocks share
+// them through L2: 0.67x the algorithmic bytes at c2 and c4) and is within 2%
+// of the fastest order (d-block-major: c2 -1.8% time at 3x the DRAM bytes).
+int k3_group(const bsm_ctx* c, int tiles) {
+    if (c->k3_variant & 4) return tiles;                               // d-block-major
+    if (c->k3_variant & 8) return std::max(1, std::min(tiles, 2 * c->sm_count));  // one wave per d-block pass
+    if (c->k3_group > 0) return std::min(tiles, c->k3_group);
+    return 1;
+}
+
 int wta_device(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_t* dr, const uint32_t* mr, int W,
                int rows, int d_max, bool both, int dir, bool masked, uint32_t* keys_l, uint32_t* keys_r, int timing) {
     Scope s(c, timing);
@@ -399,9 +414,9 @@ int wta_device(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_
         if (use_r) BSM_CUDA(cudaMemsetAsync(keys_r, 0xFF, size_t(rows) * W * 4, c->stream));
     }
     const long long tiles = (static_cast<long long>(rows) * Wq + kCostTile - 1) / kCostTile;
-    if (tiles > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel grid");
-    if (dz * (both ? 2 : 1) > 65535) return set_err(BSM_UNSUPPORTED, "bsm: d_max too large for the cost kernel grid");
-    dim3 grid(unsigned(tiles), unsigned(dz * (both ? 2 : 1)));
+    const int ndd = dz * (both ? 2 : 1);
+    if (tiles * ndd > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel grid");
+    dim3 grid(unsigned(tiles * ndd));
     const size_t stage_words = size_t(masked ? 2 : 1) * kCostK * kCostTile + size_t(kCostK) * (kCostTile + kCostDisp);
     const size_t sm = (kCostStages * stage_words + 8 * kCostTile) * 4 + kCostStages * 16 + kCostStages * 4;
     CUtensorMap lr, lm, lo, rr, rm, ro;  // unused slots are copies of a valid map
@@ -415,7 +430,8 @@ int wta_device(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_
     BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, kCostTile + kCostDisp));
     auto launch = [&](auto kern) -> int {
         BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<grid, 256, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, rows, c->NW, d_max, dz, both ? 0 : dir,
+        kern<<<grid, 256, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, rows, c->NW, d_max, dz, ndd,
+                                           int(tiles), k3_group(c, int(tiles)), both ? 0 : dir,
                                            keys_l, keys_r, 2u);
         return BSM_OK;
     };
@@ -785,6 +801,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     bsm_ctx* c = new bsm_ctx();
     c->device = device;
     if (const char* v = std::getenv("BSM_K3_VARIANT")) c->k3_variant = std::atoi(v);
+    if (const char* v = std::getenv("BSM_K3_GROUP")) c->k3_group = std::atoi(v);
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;

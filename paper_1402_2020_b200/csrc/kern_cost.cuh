@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t smem_arrive_count(uint32_t* ctr) {
 template <bool RIGHT, bool MASKED, bool LASTREFILL>
 __device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const CUtensorMap* tm_mask,
                                               const CUtensorMap* tm_oth, int W, int Wq, int npix, int NW, int D,
-                                              int d0, bool split, uint32_t* __restrict__ keys, uint32_t two) {
+                                              int p0, int d0, bool split, uint32_t* __restrict__ keys, uint32_t two) {
     constexpr int T = kCostTile, DC = kCostDisp, K = kCostK, ST = kCostStages, BW = T + DC;
     constexpr int SA = K * T, SB = K * BW;
     constexpr int STAGE = (MASKED ? 2 * SA : SA) + SB;
@@ -84,7 +84,6 @@ __device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const C
     uint32_t* ctr = reinterpret_cast<uint32_t*>(bars + 2 * ST);        // [ST] slot-release counters
 
     const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-    const int p0 = blockIdx.x * T;
     const int bbase = RIGHT ? p0 + d0 : p0 - d0 - DC;
     const int nchunks = (NW + K - 1) / K;
     // this lane's 4 pixels: row yl, columns xl .. xl + 3
@@ -131,20 +130,20 @@ __device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const C
         const int st = c % ST;
         mbar_wait(bars + st, uint32_t(c / ST) & 1u);
         if (busy) {
-        const uint32_t* sa = csm + st * STAGE;
-        const uint32_t* sm = sa + SA;
-        const uint32_t* sb = sa + (MASKED ? 2 * SA : SA);
+        // lane pointers into the slot, advanced by two words per iteration
+        const uint32_t* pa = csm + st * STAGE + xs;
+        const uint32_t* pb = csm + st * STAGE + (MASKED ? 2 * SA : SA) + c0;
 #pragma unroll 1
-        for (int w = 0; w < K; w += 2) {
+        for (int w = 0; w < K; w += 2, pa += 2 * T, pb += 2 * BW) {
             uint32_t a[2][4], m[2][4], b[2][12];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const uint4 a4 = *reinterpret_cast<const uint4*>(sa + (w + h) * T + xs);
+                const uint4 a4 = *reinterpret_cast<const uint4*>(pa + h * T);
                 uint4 m4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(sm + (w + h) * T + xs);
-                const uint4 b0 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0);
-                const uint4 b1 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 4);
-                const uint4 b2 = *reinterpret_cast<const uint4*>(sb + (w + h) * BW + c0 + 8);
+                if constexpr (MASKED) m4 = *reinterpret_cast<const uint4*>(pa + SA + h * T);
+                const uint4 b0 = *reinterpret_cast<const uint4*>(pb + h * BW);
+                const uint4 b1 = *reinterpret_cast<const uint4*>(pb + h * BW + 4);
+                const uint4 b2 = *reinterpret_cast<const uint4*>(pb + h * BW + 8);
                 a[h][0] = a4.x; a[h][1] = a4.y; a[h][2] = a4.z; a[h][3] = a4.w;
                 m[h][0] = m4.x; m[h][1] = m4.y; m[h][2] = m4.z; m[h][3] = m4.w;
                 b[h][0] = b0.x; b[h][1] = b0.y; b[h][2] = b0.z; b[h][3] = b0.w;
@@ -187,18 +186,27 @@ __device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const C
 #pragma unroll
         for (int s = 0; s < 8; ++s) acc[j][s] += __popc(ones[j][s]);
 
+    // the epilogue's pixel coordinates are recomputed here (from a laundered
+    // lane index) rather than kept live through the word loop, whose 4 x 8
+    // cells already hold 128 registers
+    int lane2;
+    asm volatile("mov.u32 %0, %1;" : "=r"(lane2) : "r"(lane));
+    const int pe = p0 + lane2 * 4;
+    const int ye = pe / Wq, xe = pe - ye * Wq;
+    const bool lane_ok = pe < npix;
+    const int de = d0 + (tid >> 5) * 8;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int x = xl + j;
+        const int x = xe + j;
         uint32_t best = 0xFFFFFFFFu;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            const int d = dlo + s;
-            const bool ok = lane_in && x < W && d < D && (RIGHT ? x + d < W : x >= d);
+            const int d = de + s;
+            const bool ok = lane_ok && x < W && d < D && (RIGHT ? x + d < W : x >= d);
             const uint32_t key = (acc[j][s] << 16) | uint32_t(d);
             if (ok && key < best) best = key;
         }
-        red[wi * T + xs + j] = best;
+        red[(tid >> 5) * T + lane2 * 4 + j] = best;
     }
     __syncthreads();
     if (tid < T) {
@@ -214,8 +222,12 @@ __device__ __forceinline__ void cost_wta_tile(const CUtensorMap* tm_ref, const C
     }
 }
 
-// blockIdx.x: pixel tile; blockIdx.y: d-block (+ dz for the second direction
-// when both run in this launch).  dir0: direction of blockIdx.y < dz
+// 1-D grid over (tile, dd), ndd = dz (x 2 when both directions run in this
+// launch), in groups of `group` consecutive tiles: inside a group the order is
+// d-block-major, across groups tile-major (group = 1: tile-major, the default:
+// the d-blocks and both directions of a tile are launch-order neighbours, so
+// the tile's words are re-read from L2, not DRAM; group = tiles: d-major).
+// dd < dz: d-block dd of direction dir0; dd >= dz: d-block dd - dz of the other direction
 // (0 = left reference, x - d; 1 = right reference, x + d).  The left-reference
 // maps / keys are l_*, keys_l; the right-reference ones r_*, keys_r.
 template <bool MASKED, bool LASTREFILL>
@@ -223,14 +235,19 @@ __global__ void __launch_bounds__(256, 2)
     k_cost_wta(const __grid_constant__ CUtensorMap l_ref, const __grid_constant__ CUtensorMap l_mask,
                const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_ref,
                const __grid_constant__ CUtensorMap r_mask, const __grid_constant__ CUtensorMap r_oth, int W, int Wq,
-               int rows, int NW, int D, int dz, int dir0, uint32_t* __restrict__ keys_l,
+               int rows, int NW, int D, int dz, int ndd, int tiles, int group, int dir0, uint32_t* __restrict__ keys_l,
                uint32_t* __restrict__ keys_r, uint32_t two) {
-    const int by = int(blockIdx.y);
-    const bool second = by >= dz;
+    const unsigned span = unsigned(group) * unsigned(ndd), g = blockIdx.x / span, r = blockIdx.x % span;
+    const unsigned gsz = min(unsigned(group), unsigned(tiles) - g * unsigned(group));  // the last group may be short
+    const int tile = int(g * unsigned(group) + r % gsz), dd = int(r / gsz);
+    const bool second = dd >= dz;
     const int dir = dir0 ^ (second ? 1 : 0);
-    const int d0 = (second ? by - dz : by) * kCostDisp;
+    const int d0 = (second ? dd - dz : dd) * kCostDisp;
+    const int p0 = tile * kCostTile;
     if (dir)
-        cost_wta_tile<true, MASKED, LASTREFILL>(&r_ref, &r_mask, &r_oth, W, Wq, rows * Wq, NW, D, d0, dz > 1, keys_r, two);
+        cost_wta_tile<true, MASKED, LASTREFILL>(&r_ref, &r_mask, &r_oth, W, Wq, rows * Wq, NW, D, p0, d0, dz > 1,
+                                                keys_r, two);
     else
-        cost_wta_tile<false, MASKED, LASTREFILL>(&l_ref, &l_mask, &l_oth, W, Wq, rows * Wq, NW, D, d0, dz > 1, keys_l, two);
+        cost_wta_tile<false, MASKED, LASTREFILL>(&l_ref, &l_mask, &l_oth, W, Wq, rows * Wq, NW, D, p0, d0, dz > 1,
+                                                 keys_l, two);
 }
