@@ -1,8 +1,14 @@
-// tests/cpp/shim_io_driver.cpp -- TEST INFRASTRUCTURE: the same extern "C"
-// surface as oracle/ref_io_driver.cpp (prefix shimio_ instead of refio_), but
-// over this repository's C++ drop-in headers (include/bsm/image_io.hpp,
-// eval.hpp, config.hpp, pattern.hpp), so tests/test_cpp_shim.py can run the
-// reference's file/eval cases through both and compare outcomes byte for byte.
+// bsm_io_capi.cpp -- C ABI (include/bsm_io.h) of the host-side file and
+// evaluation layer either side of the matching path: this repository's C++
+// drop-in headers (include/bsm/image_io.hpp, eval.hpp, config.hpp,
+// pattern.hpp) are the single implementation; the Python modules io.py and
+// evaluation.py bind this library instead of re-implementing the formats.
+// The entry points mirror oracle/ref_io_driver.cpp (prefix refio_) one for
+// one, so the tests run the reference's own file/eval code and this layer side
+// by side.  Status codes: 0 ok, 1 InvalidArgument, 2 DimensionMismatch,
+// 9 other, 10 IoError, 11 FormatError, 12 EmptyRegion.
+#include "../../include/bsm_io.h"
+
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -33,38 +39,57 @@ bsm::DisparityMap map_from(const float* d, const uint8_t* v, int W, int H) {
 
 extern "C" {
 
-const char* shimio_last_error() { return g_err.c_str(); }
+const char* bsmio_last_error() { return g_err.c_str(); }
+
+// The last decoded image / disparity map of this thread, so the two-call
+// protocol (dimensions first, then pixels into a caller buffer) decodes once.
+thread_local std::string g_img_path, g_gt_path;
+thread_local double g_gt_scale = 0;
+thread_local bsm::RgbImage g_img;
+thread_local bsm::DisparityMap g_gt;
 
 // load_image (image_io.hpp:240-263): dims always; pixels when rgb != nullptr.
-int shimio_load_image(const char* path, int* w, int* h, uint8_t* rgb) {
+int bsmio_load_image(const char* path, int* w, int* h, uint8_t* rgb) {
     try {
-        const bsm::RgbImage img = bsm::load_image(path);
-        *w = img.width;
-        *h = img.height;
-        if (rgb)
-            for (size_t i = 0; i < img.pixels.size(); ++i) {
-                rgb[3 * i] = img.pixels[i].r;
-                rgb[3 * i + 1] = img.pixels[i].g;
-                rgb[3 * i + 2] = img.pixels[i].b;
-            }
+        if (!(rgb && g_img_path == path)) {
+            g_img_path.clear();
+            g_img = bsm::load_image(path);
+            g_img_path = path;
+        }
+        *w = g_img.width;
+        *h = g_img.height;
+        if (rgb) {
+            std::memcpy(rgb, g_img.pixels.data(), g_img.pixels.size() * 3);
+            g_img_path.clear();
+            g_img = bsm::RgbImage();
+        }
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }
 
 // load_gt_disparity (image_io.hpp:268-314).
-int shimio_load_gt(const char* path, double scale, int* w, int* h, float* d, uint8_t* v) {
+int bsmio_load_gt(const char* path, double scale, int* w, int* h, float* d, uint8_t* v) {
     try {
-        const bsm::DisparityMap m = bsm::load_gt_disparity(path, scale);
-        *w = m.width;
-        *h = m.height;
-        if (d) std::memcpy(d, m.disparity.data(), m.disparity.size() * 4);
-        if (v) std::memcpy(v, m.valid.data(), m.valid.size());
+        if (!((d || v) && g_gt_path == path && g_gt_scale == scale)) {
+            g_gt_path.clear();
+            g_gt = bsm::load_gt_disparity(path, scale);
+            g_gt_path = path;
+            g_gt_scale = scale;
+        }
+        *w = g_gt.width;
+        *h = g_gt.height;
+        if (d) std::memcpy(d, g_gt.disparity.data(), g_gt.disparity.size() * 4);
+        if (v) std::memcpy(v, g_gt.valid.data(), g_gt.valid.size());
+        if (d || v) {
+            g_gt_path.clear();
+            g_gt = bsm::DisparityMap();
+        }
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }
 
 // save_disparity (:317-337) or save_disparity_pfm (:340-355).
-int shimio_save_disparity(const char* path, const float* d, const uint8_t* v, int W, int H, double scale, int pfm) {
+int bsmio_save_disparity(const char* path, const float* d, const uint8_t* v, int W, int H, double scale, int pfm) {
     try {
         const bsm::DisparityMap m = map_from(d, v, W, H);
         if (pfm) bsm::save_disparity_pfm(m, path);
@@ -74,7 +99,7 @@ int shimio_save_disparity(const char* path, const float* d, const uint8_t* v, in
 }
 
 // save_gray_pgm (:358-371) and save_ppm (:373-382).
-int shimio_save_gray_pgm(const char* path, const float* g, int W, int H) {
+int bsmio_save_gray_pgm(const char* path, const float* g, int W, int H) {
     try {
         bsm::GrayImage img(W, H);
         std::memcpy(img.values.data(), g, size_t(W) * H * 4);
@@ -83,7 +108,7 @@ int shimio_save_gray_pgm(const char* path, const float* g, int W, int H) {
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_save_ppm(const char* path, const uint8_t* rgb, int W, int H) {
+int bsmio_save_ppm(const char* path, const uint8_t* rgb, int W, int H) {
     try {
         bsm::RgbImage img(W, H);
         for (size_t i = 0; i < img.pixels.size(); ++i) img.pixels[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
@@ -93,7 +118,7 @@ int shimio_save_ppm(const char* path, const uint8_t* rgb, int W, int H) {
 }
 
 // save_config / load_config (config.hpp:81-110); ints: n S seed d_max radius threads, doubles: spread lc le tol gt_scale.
-int shimio_save_config(const char* path, const int64_t* iv, const double* dv, const char* generator) {
+int bsmio_save_config(const char* path, const int64_t* iv, const double* dv, const char* generator) {
     try {
         bsm::BsmConfig c;
         c.n = int(iv[0]);
@@ -113,7 +138,7 @@ int shimio_save_config(const char* path, const int64_t* iv, const double* dv, co
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_load_config(const char* path, int64_t* iv, double* dv, char* generator, int gen_cap) {
+int bsmio_load_config(const char* path, int64_t* iv, double* dv, char* generator, int gen_cap) {
     try {
         const bsm::BsmConfig c = bsm::load_config(path);
         iv[0] = c.n;
@@ -134,7 +159,7 @@ int shimio_load_config(const char* path, int64_t* iv, double* dv, char* generato
 }
 
 // save_pattern / load_pattern (pattern.hpp:104-160).
-int shimio_save_pattern(const char* path, const int16_t* pairs, int n, int window, double spread, uint64_t seed) {
+int bsmio_save_pattern(const char* path, const int16_t* pairs, int n, int window, double spread, uint64_t seed) {
     try {
         bsm::SamplingPattern p;
         p.n = n;
@@ -149,7 +174,7 @@ int shimio_save_pattern(const char* path, const int16_t* pairs, int n, int windo
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_load_pattern(const char* path, int* n, int* window, double* spread, uint64_t* seed, int16_t* pairs,
+int bsmio_load_pattern(const char* path, int* n, int* window, double* spread, uint64_t* seed, int16_t* pairs,
                        int cap) {
     try {
         const bsm::SamplingPattern p = bsm::load_pattern(path);
@@ -169,7 +194,7 @@ int shimio_load_pattern(const char* path, int* n, int* window, double* spread, u
 }
 
 // bad_pixel_rate (eval.hpp:31-59); region may be null.
-int shimio_bad_pixel_rate(const float* d, const uint8_t* v, const float* gd, const uint8_t* gv, const float* region,
+int bsmio_bad_pixel_rate(const float* d, const uint8_t* v, const float* gd, const uint8_t* gv, const float* region,
                          int W, int H, double threshold, double* rate, long* counted, long* bad) {
     try {
         const bsm::DisparityMap r = map_from(d, v, W, H), g = map_from(gd, gv, W, H);
@@ -186,14 +211,14 @@ int shimio_bad_pixel_rate(const float* d, const uint8_t* v, const float* gd, con
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_linear_fit_r2(const double* xs, const double* ys, int n, double* out) {
+int bsmio_linear_fit_r2(const double* xs, const double* ys, int n, double* out) {
     try {
         *out = bsm::linear_fit_r2(std::vector<double>(xs, xs + n), std::vector<double>(ys, ys + n));
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_write_sweep_csv(const char* path, const int* n, const double* err, const double* secs, int count) {
+int bsmio_write_sweep_csv(const char* path, const int* n, const double* err, const double* secs, int count) {
     try {
         std::vector<bsm::SweepPoint> pts(static_cast<size_t>(count));
         for (int i = 0; i < count; ++i) pts[size_t(i)] = {n[i], err[i], secs[i]};
@@ -202,7 +227,7 @@ int shimio_write_sweep_csv(const char* path, const int* n, const double* err, co
     } catch (const std::exception& e) { return fail(e); }
 }
 
-int shimio_write_radiometric_csv(const char* path, const double* rate9, double* diag, double* off) {
+int bsmio_write_radiometric_csv(const char* path, const double* rate9, double* diag, double* off) {
     try {
         bsm::RadiometricMatrix m;
         for (int i = 0; i < 9; ++i) m.rate[size_t(i / 3)][size_t(i % 3)] = rate9[i];

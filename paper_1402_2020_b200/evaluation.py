@@ -2,12 +2,15 @@
 
 ``bad_pixel_rate`` (eval.hpp:31-59), the 3x3 ``radiometric_protocol``
 (:63-92), the descriptor ``length_sweep`` (:94-139), ``time_pipeline``
-(:144-159), ``linear_fit_r2`` (:163-187) and the CSV writers (:189-211), with
-the reference's arithmetic order and messages.  Every disparity map comes from
-``run_pipeline`` on the device; the scoring itself is a host reduction.
+(:144-159), ``linear_fit_r2`` (:163-187) and the CSV writers (:189-211).  The
+scoring, the fit and the CSV files are the C++ layer's (include/bsm/eval.hpp
+through libbsm_io.so, the reference's arithmetic order and messages); the
+protocols here drive ``run_pipeline`` on the device.
 """
 from __future__ import annotations
 
+import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -15,12 +18,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import BsmConfig, DisparityMap, SamplingPattern, generate_pattern, run_pipeline
-from ._lib import BsmError, DimensionMismatch, InvalidArgument
-from .io import IoError
-
-
-class EmptyRegion(BsmError):
-    """bsm::EmptyRegion (errors.hpp:30-33): no counted pixels in the region."""
+from ._lib import DimensionMismatch, InvalidArgument
+from .io import EmptyRegion, IoError, check, lib  # noqa: F401  (EmptyRegion: errors.hpp:30-33)
 
 
 @dataclass
@@ -42,17 +41,16 @@ def bad_pixel_rate(result: DisparityMap, gt: DisparityMap, region: Optional[np.n
         raise DimensionMismatch("bad_pixel_rate: result and ground truth differ in size")
     if region is not None and np.asarray(region).shape != gt.disparity.shape:
         raise DimensionMismatch("bad_pixel_rate: region mask size mismatch")
-    if not threshold > 0.0:
-        raise InvalidArgument("bad_pixel_rate: threshold must be > 0")
-    sel = gt.valid != 0
-    if region is not None:
-        sel &= ~(np.asarray(region, np.float32) < np.float32(128.0))
-    counted = int(sel.sum())
-    err = np.abs(result.disparity.astype(np.float64) - gt.disparity.astype(np.float64))
-    bad = int((sel & ((result.valid == 0) | (err > threshold))).sum())
-    if counted == 0:
-        raise EmptyRegion("bad_pixel_rate: no pixels with ground truth in region")
-    return ErrorReport(100.0 * float(bad) / float(counted), "all", float(threshold), counted, bad)
+    f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+    u8 = lambda a: np.ascontiguousarray(a, dtype=np.uint8)
+    d, v, gd, gv = f32(result.disparity), u8(result.valid), f32(gt.disparity), u8(gt.valid)
+    reg = f32(region) if region is not None else None
+    rate, counted, bad = C.c_double(), C.c_long(), C.c_long()
+    H, W = d.shape
+    check(lib().bsmio_bad_pixel_rate(d.ctypes.data, v.ctypes.data, gd.ctypes.data, gv.ctypes.data,
+                                     reg.ctypes.data if reg is not None else None, W, H, float(threshold),
+                                     C.byref(rate), C.byref(counted), C.byref(bad)))
+    return ErrorReport(rate.value, "all", float(threshold), counted.value, bad.value)
 
 
 @dataclass
@@ -144,49 +142,26 @@ def time_pipeline(left, right, pattern: SamplingPattern, cfg: BsmConfig, runs: i
 
 
 def linear_fit_r2(xs: Sequence[float], ys: Sequence[float]) -> float:
-    """linear_fit_r2 (eval.hpp:163-187), same summation order."""
-    if len(xs) != len(ys) or len(xs) < 2:
+    """linear_fit_r2 (eval.hpp:163-187)."""
+    x = np.ascontiguousarray(xs, dtype=np.float64)
+    y = np.ascontiguousarray(ys, dtype=np.float64)
+    if x.shape != y.shape:
         raise InvalidArgument("linear_fit_r2: need two or more points")
-    n = float(len(xs))
-    sx = sy = sxx = sxy = 0.0
-    for x, y in zip(xs, ys):
-        x, y = float(x), float(y)
-        sx += x
-        sy += y
-        sxx += x * x
-        sxy += x * y
-    denom = n * sxx - sx * sx
-    if denom == 0.0:
-        raise InvalidArgument("linear_fit_r2: x values are all equal")
-    slope = (n * sxy - sx * sy) / denom
-    intercept = (sy - slope * sx) / n
-    ss_res = ss_tot = 0.0
-    mean_y = sy / n
-    for x, y in zip(xs, ys):
-        x, y = float(x), float(y)
-        fit = slope * x + intercept
-        ss_res += (y - fit) * (y - fit)
-        ss_tot += (y - mean_y) * (y - mean_y)
-    if ss_tot == 0.0:
-        return 1.0 if ss_res == 0.0 else 0.0
-    return 1.0 - ss_res / ss_tot
-
-
-def _write_text(path: str, text: str) -> None:
-    try:
-        with open(path, "w", newline="\n") as f:
-            f.write(text)
-    except OSError:
-        raise IoError(f"cannot open {path} for writing") from None
+    out = C.c_double()
+    check(lib().bsmio_linear_fit_r2(x.ctypes.data, y.ctypes.data, int(x.size), C.byref(out)))
+    return out.value
 
 
 def write_sweep_csv(path: str, points: Sequence[SweepPoint]) -> None:
     """write_sweep_csv (eval.hpp:189-198)."""
-    _write_text(path, "n,avg_error,wall_time\n" +
-                "".join("%d,%.6f,%.4f\n" % (p.n, p.avg_error, p.wall_time) for p in points))
+    n = np.ascontiguousarray([p.n for p in points], dtype=np.int32)
+    e = np.ascontiguousarray([p.avg_error for p in points], dtype=np.float64)
+    t = np.ascontiguousarray([p.wall_time for p in points], dtype=np.float64)
+    check(lib().bsmio_write_sweep_csv(os.fsencode(path), n.ctypes.data, e.ctypes.data, t.ctypes.data, len(points)))
 
 
 def write_radiometric_csv(path: str, m: RadiometricMatrix) -> None:
     """write_radiometric_csv (eval.hpp:200-211)."""
-    _write_text(path, "left_condition,right_condition,bad_pixel_rate\n" +
-                "".join("%d,%d,%.6f\n" % (i, j, m.rate[i][j]) for i in range(3) for j in range(3)))
+    r = np.ascontiguousarray(m.rate, dtype=np.float64).reshape(9)
+    diag, off = C.c_double(), C.c_double()
+    check(lib().bsmio_write_radiometric_csv(os.fsencode(path), r.ctypes.data, C.byref(diag), C.byref(off)))

@@ -1,6 +1,8 @@
 """Data formats either side of the matching path.
 
-Host-side mirror of the reference's file layer, same behaviour and messages:
+Python binding of the file layer implemented once, in C++ (include/bsm/
+image_io.hpp, config.hpp, pattern.hpp; C ABI include/bsm_io.h in
+``libbsm_io.so``) -- the same behaviour and messages as the reference:
 
 * image_io.hpp -- ``load_image`` (PGM P2/P5, PPM P3/P6 at 8/16 bits, PNG),
   ``load_gt_disparity`` (16-bit PGM / PFM / 8-bit gray PNG), ``save_disparity``
@@ -8,31 +10,27 @@ Host-side mirror of the reference's file layer, same behaviour and messages:
   +inf = invalid), ``save_gray_pgm``, ``save_ppm``;
 * JSON sidecars -- ``save_config`` / ``load_config`` (config.hpp:48-110) and
   ``save_pattern`` / ``load_pattern`` (pattern.hpp:104-160), byte-identical to
-  nlohmann's ``dump(1, '\\t')`` (sorted keys, tab indent);
+  the reference's nlohmann ``dump(1, '\\t')``;
 * dataset.hpp -- ``load_stereo_dataset``, ``discover_middlebury``,
-  ``load_radiometric_set`` (stock Middlebury file names).
+  ``load_radiometric_set`` (stock Middlebury file names), composed here from
+  the readers.
 
-PNG: libpng's simplified read API is restated for the variants a stereo
-dataset uses (8-bit gray, RGB and palette, non-interlaced); other variants
+PNG: 8-bit gray, RGB and palette, non-interlaced (zlib); other variants
 (16-bit, alpha, interlaced, colour-to-gray) raise FormatError.  Images are
 returned as (H, W, 3) uint8 RGB like the reference's RgbImage; ``run_pipeline``
 takes grayscale (r = g = b) views on the uint8 path automatically.
 """
 from __future__ import annotations
 
-import json
-import math
+import ctypes as C
 import os
-import struct
-import sys
-import zlib
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
 import numpy as np
 
-from . import GENERATOR_NAME, BsmConfig, DisparityMap, SamplingPattern
-from ._lib import BsmError, InvalidArgument
+from . import BsmConfig, DisparityMap, SamplingPattern
+from ._lib import BsmError, DimensionMismatch, InvalidArgument
 
 
 class IoError(BsmError):
@@ -43,394 +41,152 @@ class FormatError(BsmError):
     """bsm::FormatError (errors.hpp:17-20): corrupt header or truncated payload."""
 
 
-_SPACE = b" \t\n\v\f\r"
+class EmptyRegion(BsmError):
+    """bsm::EmptyRegion (eval.hpp): no pixel of the evaluation region has ground truth."""
 
 
-def _read_file(path: str) -> bytes:
-    try:
-        with open(path, "rb") as f:
-            return f.read()
-    except OSError:
-        raise IoError(f"cannot open {path}") from None
+IO_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbsm_io.so")
+_P, _I, _D = C.c_void_p, C.c_int, C.c_double
+_SIGS = {
+    "bsmio_load_image": [C.c_char_p, C.POINTER(_I), C.POINTER(_I), _P],
+    "bsmio_load_gt": [C.c_char_p, _D, C.POINTER(_I), C.POINTER(_I), _P, _P],
+    "bsmio_save_disparity": [C.c_char_p, _P, _P, _I, _I, _D, _I],
+    "bsmio_save_gray_pgm": [C.c_char_p, _P, _I, _I],
+    "bsmio_save_ppm": [C.c_char_p, _P, _I, _I],
+    "bsmio_save_config": [C.c_char_p, _P, _P, C.c_char_p],
+    "bsmio_load_config": [C.c_char_p, _P, _P, C.c_char_p, _I],
+    "bsmio_save_pattern": [C.c_char_p, _P, _I, _I, _D, C.c_uint64],
+    "bsmio_load_pattern": [C.c_char_p, C.POINTER(_I), C.POINTER(_I), C.POINTER(_D), C.POINTER(C.c_uint64), _P, _I],
+    "bsmio_bad_pixel_rate": [_P, _P, _P, _P, _P, _I, _I, _D, C.POINTER(_D), C.POINTER(C.c_long),
+                             C.POINTER(C.c_long)],
+    "bsmio_linear_fit_r2": [_P, _P, _I, C.POINTER(_D)],
+    "bsmio_write_sweep_csv": [C.c_char_p, _P, _P, _P, _I],
+    "bsmio_write_radiometric_csv": [C.c_char_p, _P, C.POINTER(_D), C.POINTER(_D)],
+}
+_io = None
 
 
-class _Cursor:
-    """PnmCursor (image_io.hpp:33-78): whitespace tokens, '#' comments."""
-
-    def __init__(self, data: bytes):
-        self.data = data
-        self.pos = 0
-
-    def skip(self):
-        d, n = self.data, len(self.data)
-        while self.pos < n:
-            c = d[self.pos]
-            if c == 0x23:  # '#'
-                while self.pos < n and d[self.pos] != 0x0A:
-                    self.pos += 1
-            elif c in _SPACE:
-                self.pos += 1
-            else:
-                break
-
-    def token(self, what: str) -> str:
-        self.skip()
-        d, n = self.data, len(self.data)
-        start = self.pos
-        while self.pos < n and d[self.pos] not in _SPACE and d[self.pos] != 0x23:
-            self.pos += 1
-        if self.pos == start:
-            raise FormatError(f"missing {what} in PNM header")
-        return d[start:self.pos].decode("latin-1")
-
-    def int_token(self, what: str) -> int:
-        t = self.token(what)
-        s = t[1:] if t[:1] in "+-" else t
-        if not s or not s.isdigit() or not s.isascii():
-            if s[:1].isdigit():  # std::stol parsed a prefix: "bad <what> in PNM header"
-                raise FormatError(f"bad {what} in PNM header")
-            raise FormatError(f"bad {what} '{t}' in PNM header")
-        return int(t)
-
-    def expect_single_space(self):
-        if self.pos >= len(self.data) or self.data[self.pos] not in _SPACE:
-            raise FormatError("missing separator before PNM payload")
-        self.pos += 1
+def lib() -> C.CDLL:
+    """Load libbsm_io.so (built with the product by __graft_entry__.build())."""
+    global _io
+    if _io is None:
+        if not os.path.exists(IO_PATH):
+            raise BsmError(f"{IO_PATH} is missing: run __graft_entry__.build()")
+        L = C.CDLL(IO_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.bsmio_last_error.argtypes = []
+        L.bsmio_last_error.restype = C.c_char_p
+        _io = L
+    return _io
 
 
-def _pnm_header(cur: _Cursor):
-    magic = cur.token("magic")
-    if len(magic) != 2 or magic[0] != "P" or magic[1] not in "2356":
-        raise FormatError(f"unsupported PNM magic '{magic}'")
-    w = cur.int_token("width")
-    h = cur.int_token("height")
-    maxval = cur.int_token("maxval")
-    if w < 1 or h < 1 or w > (1 << 20) or h > (1 << 20):
-        raise FormatError("bad PNM dimensions")
-    if maxval < 1 or maxval > 65535:
-        raise FormatError("bad PNM maxval")
-    return magic[1], w, h, maxval
+_EXC = {1: InvalidArgument, 2: DimensionMismatch, 10: IoError, 11: FormatError, 12: EmptyRegion}
 
 
-def _pnm_samples(cur: _Cursor, magic: str, w: int, h: int, maxval: int, channels: int) -> np.ndarray:
-    count = w * h * channels
-    if magic in "23":
-        out = np.empty(count, np.uint16)
-        for i in range(count):
-            v = cur.int_token("sample")
-            if v < 0 or v > maxval:
-                raise FormatError("PNM sample out of range")
-            out[i] = v
-        return out
-    cur.expect_single_space()
-    nbytes = 2 if maxval > 255 else 1
-    if len(cur.data) - cur.pos < count * nbytes:
-        raise FormatError("truncated PNM payload")
-    raw = np.frombuffer(cur.data, np.uint8, count * nbytes, cur.pos)
-    cur.pos += count * nbytes
-    if nbytes == 1:
-        return raw.astype(np.uint16)
-    return raw.view(">u2").astype(np.uint16)  # big-endian samples
+def check(rc: int) -> None:
+    if rc:
+        raise _EXC.get(rc, BsmError)(lib().bsmio_last_error().decode(errors="replace"))
 
 
-def _to_8bit(v: np.ndarray, maxval: int) -> np.ndarray:
-    if maxval == 255:
-        return v.astype(np.uint8)
-    return ((v.astype(np.int64) * 255 + maxval // 2) // maxval).astype(np.uint8)
+def _b(path: str) -> bytes:
+    return os.fsencode(path)
 
 
-# ---------------------------------------------------------------------------
-# PNG (restated subset of libpng's simplified read API)
-_PNG_SIG = b"\x89PNG\r\n\x1a\n"
-
-
-def _png_decode(data: bytes, path: str, want_rgb: bool) -> np.ndarray:
-    def bad(msg):
-        return FormatError(f"bad PNG {path}: {msg}")
-
-    pos = 8
-    ihdr = None
-    plte = None
-    idat = []
-    while pos + 8 <= len(data):
-        ln, typ = struct.unpack(">I4s", data[pos:pos + 8])
-        body = data[pos + 8:pos + 8 + ln]
-        if len(body) != ln or pos + 12 + ln > len(data):
-            raise bad("truncated chunk")
-        crc = struct.unpack(">I", data[pos + 8 + ln:pos + 12 + ln])[0]
-        if zlib.crc32(typ + body) & 0xFFFFFFFF != crc:
-            raise bad("CRC error")
-        if typ == b"IHDR":
-            ihdr = struct.unpack(">IIBBBBB", body)
-        elif typ == b"PLTE":
-            plte = np.frombuffer(body, np.uint8).reshape(-1, 3)
-        elif typ == b"IDAT":
-            idat.append(body)
-        elif typ == b"IEND":
-            break
-        pos += 12 + ln
-    if ihdr is None or not idat:
-        raise bad("missing IHDR/IDAT")
-    w, h, depth, ctype, comp, filt, interlace = ihdr
-    if w < 1 or h < 1 or comp != 0 or filt != 0:
-        raise bad("invalid IHDR")
-    if depth != 8 or ctype not in (0, 2, 3) or interlace != 0:
-        raise bad("unsupported PNG variant (this build reads 8-bit gray/RGB/palette, non-interlaced)")
-    if ctype == 3 and plte is None:
-        raise bad("palette image without PLTE")
-    bpp = {0: 1, 2: 3, 3: 1}[ctype]
-    try:
-        raw = zlib.decompress(b"".join(idat))
-    except zlib.error as e:
-        raise bad(str(e)) from None
-    stride = w * bpp
-    if len(raw) < h * (stride + 1):
-        raise bad("truncated image data")
-    img = np.zeros((h, stride), np.uint8)
-    prev = np.zeros(stride, np.int32)
-    for y in range(h):
-        ft = raw[y * (stride + 1)]
-        line = np.frombuffer(raw, np.uint8, stride, y * (stride + 1) + 1).astype(np.int32)
-        if ft == 0:
-            cur = line
-        elif ft == 2:
-            cur = (line + prev) & 255
-        elif ft == 1:
-            cur = (np.cumsum(line.reshape(w, bpp), axis=0) & 255).reshape(-1)
-        elif ft in (3, 4):
-            cur = np.zeros(stride, np.int32)
-            for x in range(stride):
-                a = cur[x - bpp] if x >= bpp else 0
-                b = prev[x]
-                if ft == 3:
-                    p = (a + b) >> 1
-                else:
-                    c = prev[x - bpp] if x >= bpp else 0
-                    pa, pb, pc = abs(b - c), abs(a - c), abs(a + b - 2 * c)
-                    p = a if (pa <= pb and pa <= pc) else (b if pb <= pc else c)
-                cur[x] = (line[x] + p) & 255
-        else:
-            raise bad("bad filter type")
-        img[y] = cur
-        prev = cur
-    if ctype == 3:
-        idx = img.reshape(h, w)
-        if idx.max(initial=0) >= len(plte):
-            raise bad("palette index out of range")
-        rgb = plte[idx]
-        if not want_rgb:
-            raise bad("colour-to-gray conversion is not supported by this build")
-        return rgb
-    if ctype == 2:
-        if not want_rgb:
-            raise bad("colour-to-gray conversion is not supported by this build")
-        return img.reshape(h, w, 3)
-    g = img.reshape(h, w)
-    return np.repeat(g[:, :, None], 3, axis=2) if want_rgb else g
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
 
 
 # ---------------------------------------------------------------------------
 # image_io.hpp
 def load_image(path: str) -> np.ndarray:
-    """load_image (image_io.hpp:240-263): (H, W, 3) uint8 RGB; gray sources give r = g = b."""
-    data = _read_file(path)
-    if not data:
-        raise FormatError(f"empty file {path}")
-    if data[:8] == _PNG_SIG:
-        return _png_decode(data, path, want_rgb=True)
-    cur = _Cursor(data)
-    magic, w, h, maxval = _pnm_header(cur)
-    color = magic in "36"
-    s = _to_8bit(_pnm_samples(cur, magic, w, h, maxval, 3 if color else 1), maxval)
-    if color:
-        return s.reshape(h, w, 3)
-    g = s.reshape(h, w)
-    return np.repeat(g[:, :, None], 3, axis=2)
-
-
-def _parse_pfm(data: bytes, path: str):
-    cur = _Cursor(data)
-    magic = cur.token("magic")
-    if magic not in ("Pf", "PF"):
-        raise FormatError(f"bad PFM magic in {path}")
-    ch = 3 if magic == "PF" else 1
-    w = cur.int_token("width")
-    h = cur.int_token("height")
-    if w < 1 or h < 1 or w > (1 << 20) or h > (1 << 20):
-        raise FormatError(f"bad PFM dimensions in {path}")
-    tok = cur.token("scale")
-    try:
-        scale = float(tok)
-    except ValueError:
-        raise FormatError(f"bad PFM scale in {path}") from None
-    if scale == 0:
-        raise FormatError(f"bad PFM scale in {path}")
-    cur.expect_single_space()
-    count = w * h * ch
-    if len(data) - cur.pos < count * 4:
-        raise FormatError(f"truncated PFM payload in {path}")
-    vals = np.frombuffer(data, ">f4" if scale > 0 else "<f4", count, cur.pos).astype(np.float32)
-    return w, h, ch, vals.reshape(h, w * ch)[::-1].reshape(-1)  # rows are stored bottom-up
+    """load_image (image_io.hpp:240-263): (H, W, 3) uint8 RGB; gray sources
+    expand to r = g = b, 16-bit samples rescale to 8 bits."""
+    w, h = C.c_int(), C.c_int()
+    check(lib().bsmio_load_image(_b(path), C.byref(w), C.byref(h), None))
+    out = np.empty((h.value, w.value, 3), np.uint8)
+    check(lib().bsmio_load_image(_b(path), C.byref(w), C.byref(h), _ptr(out)))
+    return out
 
 
 def load_gt_disparity(path: str, scale: float) -> DisparityMap:
     """load_gt_disparity (image_io.hpp:268-314): stored value / scale; PGM 0 and
     non-finite PFM values are unknown."""
-    if not scale > 0:
-        raise InvalidArgument("disparity scale must be > 0")
-    data = _read_file(path)
-    if not data:
-        raise FormatError(f"empty file {path}")
-    if len(data) >= 2 and data[0] == 0x50 and data[1] in (0x66, 0x46):
-        w, h, ch, vals = _parse_pfm(data, path)
-        if ch != 1:
-            raise FormatError(f"disparity PFM must be grayscale: {path}")
-        fin = np.isfinite(vals)
-        d = np.where(fin, (vals.astype(np.float64) / scale).astype(np.float32), np.float32(0)).astype(np.float32)
-        return DisparityMap(d.reshape(h, w), fin.astype(np.uint8).reshape(h, w))
-    if data[:8] == _PNG_SIG:
-        stored = _png_decode(data, path, want_rgb=False).astype(np.uint16)
-        h, w = stored.shape
-        stored = stored.reshape(-1)
-    else:
-        cur = _Cursor(data)
-        magic, w, h, maxval = _pnm_header(cur)
-        if magic in "36":
-            raise FormatError(f"disparity PGM must be grayscale: {path}")
-        stored = _pnm_samples(cur, magic, w, h, maxval, 1)
-    ok = stored != 0
-    d = np.where(ok, (stored.astype(np.float64) / scale).astype(np.float32), np.float32(0)).astype(np.float32)
-    return DisparityMap(d.reshape(h, w), ok.astype(np.uint8).reshape(h, w))
+    w, h = C.c_int(), C.c_int()
+    check(lib().bsmio_load_gt(_b(path), float(scale), C.byref(w), C.byref(h), None, None))
+    d = np.empty((h.value, w.value), np.float32)
+    v = np.empty((h.value, w.value), np.uint8)
+    check(lib().bsmio_load_gt(_b(path), float(scale), C.byref(w), C.byref(h), _ptr(d), _ptr(v)))
+    return DisparityMap(d, v)
 
 
-def _write(path: str, payload: bytes) -> None:
-    try:
-        with open(path, "wb") as f:
-            f.write(payload)
-    except OSError:
-        raise IoError(f"cannot open {path} for writing") from None
-
-
-def _round_half_away(x: np.ndarray) -> np.ndarray:
-    """std::round / std::lround: nearest, halves away from zero (exact: trunc + fraction test)."""
-    t = np.trunc(x)
-    return t + np.sign(x) * (np.abs(x - t) >= 0.5)
+def _map(m: DisparityMap):
+    return (np.ascontiguousarray(m.disparity, dtype=np.float32), np.ascontiguousarray(m.valid, dtype=np.uint8))
 
 
 def save_disparity(m: DisparityMap, path: str, scale: float) -> None:
-    """save_disparity (image_io.hpp:317-337): 16-bit PGM of lround(d * scale), invalid = 0."""
-    if scale <= 0:
-        raise InvalidArgument("disparity scale must be > 0")
-    v = _round_half_away(m.disparity.astype(np.float64) * float(scale))
-    v = np.clip(v, 0, 65535)
-    v = np.where(m.valid != 0, v, 0).astype(">u2")
-    _write(path, f"P5\n{m.width} {m.height}\n65535\n".encode() + v.tobytes())
+    """save_disparity (image_io.hpp:317-337): 16-bit PGM of round(d * scale), 0 = invalid."""
+    d, v = _map(m)
+    check(lib().bsmio_save_disparity(_b(path), _ptr(d), _ptr(v), d.shape[1], d.shape[0], float(scale), 0))
 
 
 def save_disparity_pfm(m: DisparityMap, path: str) -> None:
-    """save_disparity_pfm (image_io.hpp:340-355): grayscale PFM, bottom-up, +inf invalid."""
-    big = sys.byteorder == "big"
-    d = np.where(m.valid != 0, m.disparity, np.float32(np.inf)).astype(np.float32)
-    hdr = f"Pf\n{m.width} {m.height}\n{'1.0' if big else '-1.0'}\n".encode()
-    _write(path, hdr + np.ascontiguousarray(d[::-1]).astype("=f4").tobytes())
+    """save_disparity_pfm (image_io.hpp:340-355): bottom-up float, +inf = invalid."""
+    d, v = _map(m)
+    check(lib().bsmio_save_disparity(_b(path), _ptr(d), _ptr(v), d.shape[1], d.shape[0], 1.0, 1))
 
 
 def save_gray_pgm(gray: np.ndarray, path: str) -> None:
-    """save_gray_pgm (image_io.hpp:358-371): 8-bit PGM of round(v) clamped to [0, 255]."""
-    g = np.asarray(gray, np.float32)
-    h, w = g.shape
-    r = np.clip(_round_half_away(g), 0, 255).astype(np.uint8)
-    _write(path, f"P5\n{w} {h}\n255\n".encode() + r.tobytes())
+    """save_gray_pgm (image_io.hpp:358-371)."""
+    g = np.ascontiguousarray(gray, dtype=np.float32)
+    check(lib().bsmio_save_gray_pgm(_b(path), _ptr(g), g.shape[1], g.shape[0]))
 
 
 def save_ppm(rgb: np.ndarray, path: str) -> None:
     """save_ppm (image_io.hpp:373-382)."""
-    a = np.ascontiguousarray(rgb, np.uint8)
-    h, w = a.shape[:2]
-    _write(path, f"P6\n{w} {h}\n255\n".encode() + a.tobytes())
+    a = np.ascontiguousarray(rgb, dtype=np.uint8)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise InvalidArgument("save_ppm: expected an (H, W, 3) uint8 image")
+    check(lib().bsmio_save_ppm(_b(path), _ptr(a), a.shape[1], a.shape[0]))
 
 
 # ---------------------------------------------------------------------------
-# JSON sidecars (nlohmann dump(1, '\t'): keys sorted, one tab per level)
-def _dump(obj) -> bytes:
-    return (json.dumps(obj, indent="\t", sort_keys=True, ensure_ascii=False) + "\n").encode()
-
-
+# JSON sidecars (config.hpp, pattern.hpp)
 def save_config(cfg: BsmConfig, path: str) -> None:
     """save_config (config.hpp:81-86)."""
-    obj = {"n": int(cfg.n), "S": int(cfg.window), "spread": float(cfg.spread), "seed": int(cfg.seed),
-           "d_max": int(cfg.d_max), "lambda_c": float(cfg.lambda_c), "lambda_e": float(cfg.lambda_e),
-           "lr_tolerance": float(cfg.lr_tolerance), "vote_radius": int(cfg.vote_radius),
-           "gt_scale": float(cfg.gt_scale), "threads": int(cfg.threads), "generator": str(cfg.generator)}
-    _write(path, _dump(obj))
-
-
-def _load_json(path: str, what: str):
-    data = _read_file(path)
-    try:
-        return json.loads(data.decode("utf-8"))
-    except (ValueError, UnicodeDecodeError) as e:
-        raise FormatError(f"bad {what} file {path}: {e}") from None
+    iv = np.array([cfg.n, cfg.window, cfg.seed, cfg.d_max, cfg.vote_radius, cfg.threads], np.int64)
+    dv = np.array([cfg.spread, cfg.lambda_c, cfg.lambda_e, cfg.lr_tolerance, cfg.gt_scale], np.float64)
+    check(lib().bsmio_save_config(_b(path), _ptr(iv), _ptr(dv), str(cfg.generator).encode()))
 
 
 def load_config(path: str) -> BsmConfig:
     """load_config (config.hpp:88-101); missing keys keep their defaults."""
-    j = _load_json(path, "config")
-    if not isinstance(j, dict):
-        raise FormatError(f"bad config file {path}: not an object")
-    c = BsmConfig()
-    spec = [("n", "n", int), ("S", "window", int), ("spread", "spread", float), ("seed", "seed", int),
-            ("d_max", "d_max", int), ("lambda_c", "lambda_c", float), ("lambda_e", "lambda_e", float),
-            ("lr_tolerance", "lr_tolerance", float), ("vote_radius", "vote_radius", int),
-            ("gt_scale", "gt_scale", float), ("threads", "threads", int), ("generator", "generator", str)]
-    for key, attr, typ in spec:
-        if key not in j:
-            continue
-        v = j[key]
-        if typ is str:
-            if not isinstance(v, str):
-                raise FormatError(f"bad config file {path}: '{key}' must be a string")
-        elif isinstance(v, bool) or not isinstance(v, (int, float)):
-            raise FormatError(f"bad config file {path}: '{key}' must be a number")
-        elif typ is int:
-            v = int(v)
-        else:
-            v = float(v)
-        setattr(c, attr, v)
-    return c
+    iv = np.zeros(6, np.int64)
+    dv = np.zeros(5, np.float64)
+    gen = C.create_string_buffer(4096)
+    check(lib().bsmio_load_config(_b(path), _ptr(iv), _ptr(dv), gen, 4096))
+    return BsmConfig(n=int(iv[0]), window=int(iv[1]), seed=int(iv[2]), d_max=int(iv[3]), vote_radius=int(iv[4]),
+                     threads=int(iv[5]), spread=float(dv[0]), lambda_c=float(dv[1]), lambda_e=float(dv[2]),
+                     lr_tolerance=float(dv[3]), gt_scale=float(dv[4]), generator=gen.value.decode())
 
 
 def save_pattern(p: SamplingPattern, path: str) -> None:
     """save_pattern (pattern.hpp:106-121): generator, parameters and the offset list."""
-    # the sidecar writer prints each offset quadruple on one line ("[px,py,qx,qy]")
-    rows = ",\n".join("\t\t[" + ",".join(str(int(v)) for v in row) + "]" for row in np.asarray(p.pairs)[: p.n])
-    obj = {"generator": GENERATOR_NAME, "n": int(p.n), "S": int(p.window), "spread": float(p.spread),
-           "seed": int(p.seed), "pairs": "@PAIRS@"}
-    text = _dump(obj).decode().replace('"@PAIRS@"', "[\n" + rows + "\n\t]")
-    _write(path, text.encode())
+    pairs = np.ascontiguousarray(np.asarray(p.pairs, dtype=np.int16).reshape(-1, 4)[: p.n])
+    check(lib().bsmio_save_pattern(_b(path), _ptr(pairs), int(p.n), int(p.window), float(p.spread),
+                                   C.c_uint64(int(p.seed))))
 
 
 def load_pattern(path: str) -> SamplingPattern:
     """load_pattern (pattern.hpp:123-158)."""
-    j = _load_json(path, "pattern")
-    try:
-        gen = j["generator"]
-        if gen != GENERATOR_NAME:
-            raise FormatError(f"pattern file {path} uses unknown generator '{gen}'")
-        n, window, spread, seed = int(j["n"]), int(j["S"]), float(j["spread"]), int(j["seed"])
-        pairs = j["pairs"]
-        if len(pairs) != n:
-            raise FormatError(f"pattern file {path}: pair count does not match n")
-        half = window // 2
-        arr = np.zeros((max(n, 1), 4), np.int16)
-        for i, e in enumerate(pairs):
-            q = [int(e[k]) for k in range(4)]
-            if any(v < -half or v > half for v in q):
-                raise FormatError(f"pattern file {path}: offset outside window")
-            arr[i] = q
-    except (KeyError, IndexError, TypeError, ValueError) as e:
-        raise FormatError(f"bad pattern file {path}: {e}") from None
-    return SamplingPattern(n, window, spread, seed, arr)
+    n, w, sp, sd = C.c_int(), C.c_int(), C.c_double(), C.c_uint64()
+    check(lib().bsmio_load_pattern(_b(path), C.byref(n), C.byref(w), C.byref(sp), C.byref(sd), None, 0))
+    arr = np.zeros((max(n.value, 1), 4), np.int16)
+    check(lib().bsmio_load_pattern(_b(path), C.byref(n), C.byref(w), C.byref(sp), C.byref(sd), _ptr(arr),
+                                   n.value))
+    return SamplingPattern(n.value, w.value, sp.value, sd.value, arr)
 
 
 # ---------------------------------------------------------------------------

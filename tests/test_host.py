@@ -30,6 +30,18 @@ def test_library_exports_every_declared_symbol():
     assert set(_lib.exported_symbols()) == set(names)
 
 
+def test_io_library_exports_every_declared_symbol():
+    """libbsm_io.so (include/bsm_io.h): the file / evaluation layer's C ABI,
+    bound by io.py and evaluation.py."""
+    from paper_1402_2020_b200 import io as bio
+    txt = open(os.path.join(ROOT, "include", "bsm_io.h")).read()
+    names = sorted(set(re.findall(r"\b(bsmio_[a-z0-9_]+)\s*\(", txt)))
+    assert len(names) >= 14
+    L = C.CDLL(bio.IO_PATH)
+    assert not [n for n in names if not hasattr(L, n)]
+    assert set(bio._SIGS) | {"bsmio_last_error"} == set(names)
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
