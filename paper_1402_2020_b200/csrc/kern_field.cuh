@@ -349,8 +349,10 @@ __global__ void __launch_bounds__(32, 16)
                 const uint32_t v1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
                 const uint32_t v2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
                 const uint32_t v3 = vmax_u16x2(lds_u32(rho, P.w), lds_u32(rho, Q.w));
-                const uint32_t x01 = __byte_perm(v0, v1, 0x6240);  // [A0 A1 B0 B1]
-                const uint32_t x23 = __byte_perm(v2, v3, 0x6240);  // [A2 A3 B2 B3]
+                // v = [A 0 B 0] bytes: v0 + 256 v1 = [A0 A1 B0 B1] (no carries: an
+                // add on the FMA pipe instead of a PRMT on the ALU pipe)
+                const uint32_t x01 = v1 * 256u + v0;  // [A0 A1 B0 B1]
+                const uint32_t x23 = v3 * 256u + v2;  // [A2 A3 B2 B3]
                 wa[t4] = __byte_perm(x01, x23, 0x5410);
                 wb[t4] = __byte_perm(x01, x23, 0x7632);
             }
