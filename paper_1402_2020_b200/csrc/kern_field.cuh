@@ -213,16 +213,29 @@ __device__ __forceinline__ void select_le2(const uint32_t (&pa)[8][MCH], const u
         }
         const int zas = int(__reduce_add_sync(0xFFFFFFFFu, ca));
         const int zbs = int(__reduce_add_sync(0xFFFFFFFFu, cb));
-        // warp-uniform choices; written as selects so both chains stay branch-free
+        // warp-uniform choices taken as uniform branches (no per-word selects)
         const bool ha = zas < ka, hb = zbs < kb;
-        ka -= ha ? zas : 0;
-        kb -= hb ? zbs : 0;
+        if (ha) {
+            ka -= zas;
 #pragma unroll
-        for (int m = 0; m < MCH; ++m) {
-            la[m] |= ha ? za[m] : 0u;
-            ea[m] = ha ? (ea[m] & pa[j][m]) : za[m];
-            lb[m] |= hb ? zb[m] : 0u;
-            eb[m] = hb ? (eb[m] & pb[j][m]) : zb[m];
+            for (int m = 0; m < MCH; ++m) {
+                la[m] |= za[m];
+                ea[m] &= pa[j][m];
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < MCH; ++m) ea[m] = za[m];
+        }
+        if (hb) {
+            kb -= zbs;
+#pragma unroll
+            for (int m = 0; m < MCH; ++m) {
+                lb[m] |= zb[m];
+                eb[m] &= pb[j][m];
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < MCH; ++m) eb[m] = zb[m];
         }
     }
 #pragma unroll
