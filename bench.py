@@ -31,9 +31,10 @@ run one pair per rank (replicas).
   cold_start  context creation + pattern upload + first pipeline (tables)
 
 --impl reference: the reference CPU implementation alone (rank 0), same
-metric and config; the K timed steps tile pair 0 of the workload row-band by
-row-band (each band run through run_pipeline as its own image), so the run
-covers one whole frame; value = median over steps (time_pipeline's median,
+metric and config; the K timed steps walk down pair 0 of the workload in
+consecutive row bands (each band run through run_pipeline as its own image,
+at least 8 rows per host thread), covering the whole frame when K bands
+reach it; value = median over steps (time_pipeline's median,
 eval.hpp:144-159).
 """
 from __future__ import annotations
@@ -180,16 +181,6 @@ def ref_band(ref, pairs_arr, left, right, y0, y1, d_max, threads):
     return out["seconds"], L.shape[1] * (y1 - y0) * d_max
 
 
-def split_rows(H: int, k: int):
-    k = max(1, min(k, H))
-    base, extra = divmod(H, k)
-    y = 0
-    for i in range(k):
-        h = base + (1 if i < extra else 0)
-        yield y, y + h
-        y += h
-
-
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, rank 0 only."""
     if env_int("RANK", 0) != 0:
@@ -206,20 +197,24 @@ def run_reference(args):
     if args.warmup > 0:  # page in the library and the thread pool on a small band
         ref_band(ref, pairs_arr, left, right, 0, min(8, H), w.d_max, threads)
     steps = max(1, args.steps)
-    bands = list(split_rows(H, steps))
-    secs, evals, tput = [], [], []
+    # consecutive bands walk down the frame (wrapping at the bottom); a band
+    # holds at least 8 rows per thread so the reference's row-parallel
+    # parallel_for (parallel.hpp:15-46) is balanced
+    rows = min(H, max(-(-H // steps), 8 * threads))
+    secs, evals, tput, covered = [], [], [], set()
     for i in range(steps):
-        y0, y1 = bands[i % len(bands)]
+        y0 = (i * rows) % H
+        y1 = min(H, y0 + rows)
         s, e = ref_band(ref, pairs_arr, left, right, y0, y1, w.d_max, threads)
         secs.append(s)
         evals.append(e)
         tput.append(e / s / 1e6)
+        covered.update(range(y0, y1))
     value = statistics.median(tput)
     frame = sum(evals) / sum(secs) / 1e6
-    covered = sum(b[1] - b[0] for b in bands[:steps])
-    sample = (f"pair 0 of {w.name} ({w.width}x{H}, D={w.d_max}) split into {len(bands)} row bands, one band per "
-              f"step run through run_pipeline as its own image ({covered} of {H} rows covered); "
-              f"{os.path.basename(ref.path)}, {threads} threads")
+    sample = (f"pair 0 of {w.name} ({w.width}x{H}, D={w.d_max}): {steps} consecutive bands of up to {rows} rows, "
+              f"one per step, each run through run_pipeline as its own image ({len(covered)} of {H} rows "
+              f"covered); {os.path.basename(ref.path)}, {threads} threads")
     line = {
         "impl": "reference", "metric": "Mdisp-evals/s", "value": value, "unit": "Mdisp-evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -250,7 +245,7 @@ def cpu_baseline_leg(args, w, pairs_arr):
     ref = oracle.Reference()
     left, right = ref_inputs(ref, args.workload, 0)
     H = left.shape[0]
-    rows = min(args.ref_rows, H)
+    rows = min(args.ref_rows or 8 * threads, H)
     y0 = (H - rows) // 2
     ref_band(ref, pairs_arr, left, right, y0, y0 + min(8, rows), w.d_max, threads)  # warm-up
     tp = []
@@ -275,7 +270,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=WORKLOADS_CLI)
     ap.add_argument("--pairs", type=int, default=0, help="batch size override (c4; default: the config's 64)")
-    ap.add_argument("--ref-rows", type=int, default=96)
+    ap.add_argument("--ref-rows", type=int, default=0, help="cpu_baseline band rows (0: 8 per host thread)")
     ap.add_argument("--ref-repeats", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="value loop only (for ncu)")

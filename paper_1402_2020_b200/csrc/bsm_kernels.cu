@@ -93,8 +93,11 @@ struct DevBuf {
             base = nullptr;
             return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMalloc: ") + cudaGetErrorString(e));
         }
-        if (g_guard && (e = cudaMemset(base, 0xA5, bytes + extra)) != cudaSuccess)
-            return set_err(BSM_CUDA_ERROR, std::string("CUDA: cudaMemset: ") + cudaGetErrorString(e));
+        // (the fill runs on the legacy stream, which the context's non-blocking
+        // stream does not wait for: complete it before the buffer is handed out)
+        if (g_guard && ((e = cudaMemset(base, 0xA5, bytes + extra)) != cudaSuccess ||
+                        (e = cudaStreamSynchronize(nullptr)) != cudaSuccess))
+            return set_err(BSM_CUDA_ERROR, std::string("CUDA: guard fill: ") + cudaGetErrorString(e));
         p = static_cast<char*>(base) + (g_guard ? kGuard : 0);
         cap = bytes;
         return BSM_OK;
@@ -965,7 +968,11 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     // Byte offsets into the u32 rank table of each bit position's two
     // endpoints (k_mask4 / k_mask_f32): P table at [0, kPqTable), Q table at
     // [kPqTable, 2 kPqTable), lane-block order -- lane l, chunk m < MCH, t:
-    // bit 32*MCH*l + 32m + t at uint4 [(m*8 + t/4)*32 + l], component t%4.
+    // bit 32*MCH*l + 32m + t at uint4 [(m*8 + t%8)*32 + l], component t/8 for
+    // MCH <= 4 (the four positions t, t+8, t+16, t+24 of one load land in the
+    // four byte lanes of one word, so k_mask4's bit-plane transposes run across
+    // words); [(m*8 + t/4)*32 + l], component t%4 for MCH = 8 (whose per-pixel
+    // pass keeps the per-8-byte transposes to stay within 128 registers).
     // Pads read the sentinel.  For MCH <= 4, k_mask_f32 reads the packed table
     // at [2 kPqTable, 3 kPqTable): P | Q << 16 (mslots <= 2 * 4096 + 64 there,
     // so byte offsets fit 16 bits) -- half the L1 footprint of the gathers.
@@ -974,7 +981,8 @@ int bsm_set_pattern(bsm_ctx* c, const int16_t* pairs, int n, int window) {
     for (int i = 0; i < kPqTable; ++i) pqb[2 * kPqTable + i] = uint32_t(4 * c->mslots) * 65537u;
     for (int j = 0; j < n; ++j) {
         const int l = j / lane_pos, m = (j >> 5) % c->mch, t = j & 31;
-        const size_t at = (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
+        const size_t at = c->mch <= 4 ? (size_t(m * 8 + (t & 7)) * 32 + l) * 4 + (t >> 3)
+                                      : (size_t(m * 8 + (t >> 2)) * 32 + l) * 4 + (t & 3);
         const uint32_t e = pq[size_t(c->order[size_t(j)])];
         const uint32_t a = flip[size_t(j)] ? e >> 16 : e & 0xFFFFu, b = flip[size_t(j)] ? e & 0xFFFFu : e >> 16;
         pqb[at] = uint32_t(4 * rslot[size_t(a)]);

@@ -161,6 +161,36 @@ __device__ __forceinline__ void transpose8x8_32(uint32_t& lo, uint32_t& hi) {
     hi ^= t >> 4;
 }
 
+// src[0..7]: 32 byte values, value t = byte t/8 of src[t%8] (the gather order
+// of the index tables for MCH <= 4); afterwards w[j] bit t = bit j of value t.
+// Each byte lane
+// holds an 8 x 8 bit matrix (row k = w[k]'s byte); three delta-swap stages
+// across the words transpose all four at once, and word j of the result is
+// plane j (byte lane b = positions 8b..8b+7): 12 swaps, no byte shuffles.
+__device__ __forceinline__ void bytes_to_planes_x(const uint32_t (&src)[8], uint32_t (&w)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = src[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // distance 4: bits 4..7 of rows k <-> bits 0..3 of rows k + 4
+        const uint32_t t = ((w[k] >> 4) ^ w[k + 4]) & 0x0F0F0F0Fu;
+        w[k + 4] ^= t;
+        w[k] ^= t * 16u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // distance 2
+        if (k & 2) continue;
+        const uint32_t t = ((w[k] >> 2) ^ w[k + 2]) & 0x33333333u;
+        w[k + 2] ^= t;
+        w[k] ^= t * 4u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {  // distance 1
+        const uint32_t t = ((w[k] >> 1) ^ w[k + 1]) & 0x55555555u;
+        w[k + 1] ^= t;
+        w[k] ^= t * 2u;
+    }
+}
+
 // w[0..7]: 32 byte values (value t = byte t%4 of w[t/4]); planes[j] bit t = bit j of value t.
 __device__ __forceinline__ void bytes_to_planes(const uint32_t (&w)[8], uint32_t (&pl)[8]) {
     uint32_t lo[4], hi[4];
@@ -376,8 +406,8 @@ __global__ void __launch_bounds__(32, 16)
             for (int m = 0; m < MCH; ++m) {
                 uint32_t wa[8], wb[8], ta[8], tb[8];
                 gather(m, wa, wb);
-                bytes_to_planes(wa, ta);
-                bytes_to_planes(wb, tb);
+                bytes_to_planes_x(wa, ta);
+                bytes_to_planes_x(wb, tb);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     pa[j][m] = ta[j];
@@ -389,7 +419,10 @@ __global__ void __launch_bounds__(32, 16)
             store_words<MCH>(stage + q * STG + MCH * lane, oa);
             store_words<MCH>(stage + (q + 1) * STG + MCH * lane, ob);
         } else {
-            // one pixel's planes at a time: the gathers run twice
+            // one pixel's planes at a time: the gathers run twice (the index
+            // tables keep the 4-consecutive-positions order for MCH = 8, see
+            // bsm_set_pattern, so the per-8-byte transposes keep register
+            // pressure at the 128 budget)
 #pragma unroll 1
             for (int side = 0; side < 2; ++side) {
                 uint32_t pl[8][MCH];
@@ -587,10 +620,13 @@ __global__ void __launch_bounds__(32, 16)
                         P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
                         Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
                     }
-                    x[4 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
-                    x[4 * t4 + 1] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
-                    x[4 * t4 + 2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
-                    x[4 * t4 + 3] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
+                    // positions t4 + 8c (MCH <= 4) or 4 t4 + c (MCH = 8): the
+                    // index tables' order (bsm_set_pattern)
+                    constexpr int S1 = MCH <= 4 ? 1 : 4, S2 = MCH <= 4 ? 8 : 1;
+                    x[S1 * t4] = max(lds_u32(tv, P.x), lds_u32(tv, Q.x));
+                    x[S1 * t4 + S2] = max(lds_u32(tv, P.y), lds_u32(tv, Q.y));
+                    x[S1 * t4 + 2 * S2] = max(lds_u32(tv, P.z), lds_u32(tv, Q.z));
+                    x[S1 * t4 + 3 * S2] = max(lds_u32(tv, P.w), lds_u32(tv, Q.w));
                 }
                 transpose32(x);
                 store(m, x);
