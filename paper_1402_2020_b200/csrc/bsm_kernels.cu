@@ -169,6 +169,7 @@ struct bsm_ctx {
     int ev_used[T_COUNT] = {};
     int launches = 0;
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
+    int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
                      // 2 x SMs tiles
@@ -349,17 +350,27 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         dim3 grid3((Wq + kM3Px - 1) / kM3Px, rows);
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
-            kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>(),
+            const bool packed = c->mch <= 4 && !(c->mask_variant & 1);
+            kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows,
+                                                c->d_pqb.as<uint4>() + (packed ? 2 * kPqTable / 4 : 0),
                                                 c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<int32_t>(),
                                                 c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
                                                 c->half, mask4_tw(c->half), c->NW, Wq, P, mask);
             return BSM_OK;
         };
         // chunks of 32 positions per lane: the work scales with n
-        BSM_TRY(c->mch == 1   ? launch(k_mask4<1>)
-                : c->mch == 2 ? launch(k_mask4<2>)
-                : c->mch == 4 ? launch(k_mask4<4>)
-                              : launch(k_mask4<8>));
+        // MCH <= 4: the packed P | Q << 16 index table (half the index loads;
+        // the split runs on the FMA pipe): -3% mask time at c2 / c4
+        if (!(c->mask_variant & 1))
+            BSM_TRY(c->mch == 1   ? launch(k_mask4<1, true>)
+                    : c->mch == 2 ? launch(k_mask4<2, true>)
+                    : c->mch == 4 ? launch(k_mask4<4, true>)
+                                  : launch(k_mask4<8>));
+        else
+            BSM_TRY(c->mch == 1   ? launch(k_mask4<1>)
+                    : c->mch == 2 ? launch(k_mask4<2>)
+                    : c->mch == 4 ? launch(k_mask4<4>)
+                                  : launch(k_mask4<8>));
         BSM_TRY(check_launch(c, "mask"));
     }
     return BSM_OK;
@@ -805,6 +816,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     c->device = device;
     if (const char* v = std::getenv("BSM_K3_VARIANT")) c->k3_variant = std::atoi(v);
     if (const char* v = std::getenv("BSM_K3_GROUP")) c->k3_group = std::atoi(v);
+    if (const char* v = std::getenv("BSM_MASK_VARIANT")) c->mask_variant = std::atoi(v);
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;

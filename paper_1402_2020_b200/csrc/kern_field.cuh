@@ -322,7 +322,7 @@ __device__ __forceinline__ void select_le1(const uint32_t (&pa)[8][MCH], int k, 
 // 4 of padding (16-B aligned rows, conflict-free read-out).
 __host__ __device__ constexpr int mask4_stage_stride(int mch) { return 32 * mch + 4; }
 
-template <int MCH>
+template <int MCH, bool PACKED = false>
 __global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
@@ -386,8 +386,18 @@ __global__ void __launch_bounds__(32, 16)
         auto gather = [&](int m, uint32_t(&wa)[8], uint32_t(&wb)[8]) {
 #pragma unroll
             for (int t4 = 0; t4 < 8; ++t4) {
-                const uint4 P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
-                const uint4 Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                uint4 P, Q;
+                if constexpr (PACKED) {
+                    // one load of P | Q << 16 (p4 points at the packed table),
+                    // split on the FMA pipe: hi = x >> 16, lo = x - (hi << 16)
+                    const uint4 X = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                    Q = make_uint4(__umulhi(X.x, 65536u), __umulhi(X.y, 65536u), __umulhi(X.z, 65536u),
+                                   __umulhi(X.w, 65536u));
+                    P = make_uint4(X.x - Q.x * 65536u, X.y - Q.y * 65536u, X.z - Q.z * 65536u, X.w - Q.w * 65536u);
+                } else {
+                    P = __ldg(p4 + (m * 8 + t4) * 32 + lane);
+                    Q = __ldg(q4 + (m * 8 + t4) * 32 + lane);
+                }
                 const uint32_t v0 = vmax_u16x2(lds_u32(rho, P.x), lds_u32(rho, Q.x));
                 const uint32_t v1 = vmax_u16x2(lds_u32(rho, P.y), lds_u32(rho, Q.y));
                 const uint32_t v2 = vmax_u16x2(lds_u32(rho, P.z), lds_u32(rho, Q.z));
