@@ -205,3 +205,37 @@ def test_cpp_cli_host_behaviour(tmp_path):
     bio.save_disparity(gt, str(tmp_path / "gt.pgm"), 16.0)
     r = run("eval", str(tmp_path / "gt.pgm"), str(tmp_path / "gt.pgm"))
     assert r.returncode == 0 and r.stdout == "all        0.00  (0 of 20 pixels beyond 1.00)\n"
+
+
+# ---------------------------------------------------------------------------
+# A plain C client (tests/cpp/capi_multi.c): the batch entry point and the
+# NCCL partitions at world 1, with no C++ and no PyTorch in the process.
+C_SRC = os.path.join(ROOT, "tests", "cpp", "capi_multi.c")
+C_BIN = os.path.join(ROOT, "build", "capi_multi")
+
+
+def test_c_client_compiles_against_the_header():
+    os.makedirs(os.path.dirname(C_BIN), exist_ok=True)
+    subprocess.run(["gcc", "-std=c11", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), C_SRC, "-o",
+                    C_BIN, "-L", LIBDIR, "-lbsm_cuda", f"-Wl,-rpath,{LIBDIR}"], check=True)
+
+
+@pytest.mark.gpu
+def test_c_client_batch_and_nccl_match_reference(tmp_path, ref, default_pairs):
+    from paper_1402_2020_b200.synth import synth_pair
+    test_c_client_compiles_against_the_header()
+    W, H, D = 170, 41, 48
+    pairs = [synth_pair(0, 50 + i, W, H) for i in range(3)]
+    (tmp_path / "p.raw").write_bytes(b"".join(l.tobytes() + r.tobytes() for l, r in pairs))
+    out = subprocess.run([C_BIN, str(W), str(H), str(D), str(tmp_path / "p.raw"), str(tmp_path / "o.bin")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    raw = np.fromfile(tmp_path / "o.bin", np.uint8)
+    px = W * H
+    maps = [(raw[k * 5 * px:k * 5 * px + 4 * px].view(np.float32).reshape(H, W),
+             raw[k * 5 * px + 4 * px:(k + 1) * 5 * px].reshape(H, W)) for k in range(len(raw) // (5 * px))]
+    assert len(maps) == 3 + 1 + 3
+    want = [ref.pipeline(l, r, default_pairs, 26, D, threads=8) for l, r in pairs]
+    got_order = [0, 1, 2, 0, 0, 1, 2]  # batch, frame bands of pair 0, sharded pairs
+    for (d, v), i in zip(maps, got_order):
+        assert np.array_equal(d, want[i]["refined_d"]) and np.array_equal(v, want[i]["refined_v"])
