@@ -88,3 +88,17 @@ def test_batch_contract(ctx):
     assert lib().bsm_pipeline_batch_u8(ctx.handle, 1, nulls, nulls, 40, 20, C.byref(p), None, None) == 1
     assert lib().bsm_pipeline_batch_u8(ctx.handle, -1, None, None, 40, 20, C.byref(p), None, None) == 1
     assert lib().bsm_pipeline_batch_u8(ctx.handle, 0, None, None, 40, 20, C.byref(p), None, None) == 0
+
+
+def test_repeated_runs_bit_identical(ctx):
+    """Race check without compute-sanitizer: K3's slot counters, the atomicMin
+    merge of d-blocks and K6's work counter must give the same maps on every
+    run (the reference is deterministic by construction, parallel.hpp:12-14)."""
+    left, right = workload_pair("c2")
+    cfg = bsm.BsmConfig(d_max=240)
+    first = bsm.run_pipeline(left, right, cfg, ctx=ctx)
+    for _ in range(6):
+        again = bsm.run_pipeline(left, right, cfg, ctx=ctx)
+        assert again.refined == first.refined and again.checked == first.checked
+        assert np.array_equal(again.left_wta.disparity, first.left_wta.disparity)
+        assert np.array_equal(again.right_wta.disparity, first.right_wta.disparity)
