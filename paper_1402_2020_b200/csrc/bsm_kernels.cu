@@ -778,7 +778,7 @@ int check_batch_ptrs(int n_pairs, const void* const* a, const void* const* b) {
 
 int check_dims(int W, int H) {
     if (W < 1 || H < 1) return set_err(BSM_INVALID_ARGUMENT, "bsm: image dimensions must be >= 1");
-    if (int64_t(W) * H > (int64_t(1) << 31) - 1)
+    if (int64_t(round_up(W, 128)) * H > (int64_t(1) << 31) - 1)  // field planes index pixels with int
         return set_err(BSM_UNSUPPORTED, "bsm: images above 2^31 pixels are outside this build's envelope");
     if (H > 65535) return set_err(BSM_UNSUPPORTED, "bsm: images taller than 65535 rows are outside this build's envelope");
     return BSM_OK;
