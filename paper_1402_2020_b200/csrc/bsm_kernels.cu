@@ -169,6 +169,7 @@ struct bsm_ctx {
     int ev_used[T_COUNT] = {};
     int launches = 0;
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
+    int maskf_force_low = 0;  // test hook (BSM_MASKF_FORCE_LOW=1): k_mask_f32 resolves every low byte
     int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
@@ -553,7 +554,7 @@ int ensure_descf_table(bsm_ctx* c) {
     return BSM_OK;
 }
 
-size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(24) * c->mch * 32 * 4; }
+size_t maskf_smem(const bsm_ctx* c) { return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(23) * c->mch * 32 * 4; }
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) from float gray / Lab planes.
 int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, int H, int ybeg, int rows,
@@ -581,7 +582,8 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, in
             kern<<<grid, 32, sm, c->stream>>>(lab, W, H, ybeg, rows,
                                               c->d_pqb.as<uint4>() + (c->mch <= 4 ? 2 * kPqTable / 4 : 0),
                                               c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uxy.as<int32_t>(), c->mslots,
-                                              round_up(c->mslots + 1, 4), c->NW, Wq, P, mask, c->half);
+                                              round_up(c->mslots + 1, 4), c->NW, Wq, P, mask, c->half,
+                                              c->maskf_force_low);
             return BSM_OK;
         };
         BSM_TRY(c->mch == 1   ? launch(k_mask_f32<1>)
@@ -816,6 +818,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     c->device = device;
     if (const char* v = std::getenv("BSM_K3_VARIANT")) c->k3_variant = std::atoi(v);
     if (const char* v = std::getenv("BSM_K3_GROUP")) c->k3_group = std::atoi(v);
+    if (const char* v = std::getenv("BSM_MASKF_FORCE_LOW")) c->maskf_force_low = std::atoi(v) != 0;
     if (const char* v = std::getenv("BSM_MASK_VARIANT")) c->mask_variant = std::atoi(v);
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {

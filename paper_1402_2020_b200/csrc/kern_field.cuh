@@ -568,13 +568,14 @@ template <int MCH>
 __global__ void __launch_bounds__(32, 16)
     k_mask_f32(const float4* __restrict__ lab4, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
                const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uxy, int u, int rho_words,
-               int NW, int Wq, size_t P, uint32_t* __restrict__ mask, int half) {
+               int NW, int Wq, size_t P, uint32_t* __restrict__ mask, int half, int force_low) {
     // Lab samples (float4 per pixel) are read through L1 (no shared tile):
-    // shared memory holds only the slot keys and 24 rows of bit planes (the
-    // low byte's planes reuse the rows of bits 8..15), for occupancy.
+    // shared memory holds only the slot keys and 23 rows of bit planes (key
+    // bits 30..8: SADs are non-negative floats, so bit 31 is 0 in every key;
+    // the low byte's planes reuse the rows of bits 8..15), for occupancy.
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* tv = dsm;                                   // rho_words: SAD bits per slot (+ sentinel)
-    uint32_t* planes = tv + rho_words;                    // [24 rows][MCH chunks][32 lanes]
+    uint32_t* planes = tv + rho_words;                    // [23 rows][MCH chunks][32 lanes]
     auto prow = [](int b) { return b >= 8 ? b - 8 : b; };  // plane row of key bit b
     const int G = (n + 31) >> 5;
     const int lane = threadIdx.x;
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(32, 16)
         };
         planes_of([&](int m, const uint32_t (&x)[32]) {
 #pragma unroll
-            for (int j = 8; j < 32; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
+            for (int j = 8; j < 31; ++j) planes[(prow(j) * MCH + m) * 32 + lane] = x[j];
         });
         __syncwarp();
         // MSB-first k-th smallest over 32-bit keys (pads are 0xFFFFFFFF) with
@@ -683,7 +684,9 @@ __global__ void __launch_bounds__(32, 16)
                 }
             }
         };
-        rounds(31, 8);
+        // bit 31 is 0 for every key; the pads (0xFFFFFFFF) drop out of eq at
+        // the first 0 bit of the threshold, which a finite key always has
+        rounds(30, 8);
         // Every value is a slot key, so the positions still tied (top 24 bits
         // equal to the threshold's) all hold the threshold itself when the
         // slot keys with those top bits are one value: then eq is final.
@@ -696,11 +699,8 @@ __global__ void __launch_bounds__(32, 16)
                 mx = max(mx, v);
             }
         }
-#ifdef BSM_MASKF_ALWAYS_LOW  // test hook: resolve the low byte for every pixel
-        if (true) {
-#else
-        if (__reduce_min_sync(full, mn) != __reduce_max_sync(full, mx)) {
-#endif
+        // (force_low: test hook, BSM_MASKF_FORCE_LOW=1 -- resolve the low byte for every pixel)
+        if (force_low || __reduce_min_sync(full, mn) != __reduce_max_sync(full, mx)) {
             __syncwarp();
             planes_of([&](int m, const uint32_t (&x)[32]) {  // rows of bits 8..15 are dead now
 #pragma unroll

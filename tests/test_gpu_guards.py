@@ -46,3 +46,33 @@ print("GUARDS", on, damaged)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("GUARDS")]
     assert lines == ["GUARDS True 0", "GUARDS True 0"], lines
+
+
+def test_colour_mask_low_byte_path_matches_reference():
+    """k_mask_f32 resolves the low key byte only when the threshold's tie spans
+    several slot keys (rare); BSM_MASKF_FORCE_LOW=1 takes that path for every
+    pixel, which must give the same masks (compute_field on float planes
+    against descriptor.hpp:118-154 compiled in place)."""
+    code = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import numpy as np
+import oracle
+import paper_1402_2020_b200 as bsm
+from paper_1402_2020_b200.synth import colour_pair
+ref = oracle.Reference()
+bad = 0
+for n, seed in ((4096, 1), (2048, 2), (1000, 3), (8192, 4)):
+    L, _ = colour_pair(24, 70, seed=seed)
+    g, lab = bsm.to_gray_lab(L)
+    lab[::3, ::5] = lab[0, 0]  # heavy exact ties among the window SADs
+    pairs = ref.generate_pattern(n, 26, 4.0, seed)
+    d_ref, m_ref = ref.compute_field(g, lab, pairs, 26)
+    d_gpu, m_gpu = bsm.compute_field((g, lab), bsm.SamplingPattern(n, 26, 4.0, seed, pairs))
+    bad += int(not (np.array_equal(d_gpu, d_ref) and np.array_equal(m_gpu, m_ref)))
+print("BAD", bad)
+'''
+    env = dict(os.environ, BSM_MASKF_FORCE_LOW="1", ROOT=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "BAD 0" in r.stdout, r.stdout[-2000:]
