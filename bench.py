@@ -56,6 +56,7 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
 WORDOPS_PER_CLK_SM = 32  # ALU: 64 LOP3/clk/SM at 2 LOP3 per word-op; XU: 16 POPC/clk/SM at 0.5 per word-op
+ISSUE_WORDOPS_PER_CLK_SM = 128 * 64 / 208  # 128 thread-instructions/clk/SM, 208 per 64 word-ops (K3's loop)
 WORKLOADS_CLI = ["c1", "c2", "c3", "c4", "c5", "c2rgb"]
 
 
@@ -534,6 +535,10 @@ def main():
         "peak_source": f"nominal: {WORDOPS_PER_CLK_SM} word-ops/clk/SM (64 LOP3/clk/SM at 2 per word-op = 16 "
                        f"POPC/clk/SM at 0.5 per word-op) x {sms} SMs x {clk:.0f} MHz",
         "achievable_peak": csa_peak / 1e9, "frac_of_achievable": achieved / csa_peak,
+        # the carry-save loop issues 208 instructions per 64 word-ops per lane (128 LOP3 + 32 POPC
+        # + 32 IMAD + 10 LDS.128 + 6): against 4 schedulers x 32 lanes per clk per SM
+        "issue_peak": ISSUE_WORDOPS_PER_CLK_SM * sms * clk * 1e6 / 1e9,
+        "frac_of_issue": achieved / (ISSUE_WORDOPS_PER_CLK_SM * sms * clk * 1e6),
         "achievable_source": "live register-only microbenchmark of the kernel's carry-save instruction mix",
         "popc_only_peak": popc_peak / 1e9,
         "kernel_ms": wta_ms, "alg_word_ops": 2 * evals_dir * 128,
