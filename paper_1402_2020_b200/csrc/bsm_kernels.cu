@@ -751,6 +751,25 @@ int sync(bsm_ctx* c) {
     return BSM_OK;
 }
 
+// The per-stage vote_refine's pre-pass on the device (c->chk_d / chk_v hold
+// the caller's map): invalid list + max_bin into c->counters / c->inv, and
+// ref_d / ref_v initialised with the input map; max_bin returned to the host
+// (the bin count sizes the refine kernel's shared memory).
+int invalid_list(bsm_ctx* c, size_t px, double lim, int& max_bin) {
+    BSM_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, c->chk_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
+    BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, c->chk_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
+    k_invalid_list<<<unsigned((px + 255) / 256), 256, 0, c->stream>>>(c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), px,
+                                                                      lim, c->counters.as<int>(), c->inv.as<int>());
+    BSM_TRY(check_launch(c, "invalid_list"));
+    int cnt[4];
+    BSM_CUDA(cudaMemcpyAsync(cnt, c->counters.p, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
+    BSM_TRY(sync(c));
+    if (cnt[3]) return set_err(BSM_INVALID_ARGUMENT, "vote_refine: valid disparity out of range");
+    max_bin = cnt[0];
+    return BSM_OK;
+}
+
 // Copy streams, events and the two slots of views / refined maps used to
 // overlap pair i's compute with pair i+1's upload and pair i-1's download.
 int ensure_batch(bsm_ctx* c, size_t px) {
@@ -1144,37 +1163,19 @@ int bsm_vote_refine_u8(bsm_ctx* c, const float* d, const uint8_t* v, const uint8
     if (vote_radius < 1) return set_err(BSM_INVALID_ARGUMENT, "refine: vote_radius must be >= 1");
     if (vote_radius > 180) return set_err(BSM_UNSUPPORTED, "bsm: vote_radius > 180 is outside this build's envelope");
     const size_t px = size_t(W) * H;
-    // Host pre-pass over the caller's map: max_bin (refine.hpp:68-72) and the
-    // invalid list.  Valid disparities must round to a bin >= 0.
-    int max_bin = 0;
-    std::vector<int> invalid;
-    for (size_t i = 0; i < px; ++i) {
-        if (v[i]) {
-            const double dv = double(d[i]);
-            if (!(dv > -0.5) || !(dv < 1e6)) return set_err(BSM_INVALID_ARGUMENT, "vote_refine: valid disparity out of range");
-            max_bin = std::max(max_bin, int(std::lround(dv)));
-        } else {
-            invalid.push_back(int(i));
-        }
-    }
-    if (max_bin + 1 > 12288) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too large for the refine bins");
     BSM_TRY(c->img_l.ensure(px));
     BSM_TRY(c->chk_d.ensure(px * 4));
     BSM_TRY(c->chk_v.ensure(px));
     BSM_TRY(c->ref_d.ensure(px * 4));
     BSM_TRY(c->ref_v.ensure(px));
     BSM_TRY(c->counters.ensure(64));
-    BSM_TRY(c->inv.ensure(std::max<size_t>(4, invalid.size() * 4)));
+    BSM_TRY(c->inv.ensure(std::max<size_t>(4, px * 4)));
     BSM_CUDA(cudaMemcpyAsync(c->img_l.p, gray_img, px, cudaMemcpyHostToDevice, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->chk_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->chk_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
-    BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
-    BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
-    int cnt[2] = {max_bin, int(invalid.size())};
-    BSM_CUDA(cudaMemcpyAsync(c->counters.p, cnt, 8, cudaMemcpyHostToDevice, c->stream));
-    if (!invalid.empty())
-        BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    BSM_TRY(sync(c));  // host staging buffers (cnt, invalid) go out of scope
+    int max_bin = 0;
+    BSM_TRY(invalid_list(c, px, 1e6, max_bin));
+    if (max_bin + 1 > 12288) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too large for the refine bins");
     BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), nullptr, W, H,
                           vote_radius, max_bin + 1, lambda_c, lambda_e));
     if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1344,18 +1345,6 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
     if (vote_radius < 1) return set_err(BSM_INVALID_ARGUMENT, "refine: vote_radius must be >= 1");
     if (vote_radius > 180) return set_err(BSM_UNSUPPORTED, "bsm: vote_radius > 180 is outside this build's envelope");
     const size_t px = size_t(W) * H;
-    int max_bin = 0;
-    std::vector<int> invalid;
-    for (size_t i = 0; i < px; ++i) {
-        if (v[i]) {
-            const double dv = double(d[i]);
-            if (!(dv > -0.5) || !(dv < 65535.0))
-                return set_err(BSM_INVALID_ARGUMENT, "vote_refine: valid disparity out of range");
-            max_bin = std::max(max_bin, int(std::lround(dv)));
-        } else {
-            invalid.push_back(int(i));
-        }
-    }
     BSM_TRY(c->img_l.ensure(px));
     BSM_TRY(c->aux2.ensure(px * 12));
     BSM_TRY(c->aux3.ensure(px * 16));
@@ -1364,20 +1353,15 @@ int bsm_vote_refine_lab(bsm_ctx* c, const float* d, const uint8_t* v, const floa
     BSM_TRY(c->ref_d.ensure(px * 4));
     BSM_TRY(c->ref_v.ensure(px));
     BSM_TRY(c->counters.ensure(64));
-    BSM_TRY(c->inv.ensure(std::max<size_t>(4, invalid.size() * 4)));
+    BSM_TRY(c->inv.ensure(std::max<size_t>(4, px * 4)));
     BSM_CUDA(cudaMemsetAsync(c->img_l.p, 0, px, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->aux2.p, lab, px * 12, cudaMemcpyHostToDevice, c->stream));
     k_lab3_to_lab4<<<unsigned((px + 255) / 256), 256, 0, c->stream>>>(c->aux2.as<float>(), px, c->aux3.as<float4>());
     BSM_TRY(check_launch(c, "lab3_to_lab4"));
     BSM_CUDA(cudaMemcpyAsync(c->chk_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
     BSM_CUDA(cudaMemcpyAsync(c->chk_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
-    BSM_CUDA(cudaMemcpyAsync(c->ref_d.p, d, px * 4, cudaMemcpyHostToDevice, c->stream));
-    BSM_CUDA(cudaMemcpyAsync(c->ref_v.p, v, px, cudaMemcpyHostToDevice, c->stream));
-    int cnt[2] = {max_bin, int(invalid.size())};
-    BSM_CUDA(cudaMemcpyAsync(c->counters.p, cnt, 8, cudaMemcpyHostToDevice, c->stream));
-    if (!invalid.empty())
-        BSM_CUDA(cudaMemcpyAsync(c->inv.p, invalid.data(), invalid.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    BSM_TRY(sync(c));
+    int max_bin = 0;
+    BSM_TRY(invalid_list(c, px, 65535.0, max_bin));
     BSM_TRY(refine_launch(c, c->chk_d.as<float>(), c->chk_v.as<uint8_t>(), c->img_l.as<uint8_t>(), c->aux3.as<float4>(),
                           W, H, vote_radius, max_bin + 1, lambda_c, lambda_e));
     if (out_d) BSM_CUDA(cudaMemcpyAsync(out_d, c->ref_d.p, px * 4, cudaMemcpyDeviceToHost, c->stream));

@@ -44,6 +44,38 @@ __global__ void k_lr_check_keys(const uint32_t* __restrict__ kl, const uint32_t*
     if (need) inv[base + __popc(ballot & ((1u << lane) - 1u))] = int(i);
 }
 
+// The per-stage vote_refine's inputs on the device (refine.hpp:64-72): the
+// invalid pixels (warp-aggregated list in counters[1] / inv), max over the
+// valid pixels of lround(d) (counters[0], refine.hpp:68-72), and counters[3]
+// set when a valid disparity is out of range (not in (-0.5, lim), or NaN).
+__global__ void k_invalid_list(const float* __restrict__ d, const uint8_t* __restrict__ v, size_t px, double lim,
+                               int* __restrict__ counters, int* __restrict__ inv) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = i < px;
+    const bool valid = in && v[i] != 0;
+    int bin = 0;
+    bool bad = false;
+    if (valid) {
+        const double dv = double(d[i]);
+        bad = !(dv > -0.5) || !(dv < lim);
+        if (!bad) bin = int(llround(dv));
+    }
+    const unsigned full = 0xFFFFFFFFu;
+    const int mb = __reduce_max_sync(full, bin);
+    const bool anybad = __any_sync(full, bad);
+    const bool need = in && !valid;
+    const unsigned ballot = __ballot_sync(full, need);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) {
+        atomicMax(&counters[0], mb);
+        if (anybad) atomicExch(&counters[3], 1);
+        if (ballot) base = atomicAdd(&counters[1], __popc(ballot));
+    }
+    base = __shfl_sync(full, base, 0);
+    if (need) inv[base + __popc(ballot & ((1u << lane) - 1u))] = int(i);
+}
+
 // lr_check on float maps (per-stage API, refine.hpp:39-54).
 __global__ void k_lr_check_float(const float* __restrict__ dl, const float* __restrict__ dr, int W, int H,
                                  double tol, float* __restrict__ od, uint8_t* __restrict__ ov) {

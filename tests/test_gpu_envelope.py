@@ -64,3 +64,24 @@ def test_rejected_pattern_keeps_context_consistent(ctx):
     a = bsm.run_pipeline(left, right, bsm.BsmConfig(n=256, window=10, seed=9, d_max=10), good, ctx=ctx)
     b = bsm.run_pipeline(left, right, bsm.BsmConfig(n=256, window=10, seed=9, d_max=10), good, ctx=bsm.Context(0))
     assert a.refined == b.refined
+
+
+def test_vote_refine_rejects_out_of_range_valid_disparities(ctx):
+    """The per-stage vote_refine's device pre-pass (invalid list, max_bin)
+    rejects valid disparities that cannot name a bin (refine.hpp:68-72):
+    negative beyond -0.5, NaN, or beyond the envelope."""
+    g = synth_pair(0, 3, 40, 12)[0]
+    d = np.full((12, 40), 5.0, np.float32)
+    v = np.ones((12, 40), np.uint8)
+    v[3, 4] = 0
+    ok = bsm.vote_refine(bsm.DisparityMap(d, v), g, ctx=ctx)
+    assert ok.valid[3, 4] == 1 and ok.disparity[3, 4] == 5.0  # the only invalid pixel takes its voters' bin
+    for bad in (-0.75, np.nan, 2e6):
+        d2 = d.copy()
+        d2[0, 0] = bad
+        with pytest.raises(bsm.InvalidArgument, match="out of range"):
+            bsm.vote_refine(bsm.DisparityMap(d2, v), g, ctx=ctx)
+    # an invalid pixel may hold anything (it is never read as a voter)
+    d3 = d.copy()
+    d3[3, 4] = np.nan
+    assert bsm.vote_refine(bsm.DisparityMap(d3, v), g, ctx=ctx) == ok
