@@ -195,6 +195,24 @@ int bsm_pipeline_pairs_sharded_u8(bsm_ctx* ctx, bsm_comm* comm, int n_pairs, con
                                   const uint8_t* const* rights, int W, int H, const bsm_params* params, int root,
                                   float* const* refined_d, uint8_t* const* refined_v);
 
+/* One frame over peer memory (configs[4]; the alternative to
+ * bsm_pipeline_frame_bands_u8 without a collective launch): each rank creates
+ * a full-frame refined map in device memory and exports it (128-byte handle,
+ * CUDA IPC); the ranks exchange the handles out of band (rank order) and
+ * attach; bsm_pipeline_frame_bands_p2p_u8 computes the rank's row band with
+ * its vote-radius halo and its check and refine kernels store the band's
+ * final values straight into EVERY rank's map (NVLink P2P stores), returning
+ * once this rank's stores have completed.  After a barrier across the ranks
+ * (the caller's), bsm_frame_fetch reads the whole refined map on any rank.
+ * 1..8 ranks; destroy frames before their context. */
+typedef struct bsm_frame bsm_frame;
+int bsm_frame_create(bsm_ctx* ctx, int W, int H, int world, int rank, bsm_frame** out, uint8_t* handle128);
+int bsm_frame_attach(bsm_frame* frame, const uint8_t* handles /* world x 128 bytes, rank order */);
+int bsm_pipeline_frame_bands_p2p_u8(bsm_ctx* ctx, bsm_frame* frame, const uint8_t* left, const uint8_t* right,
+                                    const bsm_params* params);
+int bsm_frame_fetch(bsm_frame* frame, float* refined_d, uint8_t* refined_v);
+int bsm_frame_destroy(bsm_frame* frame);
+
 /* Instrumentation.  bsm_stream returns the cudaStream_t the context launches
  * on.  When profiling is enabled, bsm_last_timings reports the device time (ms)
  * of the last pipeline's kernels, in the order of bsm_timing_names. */

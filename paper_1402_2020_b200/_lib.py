@@ -109,6 +109,11 @@ _SIGS = {
     "bsm_comm_destroy": [_P],
     "bsm_pipeline_frame_bands_u8": [_P, _P, _P, _P, _I, _I, C.POINTER(bsm_params), _P, _P],
     "bsm_pipeline_pairs_sharded_u8": [_P, _P, _I, _P, _P, _I, _I, C.POINTER(bsm_params), _I, _P, _P],
+    "bsm_frame_create": [_P, _I, _I, _I, _I, C.POINTER(C.c_void_p), _P],
+    "bsm_frame_attach": [_P, _P],
+    "bsm_pipeline_frame_bands_p2p_u8": [_P, _P, _P, _P, C.POINTER(bsm_params)],
+    "bsm_frame_fetch": [_P, _P, _P],
+    "bsm_frame_destroy": [_P],
     "bsm_stream": [_P, C.POINTER(C.c_void_p)],
     "bsm_stream_wait": [_P, _P],
     "bsm_debug_check_guards": [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_int)],

@@ -264,3 +264,138 @@ int bsm_pipeline_pairs_sharded_u8(bsm_ctx* c, bsm_comm* m, int n_pairs, const ui
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// One frame over peer memory (BASELINE configs[4], the B200-first variant of
+// bsm_pipeline_frame_bands_u8): every rank owns a full-frame refined map in
+// device memory, exported with CUDA IPC; the ranks exchange the handles out of
+// band and map each other's maps; each rank's left/right check (K5) and
+// voting refinement (K6) then store its band's final values straight into
+// every rank's map over NVLink (P2P stores), so the all-gather is fused into
+// the kernels that produce the band -- no collective launch, no staging
+// buffer.  No kernel waits on another rank: the caller's barrier after the
+// call orders the stores before any rank reads its map (bsm_frame_fetch).
+struct bsm_frame {
+    bsm_ctx* ctx = nullptr;
+    int device = 0, W = 0, H = 0, world = 1, rank = 0;
+    float* d = nullptr;
+    uint8_t* v = nullptr;
+    float* peer_d[kMaxPeers] = {};
+    uint8_t* peer_v[kMaxPeers] = {};
+    bool attached = false;
+};
+
+extern "C" {
+
+int bsm_frame_create(bsm_ctx* c, int W, int H, int world, int rank, bsm_frame** out, uint8_t* handle) {
+    if (!c || !out || !handle) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    *out = nullptr;
+    BSM_TRY(check_dims(W, H));
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return set_err(world > kMaxPeers ? BSM_UNSUPPORTED : BSM_INVALID_ARGUMENT,
+                       "bsm: peer-memory frames take 1 to 8 ranks");
+    if (H < world) return set_err(BSM_INVALID_ARGUMENT, "bsm: fewer rows than ranks");
+    BSM_CUDA(cudaSetDevice(c->device));
+    bsm_frame* f = new bsm_frame();
+    f->ctx = c;
+    f->device = c->device;
+    f->W = W;
+    f->H = H;
+    f->world = world;
+    f->rank = rank;
+    const size_t px = size_t(W) * H;
+    cudaIpcMemHandle_t hd, hv;
+    cudaError_t e = cudaMalloc(&f->d, px * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&f->v, px);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hd, f->d);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hv, f->v);
+    if (e != cudaSuccess) {
+        bsm_frame_destroy(f);
+        return set_err(BSM_CUDA_ERROR, std::string("CUDA: frame allocation / IPC export: ") + cudaGetErrorString(e));
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(handle, &hd, 64);
+    std::memcpy(handle + 64, &hv, 64);
+    *out = f;
+    return BSM_OK;
+}
+
+int bsm_frame_attach(bsm_frame* f, const uint8_t* handles) {
+    if (!f || !handles) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    if (f->attached) return set_err(BSM_INVALID_ARGUMENT, "bsm: frame already attached");
+    BSM_CUDA(cudaSetDevice(f->device));
+    for (int r = 0; r < f->world; ++r) {
+        if (r == f->rank) {
+            f->peer_d[r] = f->d;
+            f->peer_v[r] = f->v;
+            continue;
+        }
+        cudaIpcMemHandle_t hd, hv;
+        std::memcpy(&hd, handles + size_t(r) * 128, 64);
+        std::memcpy(&hv, handles + size_t(r) * 128 + 64, 64);
+        void *pd = nullptr, *pv = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&pd, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&pv, hv, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+            return set_err(BSM_CUDA_ERROR, std::string("CUDA: opening rank ") + std::to_string(r) +
+                                               "'s frame: " + cudaGetErrorString(e));
+        f->peer_d[r] = static_cast<float*>(pd);
+        f->peer_v[r] = static_cast<uint8_t*>(pv);
+    }
+    f->attached = true;
+    return BSM_OK;
+}
+
+int bsm_pipeline_frame_bands_p2p_u8(bsm_ctx* c, bsm_frame* f, const uint8_t* left, const uint8_t* right,
+                                    const bsm_params* params) {
+    BSM_TRY(begin_call(c));
+    if (!f || f->ctx != c) return set_err(BSM_INVALID_ARGUMENT, "bsm: frame does not belong to this context");
+    if (!f->attached) return set_err(BSM_INVALID_ARGUMENT, "bsm: frame not attached (bsm_frame_attach)");
+    BSM_TRY(check_pattern(c));
+    BSM_TRY(validate_params(params));
+    if (!left || !right) return set_err(BSM_INVALID_ARGUMENT, "bsm: null image");
+    const int W = f->W, H = f->H;
+    int y0, y1;
+    band_of(H, f->world, f->rank, y0, y1);
+    BSM_TRY(upload_views(c, left, right, W, H));
+    PeerOut po{};
+    for (int r = 0; r < f->world; ++r) {
+        po.d[r] = f->peer_d[r];
+        po.v[r] = f->peer_v[r];
+    }
+    po.n = f->world;
+    po.W = W;
+    po.rb0 = y0 - std::max(0, y0 - params->vote_radius);  // the output band inside the halo band
+    po.g0 = y0;
+    c->peer = po;
+    const int rc = pipeline_device(c, u8views(c->img_l.as<uint8_t>(), c->img_r.as<uint8_t>()), W, H, y0, y1 - y0,
+                                   params, false);
+    c->peer = PeerOut{};
+    BSM_TRY(rc);
+    return sync(c);  // this rank's stores into every map have completed
+}
+
+int bsm_frame_fetch(bsm_frame* f, float* d, uint8_t* v) {
+    if (!f) return set_err(BSM_INVALID_ARGUMENT, "bsm: null frame");
+    BSM_CUDA(cudaSetDevice(f->device));
+    const size_t px = size_t(f->W) * f->H;
+    if (d) BSM_CUDA(cudaMemcpy(d, f->d, px * 4, cudaMemcpyDeviceToHost));
+    if (v) BSM_CUDA(cudaMemcpy(v, f->v, px, cudaMemcpyDeviceToHost));
+    return BSM_OK;
+}
+
+int bsm_frame_destroy(bsm_frame* f) {
+    if (!f) return BSM_OK;
+    cudaSetDevice(f->device);
+    for (int r = 0; r < f->world; ++r)
+        if (r != f->rank && f->peer_d[r]) {
+            cudaIpcCloseMemHandle(f->peer_d[r]);
+            cudaIpcCloseMemHandle(f->peer_v[r]);
+        }
+    if (f->d) cudaFree(f->d);
+    if (f->v) cudaFree(f->v);
+    delete f;
+    return BSM_OK;
+}
+
+}  // extern "C"

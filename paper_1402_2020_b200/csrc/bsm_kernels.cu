@@ -168,6 +168,7 @@ struct bsm_ctx {
     cudaEvent_t ev[T_COUNT][kEvPerSlot][2] = {};
     int ev_used[T_COUNT] = {};
     int launches = 0;
+    PeerOut peer{};  // peer-memory band outputs during bsm_pipeline_frame_bands_p2p_u8 (n = 0 otherwise)
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
     int maskf_force_low = 0;  // test hook (BSM_MASKF_FORCE_LOW=1): k_mask_f32 resolves every low byte
     int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4
@@ -498,8 +499,11 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
             k_make_vmap<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(cd, cv, gray, px, c->vmap.as<uint32_t>());
             BSM_TRY(check_launch(c, "make_vmap"));
             const size_t sm = fixed + size_t(warps) * 32 * 12 + size_t(warps) * np * nbins * 8;
-            auto kern = np == 4 ? (devexp ? k_vote_refine_fold<4, true> : k_vote_refine_fold<4, false>)
-                                : (devexp ? k_vote_refine_fold<1, true> : k_vote_refine_fold<1, false>);
+            const bool peer = c->peer.n > 0;  // the peer-storing kernels only for bsm_frame bands
+            auto kern = peer ? (np == 4 ? (devexp ? k_vote_refine_fold<4, true, true> : k_vote_refine_fold<4, false, true>)
+                                        : (devexp ? k_vote_refine_fold<1, true, true> : k_vote_refine_fold<1, false, true>))
+                             : (np == 4 ? (devexp ? k_vote_refine_fold<4, true, false> : k_vote_refine_fold<4, false, false>)
+                                        : (devexp ? k_vote_refine_fold<1, true, false> : k_vote_refine_fold<1, false, false>));
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
             const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
             BSM_CUDA(cudaMemsetAsync(c->counters.as<int>() + 2, 0, 4, c->stream));  // work counter
@@ -507,7 +511,7 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
                 c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
                 c->exp_dev, c->d_etab.as<unsigned long long>(), c->d_wtab.as<double>(), c->wt_ncol,
                 c->d_s2col.as<int16_t>(), c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(),
-                c->ref_v.as<uint8_t>(), c->counters.as<int>() + 2);
+                c->ref_v.as<uint8_t>(), c->counters.as<int>() + 2, c->peer);
             return check_launch(c, "vote_refine_fold");
         }
         if (lab) return set_err(BSM_UNSUPPORTED, "bsm: disparity range too wide for the colour refine bins");
@@ -516,10 +520,11 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
     BSM_TRY(ensure_weight_table(c, lc, le, radius));
     const int warps = std::max(1, std::min(8, int((96 * 1024) / (size_t(nbins) * 8))));
     const size_t sm = size_t(warps) * nbins * 8;
-    BSM_CUDA(cudaFuncSetAttribute(k_vote_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-    k_vote_refine<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
+    auto kvr = c->peer.n > 0 ? k_vote_refine<true> : k_vote_refine<false>;
+    BSM_CUDA(cudaFuncSetAttribute(kvr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    kvr<<<c->sm_count * 8, warps * 32, sm, c->stream>>>(
         cd, cv, gray, W, rows, radius, c->d_wtab.as<double>(), c->wt_ncol, c->d_s2col.as<int16_t>(),
-        c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(), c->ref_v.as<uint8_t>());
+        c->counters.as<int>(), c->inv.as<int>(), nbins, c->ref_d.as<float>(), c->ref_v.as<uint8_t>(), c->peer);
     return check_launch(c, "vote_refine");
 }
 
@@ -671,10 +676,10 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
         Scope s(c, T_LR);
         BSM_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
         const int tb = 256;
-        k_lr_check_keys<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(
+        (c->peer.n > 0 ? k_lr_check_keys<true> : k_lr_check_keys<false>)<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(
             c->keys_l.as<uint32_t>(), c->keys_r.as<uint32_t>(), W, rows, p->lr_tolerance, c->chk_d.as<float>(),
             c->chk_v.as<uint8_t>(), c->lw_d.as<float>(), c->rw_d.as<float>(), out0 - r0, out0 - r0 + out_rows,
-            c->counters.as<int>(), c->inv.as<int>());
+            c->counters.as<int>(), c->inv.as<int>(), c->peer);
         BSM_TRY(check_launch(c, "lr_check"));
         if (want_unmasked) {
             k_keys_to_float<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(c->keys_u.as<uint32_t>(), px,

@@ -3,15 +3,42 @@
 #pragma once
 
 // ---------------------------------------------------------------------------
+// Peer outputs of the frame-band partition over peer memory (bsm_frame,
+// bsm_dist.cuh): K5 and K6 also store the output band's final values straight
+// into every rank's full-frame map (own memory and peers' mapped by CUDA IPC),
+// so the all-gather is fused into the kernels that produce the band.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+    float* d[kMaxPeers];
+    uint8_t* v[kMaxPeers];
+    int n;    // ranks to store to; 0: none
+    int W;
+    int rb0;  // band-local first output row
+    int g0;   // its global row
+};
+
+template <bool PEER>
+__device__ __forceinline__ void peer_store(const PeerOut& po, int p, float d, uint8_t v) {
+    if (!PEER) return;
+    const int yy = p / po.W, x = p - yy * po.W;
+    const size_t g = size_t(po.g0 + yy - po.rb0) * po.W + x;
+    for (int k = 0; k < po.n; ++k) {
+        po.d[k][g] = d;
+        po.v[k][g] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5 -- left/right check on WTA keys.  refine.hpp:39-54: valid(x) <=>
 // xr = lround(x - dL) in [0, W) and |dL - dR(xr)| <= tol (inclusive, double).
 // Also emits the (all-valid) WTA maps as float when requested, the band-local
 // max_bin of the checked map (refine.hpp:68-72) and the list of invalid
 // pixels in the refine band [rb0, rb1).
+template <bool PEER>
 __global__ void k_lr_check_keys(const uint32_t* __restrict__ kl, const uint32_t* __restrict__ kr, int W,
                                 int rows, double tol, float* __restrict__ chk_d, uint8_t* __restrict__ chk_v,
                                 float* __restrict__ left_d, float* __restrict__ right_d, int rb0, int rb1,
-                                int* __restrict__ counters, int* __restrict__ inv) {
+                                int* __restrict__ counters, int* __restrict__ inv, const PeerOut po) {
     const size_t total = size_t(rows) * W;
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = i < total;
@@ -29,6 +56,7 @@ __global__ void k_lr_check_keys(const uint32_t* __restrict__ kl, const uint32_t*
         chk_v[i] = ok ? 1 : 0;
         if (left_d) left_d[i] = float(dl);
         if (right_d) right_d[i] = float(kr[i] & 0xFFFFu);
+        if (yy >= rb0 && yy < rb1) peer_store<PEER>(po, int(i), float(dl), ok ? 1 : 0);  // K6 overwrites the invalid ones
     }
     const unsigned full = 0xFFFFFFFFu;
     const int mb = __reduce_max_sync(full, (in && ok) ? dl : 0);
@@ -98,11 +126,12 @@ __global__ void k_lr_check_float(const float* __restrict__ dl, const float* __re
 // row-major voter order (the owner lane of a bin performs its adds in
 // sequence), so every bin sum is bit-identical to the reference's.  Argmax:
 // strict '>' from bin 0 == smallest bin among the maxima.
+template <bool PEER>
 __global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __restrict__ cv,
                               const uint8_t* __restrict__ gray, int W, int rows, int radius,
                               const double* __restrict__ wtab, int ncol, const int16_t* __restrict__ s2col,
                               const int* __restrict__ counters, const int* __restrict__ inv,
-                              int nbins_cap, float* __restrict__ od, uint8_t* __restrict__ ov) {
+                              int nbins_cap, float* __restrict__ od, uint8_t* __restrict__ ov, const PeerOut po) {
     extern __shared__ __align__(16) double sbins[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     double* bins = sbins + size_t(warp) * nbins_cap;
@@ -149,6 +178,7 @@ __global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __res
             if (lane == 0) {
                 od[p] = 0.0f;
                 ov[p] = 0;
+                peer_store<PEER>(po, p, 0.0f, 0);
             }
             continue;
         }
@@ -171,6 +201,7 @@ __global__ void k_vote_refine(const float* __restrict__ cd, const uint8_t* __res
         if (lane == 0) {
             od[p] = float(bb);
             ov[p] = 1;
+            peer_store<PEER>(po, p, float(bb), 1);
         }
         __syncwarp();
     }
@@ -263,13 +294,13 @@ __device__ __forceinline__ double exp_glibc(double x, const ExpDev& p, const uns
 // current bin's running sum in a register.  Per bin the additions are
 // therefore the reference's row-major sequence; the NP pixels fold side by
 // side.
-template <int NP, bool DEVEXP>
+template <int NP, bool DEVEXP, bool PEER>
 __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
     const uint32_t* __restrict__ vmap, const float4* __restrict__ lab, const float* __restrict__ lab256, int W,
     int rows, int radius, double lc, const double* __restrict__ e_over_le, ExpDev ep,
     const unsigned long long* __restrict__ etab, const double* __restrict__ wtab, int ncol,
     const int16_t* __restrict__ s2col, const int* __restrict__ counters, const int* __restrict__ inv, int nbins_cap,
-    float* __restrict__ od, uint8_t* __restrict__ ov, int* __restrict__ work) {
+    float* __restrict__ od, uint8_t* __restrict__ ov, int* __restrict__ work, const PeerOut po) {
     constexpr int LPP = 32 / NP;
     extern __shared__ __align__(16) double fsm[];
     unsigned long long* stab = reinterpret_cast<unsigned long long*>(fsm);  // 256 (DEVEXP)
@@ -431,6 +462,7 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
         if (live && sl == 0) {
             od[p] = any ? float(bb) : 0.0f;
             ov[p] = any ? 1 : 0;
+            peer_store<PEER>(po, p, any ? float(bb) : 0.0f, any ? 1 : 0);
         }
         __syncwarp();
     }

@@ -11,7 +11,9 @@ thin Python caller:
 * one large frame (configs[4]): contiguous row bands (``band_rows``).  Every
   rank holds both full views and computes its band with a vote-radius halo of
   redundant rows, so the only exchange is the final all-gather of the refined
-  bands (``bsm_pipeline_frame_bands_u8``: ncclAllGather).  A band-local
+  bands (``bsm_pipeline_frame_bands_u8``: ncclAllGather), or, with
+  ``transport="p2p"``, no collective at all: the check and refine kernels
+  store the band into every rank's map over peer memory (``bsm_frame``).  A band-local
   ``max_bin`` is safe: bins above it are 0 for every pixel of the band and
   cannot win the strict-'>' argmax (refine.hpp:102-105).
 
@@ -150,10 +152,53 @@ def gather_pairs(results: List[Tuple[int, DisparityMap]], n_units: int, shape: T
     return out  # type: ignore[return-value]
 
 
+class Frame:
+    """A bsm_frame: this rank's full-frame refined map in device memory,
+    exported through CUDA IPC and attached to every other rank's map (the
+    handles travel through the torch.distributed group)."""
+
+    def __init__(self, ctx: Context, W: int, H: int, group=None):
+        import torch.distributed as dist
+        self.ctx = ctx
+        self.W, self.H = W, H
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        h = C.c_void_p()
+        handle = (C.c_uint8 * 128)()
+        check(lib().bsm_frame_create(ctx.handle, W, H, self.world, self.rank, C.byref(h), handle))
+        self._h = h
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        allh = (C.c_uint8 * (128 * self.world)).from_buffer_copy(b"".join(handles))
+        check(lib().bsm_frame_attach(self._h, allh))
+
+    def fetch(self) -> DisparityMap:
+        d = np.empty((self.H, self.W), np.float32)
+        v = np.empty((self.H, self.W), np.uint8)
+        check(lib().bsm_frame_fetch(self._h, d.ctypes.data, v.ctypes.data))
+        return DisparityMap(d, v)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bsm_frame_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def run_frame_bands(left, right, cfg: BsmConfig, pattern: Optional[SamplingPattern] = None, group=None,
-                    ctx: Optional[Context] = None) -> DisparityMap:
+                    ctx: Optional[Context] = None, transport: str = "auto") -> DisparityMap:
     """run_pipeline(...).refined of one frame, row-band partitioned over the
-    group; every rank returns the whole refined map."""
+    group; every rank returns the whole refined map.
+
+    transport: "nccl" (bsm_pipeline_frame_bands_u8: one ncclAllGather of the
+    bands), "p2p" (bsm_frame: the check and refine kernels store each band
+    straight into every rank's map over peer memory; one barrier), "group"
+    (the band through run_pipeline_band, gathered by the group's own
+    collective); "auto" = "nccl" with an NCCL group, else "group"."""
     import torch.distributed as dist
     L, R = _u8(left, "left"), _u8(right, "right")
     if L.shape != R.shape:
@@ -162,7 +207,21 @@ def run_frame_bands(left, right, cfg: BsmConfig, pattern: Optional[SamplingPatte
     pattern = pattern or generate_pattern(cfg=cfg)
     ctx = ctx or default_context()
     H, W = L.shape
-    if _is_nccl(group):
+    if transport == "auto":
+        transport = "nccl" if _is_nccl(group) else "group"
+    if transport == "p2p":
+        ctx.set_pattern(pattern)
+        frame = Frame(ctx, W, H, group)
+        try:
+            p = _params(cfg)
+            check(lib().bsm_pipeline_frame_bands_p2p_u8(ctx.handle, frame._h, L.ctypes.data, R.ctypes.data,
+                                                        C.byref(p)))
+            dist.barrier(group=group)  # every rank's stores have completed
+            return frame.fetch()
+        finally:
+            dist.barrier(group=group)  # no rank unmaps a frame another rank still writes
+            frame.close()
+    if transport == "nccl":
         ctx.set_pattern(pattern)
         comm = _comm_for(ctx, group)
         d = np.empty((H, W), np.float32)

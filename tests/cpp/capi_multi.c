@@ -6,7 +6,8 @@
  * pairs.raw: N pairs of (left, right) W*H uint8 views back to back (N from the
  * file size).  out.bin: the batch's N refined maps (float W*H then uint8 W*H
  * each), then the frame-band result of pair 0, then the sharded-pairs result
- * of every pair, in the same format.  Exit status: 0 ok, else the failing
+ * of every pair, then the peer-memory frame-band result of pair 1, in the same
+ * format.  Exit status: 0 ok, else the failing
  * call's status. */
 #include <stdint.h>
 #include <stdio.h>
@@ -76,6 +77,16 @@ int main(int argc, char** argv) {
         fwrite(od[i], 4, px, o);
         fwrite(ov[i], 1, px, o);
     }
+    /* peer-memory frame bands at world 1: the band is the whole frame */
+    bsm_frame* frame = NULL;
+    uint8_t handle[128];
+    TRY(bsm_frame_create(ctx, W, H, 1, 0, &frame, handle));
+    TRY(bsm_frame_attach(frame, handle));
+    TRY(bsm_pipeline_frame_bands_p2p_u8(ctx, frame, lefts[1], rights[1], &p));
+    TRY(bsm_frame_fetch(frame, od[1], ov[1]));
+    fwrite(od[1], 4, px, o);
+    fwrite(ov[1], 1, px, o);
+    TRY(bsm_frame_destroy(frame));
     fclose(o);
     TRY(bsm_comm_destroy(comm));
     TRY(bsm_ctx_destroy(ctx));

@@ -234,8 +234,8 @@ def test_c_client_batch_and_nccl_match_reference(tmp_path, ref, default_pairs):
     px = W * H
     maps = [(raw[k * 5 * px:k * 5 * px + 4 * px].view(np.float32).reshape(H, W),
              raw[k * 5 * px + 4 * px:(k + 1) * 5 * px].reshape(H, W)) for k in range(len(raw) // (5 * px))]
-    assert len(maps) == 3 + 1 + 3
+    assert len(maps) == 3 + 1 + 3 + 1
     want = [ref.pipeline(l, r, default_pairs, 26, D, threads=8) for l, r in pairs]
-    got_order = [0, 1, 2, 0, 0, 1, 2]  # batch, frame bands of pair 0, sharded pairs
+    got_order = [0, 1, 2, 0, 0, 1, 2, 1]  # batch, frame bands of pair 0, sharded pairs, p2p frame of pair 1
     for (d, v), i in zip(maps, got_order):
         assert np.array_equal(d, want[i]["refined_d"]) and np.array_equal(v, want[i]["refined_v"])

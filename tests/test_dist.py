@@ -112,10 +112,11 @@ def _compute_worker(rank, world, port, q, kind):
         from paper_1402_2020_b200 import dist as bd
         from paper_1402_2020_b200.synth import workload_pair
         ctx = bsm.Context(0)
-        if kind == "bands":
+        if kind in ("bands", "p2p"):
             g = json.load(open(os.path.join(GOLDEN, "c5.json")))
             left, right = workload_pair("c5")
-            m = bd.run_frame_bands(left, right, bsm.BsmConfig(d_max=g["d_max"]), ctx=ctx)
+            m = bd.run_frame_bands(left, right, bsm.BsmConfig(d_max=g["d_max"]), ctx=ctx,
+                                   transport="p2p" if kind == "p2p" else "auto")
             q.put((rank, sha(m.disparity) == g["maps"]["refined_d"] and sha(m.valid) == g["maps"]["refined_v"]))
         else:
             gs = [json.load(open(os.path.join(GOLDEN, f"c4_{i}.json"))) for i in range(5)]
@@ -135,9 +136,12 @@ def _compute_worker(rank, world, port, q, kind):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", ["bands", "pairs"])
+@pytest.mark.parametrize("kind", ["bands", "pairs", "p2p"])
 def test_real_compute_world2_matches_reference(kind):
-    need = ["c5"] if kind == "bands" else [f"c4_{i}" for i in range(5)]
+    """p2p: the two processes map each other's full-frame maps (CUDA IPC) and
+    their check / refine kernels store each band into both (bsm_frame); no
+    kernel waits on the other process -- the barrier is on the host."""
+    need = ["c5"] if kind in ("bands", "p2p") else [f"c4_{i}" for i in range(5)]
     if not all(os.path.exists(os.path.join(GOLDEN, f"{t}.json")) for t in need):
         pytest.skip("goldens not generated")
     assert _spawn(_compute_worker, 2, kind) == {0: True, 1: True}
