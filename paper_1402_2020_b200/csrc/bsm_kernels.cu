@@ -225,7 +225,7 @@ int check_launch(bsm_ctx* c, const char* what) {
 // Tile-relative offset tables depend on the staged tile width.
 int desc4_tile_width(int half) { return round_up(kD2TX * 4 + 2 * half + 8, 16); }
 
-// k_descriptor4's per-pair table: word offsets of both endpoints in its
+// k_descriptor4's per-pair table: byte offsets (4 x word offsets) of both endpoints in its
 // phased 4-byte-window tile, relative to the thread's base word:
 // (half + px) % 4 selects the phase plane, py*TWs/4 + (half + px)/4 the word.
 int ensure_desc4_table(bsm_ctx* c) {
@@ -237,7 +237,7 @@ int ensure_desc4_table(bsm_ctx* c) {
         const int16_t* p = &c->pairs[4 * size_t(c->order[size_t(i)])];
         const int TH = kD2TY * kD2Rows + 2 * c->half, S4 = TWs * TH / 4;
         auto woff = [&](int px, int py) { return ((c->half + px) & 3) * S4 + py * (TWs / 4) + ((c->half + px) >> 2); };
-        t[size_t(i)] = make_int2(woff(p[0], p[1]), woff(p[2], p[3]));
+        t[size_t(i)] = make_int2(4 * woff(p[0], p[1]), 4 * woff(p[2], p[3]));  // byte offsets
     }
     BSM_TRY(c->d_desc4.ensure(t.size() * sizeof(int2)));
     BSM_CUDA(cudaMemcpy(c->d_desc4.p, t.data(), t.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -543,7 +543,7 @@ int validate_params(const bsm_params* p) {
 // The fused device pipeline.  Views are full W x H device images; the
 // refined output covers rows [out0, out0 + out_rows); fields, WTA and the
 // check cover the halo-extended rows [r0, r1).
-// k_descriptor_f32's per-pair table: tile-relative offsets py*TW + px.
+// k_descriptor_f32's per-pair table: tile-relative byte offsets 4 (py*TW + px).
 int ensure_descf_table(bsm_ctx* c) {
     const int TW = kDfTX + 2 * c->half;
     if (c->descf_tw == TW) return BSM_OK;
@@ -551,7 +551,7 @@ int ensure_descf_table(bsm_ctx* c) {
     std::vector<int2> t(size_t(G) * 32, make_int2(0, 0));
     for (int i = 0; i < c->n; ++i) {
         const int16_t* p = &c->pairs[4 * size_t(c->order[size_t(i)])];
-        t[size_t(i)] = make_int2(p[1] * TW + p[0], p[3] * TW + p[2]);
+        t[size_t(i)] = make_int2(4 * (p[1] * TW + p[0]), 4 * (p[3] * TW + p[2]));  // byte offsets
     }
     BSM_TRY(c->d_descf.ensure(t.size() * sizeof(int2)));
     BSM_CUDA(cudaMemcpy(c->d_descf.p, t.data(), t.size() * sizeof(int2), cudaMemcpyHostToDevice));

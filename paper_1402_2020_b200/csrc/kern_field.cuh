@@ -22,6 +22,12 @@ __device__ __forceinline__ uint32_t bytes_gt(uint32_t p, uint32_t q) {
     return ~ge & 0x80808080u;
 }
 
+// The word at byte offset `off` from `base` (the pair table holds byte
+// offsets, so a tile address is one add: no per-load shift).
+__device__ __forceinline__ uint32_t ld_off(const uint32_t* base, int off) {
+    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(base) + off);
+}
+
 __global__ void __launch_bounds__(kD2TX* kD2TY)
     k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
                   const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wq, size_t P,
@@ -73,7 +79,7 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
                 const int2 e = __ldg(ptab + 32 * w + k);  // tile-relative offsets of p and q
 #pragma unroll
                 for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t f = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]);  // bit 7 of byte j: pixel j
+                    const uint32_t f = bytes_gt(ld_off(tb + r * rowW, e.x), ld_off(tb + r * rowW, e.y));  // bit 7 of byte j: pixel j
                     // pair k -> bit (k & 7) of byte lane j of acc[k >> 3]
                     acc[r][k >> 3] |= (f >> (7 - (k & 7)));
                 }
@@ -83,7 +89,7 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
                 const int2 e = __ldg(ptab + 32 * w + k);
 #pragma unroll
                 for (int r = 0; r < kD2Rows; ++r) {
-                    const uint32_t v = bytes_gt(tb[r * rowW + e.x], tb[r * rowW + e.y]) >> (7 - (k & 7));
+                    const uint32_t v = bytes_gt(ld_off(tb + r * rowW, e.x), ld_off(tb + r * rowW, e.y)) >> (7 - (k & 7));
                     switch (k >> 3) {
                         case 0: acc[r][0] |= v; break;
                         case 1: acc[r][1] |= v; break;
@@ -496,6 +502,11 @@ __global__ void k_lab3_to_lab4(const float* __restrict__ lab, size_t n, float4* 
 // 214-230).  Thread per pixel column x 4 rows; clamped float tile.
 constexpr int kDfTX = 32, kDfTY = 8, kDfPY = 4;
 
+// The float at byte offset `off` from `base` (the pair table holds byte offsets).
+__device__ __forceinline__ float ldf_off(const float* base, int off) {
+    return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + off);
+}
+
 __global__ void __launch_bounds__(kDfTX* kDfTY)
     k_descriptor_f32(const float* __restrict__ gray, int W, int H, int ybeg, int rows, const int2* __restrict__ offs,
                      int n, int half, int NW, int Wq, size_t P, uint32_t* __restrict__ desc) {
@@ -522,13 +533,14 @@ __global__ void __launch_bounds__(kDfTX* kDfTY)
                 const int2 o = __ldg(offs + 32 * w + k);  // tile-relative (py*TW + px) of p and q
 #pragma unroll
                 for (int j = 0; j < kDfPY; ++j)
-                    if (t0[j * TW + o.x] > t0[j * TW + o.y]) acc[j] |= 1u << k;
+                    if (ldf_off(t0 + j * TW, o.x) > ldf_off(t0 + j * TW, o.y)) acc[j] |= 1u << k;
             }
         } else {
             for (int k = 0; k < cnt; ++k) {
                 const int2 o = __ldg(offs + 32 * w + k);
 #pragma unroll
-                for (int j = 0; j < kDfPY; ++j) acc[j] |= uint32_t(t0[j * TW + o.x] > t0[j * TW + o.y]) << k;
+                for (int j = 0; j < kDfPY; ++j)
+                    acc[j] |= uint32_t(ldf_off(t0 + j * TW, o.x) > ldf_off(t0 + j * TW, o.y)) << k;
             }
         }
 #pragma unroll
