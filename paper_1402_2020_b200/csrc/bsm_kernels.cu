@@ -62,6 +62,7 @@ inline size_t field_plane(int W, int rows) {
 
 #include "kern_field.cuh"
 #include "kern_cost.cuh"
+#include "kern_cost_tc.cuh"
 #include "kern_refine.cuh"
 #include "kern_misc.cuh"
 
@@ -174,7 +175,8 @@ struct bsm_ctx {
     int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
-                     // 2 x SMs tiles
+                     // 2 x SMs tiles, bit 4 the popcount kernel instead of
+                     // the tensor-core one (bits 0-3 apply to the popcount kernel)
     DevBuf popc_out;
     // batch pipelining (bsm_pipeline_batch_u8): two slots of input views and
     // refined maps, an H2D and a D2H copy stream ordered by events
@@ -381,7 +383,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
 // WTA keys of rows [0, rows) of device fields (SoA); keys: rows x W.
 // Tensor map of a device field [NW][P] u32 for TMA boxes of box_x pixels x
 // kCostK words; out-of-range boxes read zeros.
-int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int rows, int box_x) {
+int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int rows, int box_x,
+                     int box_w = kCostK) {
     static PFN_cuTensorMapEncodeTiled encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -394,7 +397,7 @@ int field_tensor_map(CUtensorMap* map, const uint32_t* field, int W, int NW, int
     const size_t P = field_plane(W, rows);
     const cuuint64_t dims[2] = {cuuint64_t(P), cuuint64_t(NW)};
     const cuuint64_t strides[1] = {cuuint64_t(P) * 4};
-    const cuuint32_t box[2] = {cuuint32_t(box_x), cuuint32_t(kCostK)};
+    const cuuint32_t box[2] = {cuuint32_t(box_x), cuuint32_t(box_w)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(field), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -419,9 +422,52 @@ int k3_group(const bsm_ctx* c, int tiles) {
     return 1;
 }
 
+// K3 on the tensor cores (kern_cost_tc.cuh): persistent CTAs, one per SM.
+// d-blocks of at most kTcMaxDc disparities; with several, each starts on a
+// multiple of 4 (TMA box alignment) and they merge with atomicMin.
+int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_t* dr, const uint32_t* mr, int W,
+                  int rows, int d_max, bool both, int dir, bool masked, uint32_t* keys_l, uint32_t* keys_r) {
+    const int Wq = field_pitch(W);
+    const int ndd = (d_max + kTcMaxDc - 1) / kTcMaxDc;
+    const int Dc = ndd == 1 ? d_max : round_up((d_max + ndd - 1) / ndd, 4);
+    const int ncols = round_up(kTcRows + ((Dc + 2) & ~3), 32);
+    const bool use_l = both || dir == 0, use_r = both || dir == 1;
+    if (ndd > 1) {
+        if (use_l) BSM_CUDA(cudaMemsetAsync(keys_l, 0xFF, size_t(rows) * W * 4, c->stream));
+        if (use_r) BSM_CUDA(cudaMemsetAsync(keys_r, 0xFF, size_t(rows) * W * 4, c->stream));
+    }
+    const long long npix = static_cast<long long>(rows) * Wq;
+    const long long tiles = (npix + kTcRows - 1) / kTcRows;
+    const int ndir = both ? 2 : 1;
+    if (tiles * ndd * ndir > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel");
+    const int items = int(tiles * ndd * ndir);
+    CUtensorMap lr, lm, lo, rr, rm, ro;  // unused slots are copies of a valid map
+    const uint32_t* ml_ = ml ? ml : dl;
+    const uint32_t* mr_ = mr ? mr : dr;
+    BSM_TRY(field_tensor_map(&lr, use_l ? dl : dr, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&lm, use_l ? ml_ : mr_, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, ncols / 2, kTcKS));
+    BSM_TRY(field_tensor_map(&rr, use_r ? dr : dl, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&rm, use_r ? mr_ : ml_, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
+    // at least 116 KB so that a second CTA never shares an SM (and its TMEM)
+    const size_t sm = std::max<size_t>(TcSmem(ncols, masked).total, 116 * 1024);
+    const int grid = std::min(items, c->sm_count);
+    auto launch = [&](auto kern) -> int {
+        BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        kern<<<grid, kTcThreads, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, int(npix), c->NW, d_max, Dc, ncols,
+                                                  ndd, ndir, both ? 0 : dir, items, keys_l, keys_r);
+        return BSM_OK;
+    };
+    BSM_TRY(masked ? launch(k_cost_wta_tc<true>) : launch(k_cost_wta_tc<false>));
+    return check_launch(c, "cost_wta_tc");
+}
+
 int wta_device(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint32_t* dr, const uint32_t* mr, int W,
                int rows, int d_max, bool both, int dir, bool masked, uint32_t* keys_l, uint32_t* keys_r, int timing) {
     Scope s(c, timing);
+    // default: the tensor-core kernel; BSM_K3_VARIANT bit 4 selects the popcount kernel
+    if (!(c->k3_variant & 16)) return wta_device_tc(c, dl, ml, dr, mr, W, rows, d_max, both, dir, masked, keys_l, keys_r);
     const int Wq = field_pitch(W);
     const int dz = (d_max + kCostDisp - 1) / kCostDisp;
     const bool use_l = both || dir == 0, use_r = both || dir == 1;
