@@ -441,22 +441,21 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
     const int ndir = both ? 2 : 1;
     if (tiles * ndd * ndir > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel");
     const int items = int(tiles * ndd * ndir);
-    CUtensorMap lr, lm, lo, rr, rm, ro;  // unused slots are copies of a valid map
+    CUtensorMap lo, ro;  // span words of the other view; an unused slot is a copy of a valid map
+    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, ncols / 2, kTcKS));
+    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
     const uint32_t* ml_ = ml ? ml : dl;
     const uint32_t* mr_ = mr ? mr : dr;
-    BSM_TRY(field_tensor_map(&lr, use_l ? dl : dr, W, c->NW, rows, kTcRows, kTcKS));
-    BSM_TRY(field_tensor_map(&lm, use_l ? ml_ : mr_, W, c->NW, rows, kTcRows, kTcKS));
-    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, ncols / 2, kTcKS));
-    BSM_TRY(field_tensor_map(&rr, use_r ? dr : dl, W, c->NW, rows, kTcRows, kTcKS));
-    BSM_TRY(field_tensor_map(&rm, use_r ? mr_ : ml_, W, c->NW, rows, kTcRows, kTcKS));
-    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
-    // at least 116 KB so that a second CTA never shares an SM (and its TMEM)
-    const size_t sm = std::max<size_t>(TcSmem(ncols, masked).total, 116 * 1024);
+    const TcSmem L(ncols);
+    if (L.nraw < 2) return set_err(BSM_UNSUPPORTED, "bsm: cost kernel shared-memory layout");
+    const size_t sm = L.total;  // > 114 KB: one CTA per SM (it allocates all 512 TMEM columns)
     const int grid = std::min(items, c->sm_count);
     auto launch = [&](auto kern) -> int {
         BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<grid, kTcThreads, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, int(npix), c->NW, d_max, Dc, ncols,
-                                                  ndd, ndir, both ? 0 : dir, items, keys_l, keys_r);
+        kern<<<grid, kTcThreads, sm, c->stream>>>(lo, ro, use_l ? dl : dr, use_l ? ml_ : mr_, use_r ? dr : dl,
+                                                  use_r ? mr_ : ml_, W, Wq, int(npix), int(field_plane(W, rows)),
+                                                  c->NW, d_max, Dc, ncols, ndd, ndir, both ? 0 : dir, items, keys_l,
+                                                  keys_r);
         return BSM_OK;
     };
     BSM_TRY(masked ? launch(k_cost_wta_tc<true>) : launch(k_cost_wta_tc<false>));

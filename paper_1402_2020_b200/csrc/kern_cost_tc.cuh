@@ -22,15 +22,16 @@
 // boundary), so one accumulator of 128 TMEM lanes x ncols (128 + dq rounded up
 // to 32) columns holds every cost the tile needs; row r uses columns r + u,
 // u in [0, dq].
-// Per stage of kTcKS u32 words (kTcKS MMA K-steps of 32 int8):
-//   * a loader thread brings the packed words with TMA (2-D boxes of the word
-//     planes: reference desc + mask [KS x 128], span [KS x ncols] as two
-//     boxes) into a ring of kTcRawStages slots, zero-filled outside the
-//     field; ~60 KB per SM in flight covers the DRAM latency of the
-//     compulsory misses;
-//   * 16 producer warps expand them: the A rows into TMEM (tcgen05.st, ring
-//     of kTcStages x 32 columns), the B rows into shared memory (canonical
-//     no-swizzle K-major layout, ring of kTcStages slots);
+// Per stage of kTcKS (8) u32 words (8 MMA K-steps of 32 int8):
+//   * a loader thread brings the span's packed words with TMA (two 2-D boxes
+//     [KS x ncols/2] of the other view's word planes) into a ring of as many
+//     slots as fit in shared memory (2..8), zero-filled outside the field;
+//   * 16 B-producer warps expand them into the B rows of the stage in shared
+//     memory (canonical no-swizzle K-major layout, ring of kTcStages slots);
+//   * 8 A-producer warps (2 per TMEM lane quarter) load the reference desc and
+//     mask words with plain loads, prefetched one stage ahead, and write the A
+//     rows into TMEM (tcgen05.st, ring of kTcStages x 64 columns) -- they write
+//     no shared memory, so no proxy fence drains their loads;
 //   * one thread issues the MMAs (N <= 256 each, two per K-step for
 //     ncols > 256) and commits the slot back to the producers;
 //   * after the last stage, four epilogue warps read their 32 lanes'
@@ -40,21 +41,28 @@
 // CTAs are persistent (one per SM: the whole 512-column TMEM), walking the
 // (tile, direction x d-block) items tile-major like k_cost_wta.
 #pragma once
+#ifndef BSM_TC_ABL
+#define BSM_TC_ABL 0  // ablation bits for experiments (tools/microbench/tc_probe): 0 in the library
+#endif
 
 constexpr int kTcRows = 128;                      // MMA M: reference pixels per tile
-constexpr int kTcKS = 4;                          // u32 words (MMA K-steps) per stage
-constexpr int kTcStages = 3;                      // expanded ring (smem B + TMEM A)
-constexpr int kTcRawStages = 6;                   // TMA ring of packed words
+constexpr int kTcKS = 8;                          // u32 words (MMA K-steps) per stage
+constexpr int kTcStages = 2;                      // expanded ring (smem B + TMEM A)
+constexpr int kTcMaxRaw = 8;                      // TMA ring of packed span words (as many as fit)
 constexpr int kTcMaxDc = 256;                     // disparities per d-block
-constexpr int kTcMaxCols = 384;                   // accumulator columns (127 + 256 -> 384)
+constexpr int kTcMaxCols = 384;                   // accumulator columns (128 + 256 -> 384)
 constexpr int kTcAcol = kTcMaxCols;               // first TMEM column of the A ring
-constexpr int kTcProdWarps = 16;                  // warp w: TMEM lane quarter w & 3, word w >> 2
-constexpr int kTcEpiWarps = 4;
-constexpr int kTcMmaWarp = kTcProdWarps + kTcEpiWarps;
-constexpr int kTcLoadWarp = kTcMmaWarp + 1;
-constexpr int kTcThreads = (kTcLoadWarp + 1) * 32;
-static_assert(kTcProdWarps == 4 * kTcKS, "one producer warp per (lane quarter, word of the stage)");
+constexpr uint32_t kTcSmemLimit = 227 * 1024;     // dynamic shared memory per CTA
+constexpr int kTcBWarps = 16;                     // B producers: warps 0-15
+constexpr int kTcEpiWarps = 4;                    // epilogue: warps 16-19 (lane quarters 0-3)
+constexpr int kTcMmaWarp = kTcBWarps + kTcEpiWarps;  // 20; the TMA loader is warp 21
+constexpr int kTcAWarp0 = kTcMmaWarp + 2;         // A producers: warps 22-29
+constexpr int kTcAHalves = 2;                     // A producer warps per lane quarter
+constexpr int kTcAWarps = 4 * kTcAHalves;
+constexpr int kTcThreads = (kTcAWarp0 + kTcAWarps) * 32;
+constexpr int kTcBTasks = (kTcMaxCols * kTcKS + kTcBWarps * 32 - 1) / (kTcBWarps * 32);  // (row, word) per thread
 static_assert(kTcAcol + kTcStages * kTcKS * 8 <= 512, "TMEM: accumulator + A ring");
+static_assert(kTcKS % (2 * kTcAHalves) == 0, "A producers store 2 words per tcgen05.st");
 
 __device__ __forceinline__ uint32_t tc_sign_bytes(uint32_t x) {
     // each byte -> 0xFF if its top bit is set, else 0x00 (prmt sign replicate)
@@ -62,6 +70,21 @@ __device__ __forceinline__ uint32_t tc_sign_bytes(uint32_t x) {
     asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(x));
     return r;
 }
+// mbarrier wait with a suspend-time hint (ns): the hardware may park the
+// thread until the phase completes instead of re-polling (measured: the same
+// speed as the plain try_wait loop at 200 ns .. 20 us hints).
+__device__ __forceinline__ void tc_wait(uint32_t bar_saddr, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TCW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra TCW_%=;\n"
+        "}\n" ::"r"(bar_saddr),
+        "r"(parity), "n"(20000)
+        : "memory");
+}
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) { tc_wait(smem_addr(bar), parity); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr) {
@@ -118,59 +141,73 @@ __device__ __forceinline__ TcItem tc_item(int it, int ndd, int ndir, int dir0, i
     return TcItem{tile * kTcRows, dir, d0, dc, (dc + 2) & ~3};
 }
 
-// Shared memory carve-up (bytes), shared by the kernel and the host.
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+// Shared memory carve-up (bytes), shared by the kernel and the host: the
+// expanded B ring, the TMA ring of packed span words (as many stages as fit,
+// at most kTcMaxRaw), the per-tile popcount bases and the barriers.
 struct TcSmem {
-    uint32_t sub, stage, raw_a, raw, b_ring, raw_ring, base, bars, total;
-    __host__ __device__ TcSmem(int ncols, bool masked) {
-        sub = uint32_t(ncols) * 32u;                                      // one K-step of B rows
-        stage = sub * kTcKS;                                              // expanded B stage
-        raw_a = kTcKS * kTcRows * 4u;                                     // one [KS x 128] word box
-        raw = raw_a * (masked ? 2u : 1u) + kTcKS * uint32_t(ncols) * 4u;  // packed words of a stage
+    uint32_t sub, stage, raw, nraw, b_ring, raw_ring, base, bars, total;
+    __host__ __device__ explicit TcSmem(int ncols) {
+        sub = uint32_t(ncols) * 32u;                 // one K-step of B rows
+        stage = sub * kTcKS;                         // expanded B stage
+        raw = kTcKS * uint32_t(ncols) * 4u;          // packed span words of a stage
         b_ring = 0;
         raw_ring = b_ring + kTcStages * stage;
-        base = raw_ring + kTcRawStages * raw;
-        bars = base + 2 * kTcKS * kTcRows * 4;
-        total = bars + (2 * kTcStages + 2 * kTcRawStages + 6) * 8 + 16;
+        const uint32_t fixed = 2 * kTcAHalves * kTcRows * 4 + (2 * kTcStages + 2 * kTcMaxRaw + 6) * 8 + 16;
+        const uint32_t room = kTcSmemLimit > raw_ring + fixed ? kTcSmemLimit - raw_ring - fixed : 0;
+        nraw = room / raw < uint32_t(kTcMaxRaw) ? room / raw : uint32_t(kTcMaxRaw);
+        base = raw_ring + nraw * raw;
+        bars = base + 2 * kTcAHalves * kTcRows * 4;
+        total = bars + (2 * kTcStages + 2 * kTcMaxRaw + 6) * 8 + 16;
     }
 };
 
 template <bool MASKED>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    k_cost_wta_tc(const __grid_constant__ CUtensorMap l_ref, const __grid_constant__ CUtensorMap l_mask,
-                  const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_ref,
-                  const __grid_constant__ CUtensorMap r_mask, const __grid_constant__ CUtensorMap r_oth, int W,
-                  int Wq, int npix, int NW, int D, int Dc, int ncols, int ndd, int ndir, int dir0, int items,
+    k_cost_wta_tc(const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_oth,
+                  const uint32_t* __restrict__ l_ref, const uint32_t* __restrict__ l_mask,
+                  const uint32_t* __restrict__ r_ref, const uint32_t* __restrict__ r_mask, int W, int Wq, int npix,
+                  int P, int NW, int D, int Dc, int ncols, int ndd, int ndir, int dir0, int items,
                   uint32_t* __restrict__ keys_l, uint32_t* __restrict__ keys_r) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    const TcSmem L(ncols, MASKED);
+    const TcSmem L(ncols);
     uint8_t* sB = tsm + L.b_ring;                                        // [S][KS][ncols rows x 32 B]
-    uint32_t* sraw = reinterpret_cast<uint32_t*>(tsm + L.raw_ring);      // [RS][desc | mask | span]
-    uint32_t* sbase = reinterpret_cast<uint32_t*>(tsm + L.base);         // [2 tiles][KS words][128]
+    uint32_t* sraw = reinterpret_cast<uint32_t*>(tsm + L.raw_ring);      // [nraw][2 boxes][KS][ncols / 2]
+    uint32_t* sbase = reinterpret_cast<uint32_t*>(tsm + L.base);         // [2 tiles][2 halves][128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(tsm + L.bars);
     uint64_t* full = bars;                               // [S] producers -> MMA (one arrival per warp)
     uint64_t* empty = full + kTcStages;                  // [S] MMA commit -> producers
-    uint64_t* raw_full = empty + kTcStages;              // [RS] TMA bytes -> producers
-    uint64_t* raw_empty = raw_full + kTcRawStages;       // [RS] producers (one arrival per warp) -> loader
-    uint64_t* acc_full = raw_empty + kTcRawStages;       // MMA commit -> epilogue
+    uint64_t* raw_full = empty + kTcStages;              // [nraw] TMA bytes -> B producers
+    uint64_t* raw_empty = raw_full + kTcMaxRaw;          // [nraw] B producers (one arrival per warp) -> loader
+    uint64_t* acc_full = raw_empty + kTcMaxRaw;          // MMA commit -> epilogue
     uint64_t* acc_empty = acc_full + 1;                  // epilogue (4 warps) -> MMA
-    uint64_t* base_full = acc_full + 2;                  // [2] producers -> epilogue
-    uint64_t* base_empty = acc_full + 4;                 // [2] epilogue -> producers
+    uint64_t* base_full = acc_full + 2;                  // [2] A producers -> epilogue
+    uint64_t* base_empty = acc_full + 4;                 // [2] epilogue -> A producers
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 6);
+    const uint32_t nraw = L.nraw;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(full + s, kTcProdWarps);
+            mbar_init(full + s, kTcBWarps + kTcAWarps);
             mbar_init(empty + s, 1);
         }
-        for (int s = 0; s < kTcRawStages; ++s) {
+        for (uint32_t s = 0; s < nraw; ++s) {
             mbar_init(raw_full + s, 1);
-            mbar_init(raw_empty + s, kTcProdWarps);
+            mbar_init(raw_empty + s, kTcBWarps);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, kTcEpiWarps);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(base_full + i, kTcProdWarps);
+            mbar_init(base_full + i, kTcAWarps);
             mbar_init(base_empty + i, kTcEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -187,69 +224,120 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int nst = (NW + kTcKS - 1) / kTcKS;  // stages per tile
     const int half = ncols / 2;                // span pixels per TMA box
 
-    if (warp < kTcProdWarps) {
-        // ---------------- producers ----------------
-        // A: warp w writes TMEM lanes 32 (w & 3) .. +31 (its lane quarter), the 8
-        // columns of word w >> 2 of each stage.  B: thread tid expands span row
-        // tid (when < ncols), all kTcKS words of the stage.
-        const int q = warp & 3, jw = warp >> 2;
-        const int arow = q * 32 + lane;
-        const uint32_t a_taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(kTcAcol + 8 * jw);
-        const bool has_b = tid < ncols;  // warp-uniform (ncols is a multiple of 32)
-        const uint32_t boff = uint32_t((tid >> 3) * 256 + (tid & 7) * 16);
-        const uint32_t raw_words = L.raw / 4;
-        const uint32_t* rd = sraw + jw * kTcRows + arow;                  // desc word of this A row
-        const uint32_t* rm = sraw + L.raw_a / 4 + jw * kTcRows + arow;    // mask word
-        // span row tid: box 0 holds rows [0, half), box 1 rows [half, ncols), each [KS][half]
-        const uint32_t* rb = sraw + (L.raw_a / 4) * (MASKED ? 2 : 1) + (tid < half ? tid : half * kTcKS + tid - half);
-        uint32_t g = 0;  // global stage counter
-        int t = 0;
-        for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
-            uint32_t base = 0;
-            for (int st = 0; st < nst; ++st, ++g) {
-                const uint32_t r = g % kTcRawStages, s = g % kTcStages;
-                mbar_wait(raw_full + r, (g / kTcRawStages) & 1u);
-                const uint32_t a = rd[r * raw_words];
-                const uint32_t m = MASKED ? rm[r * raw_words] : 0xFFFFFFFFu;
-                uint32_t b[kTcKS];
-                if (has_b) {
+    if (warp < kTcBWarps) {
+        // ---------------- B producers ----------------
+        // The ncols x KS (row, word) tasks of a stage are dealt round-robin over the
+        // 512 threads (a warp's 32 tasks: one word, 32 consecutive rows); each
+        // expands one packed word into the row's 32 int8 (-1 / 0) of that K-step.
+        const int ntask = ncols * kTcKS;
+        uint32_t tsrc[kTcBTasks], tdst[kTcBTasks];  // raw word offset, expanded-slot byte offset
 #pragma unroll
-                    for (int j = 0; j < kTcKS; ++j) b[j] = rb[r * raw_words + j * half];
-                }
+        for (int k = 0; k < kTcBTasks; ++k) {
+            const int i = min(tid + k * kTcBWarps * 32, ntask - 1);
+            const int j = i / ncols, n = i - j * ncols;
+            const int box = n < half ? 0 : 1;
+            // span box `box` holds rows [box half, +half) as [KS][half]
+            tsrc[k] = uint32_t(box * half * kTcKS + j * half + n - box * half);
+            tdst[k] = uint32_t(j) * L.sub + uint32_t((n >> 3) * 256 + (n & 7) * 16);
+        }
+        uint32_t g = 0;  // global stage counter
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            for (int st = 0; st < nst; ++st, ++g) {
+                const uint32_t r = g % nraw, s = g % kTcStages;
+                tc_wait(raw_full + r, (g / nraw) & 1u);
+                const uint32_t* raw = sraw + r * (L.raw / 4);
+                uint32_t b[kTcBTasks];
+#pragma unroll
+                for (int k = 0; k < kTcBTasks; ++k)
+                    if (tid + k * kTcBWarps * 32 < ntask) b[k] = raw[tsrc[k]];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(raw_empty + r);
-                // A: byte = m ? (a ? -1 : +1) : 0; column c of a word = bit c of each byte
-                const uint32_t u = a & m;
-                base += __popc(u);
-                uint32_t av[8];
+                tc_wait(empty + s, ((g / kTcStages) & 1u) ^ 1u);
+                uint8_t* slot = sB + s * L.stage;
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    av[c] = tc_sign_bytes(u << (7 - c)) | (tc_sign_bytes(m << (7 - c)) & 0x01010101u);
-                mbar_wait(empty + s, ((g / kTcStages) & 1u) ^ 1u);
-                tc_fence_after();
-                __syncwarp();
-                tc_st8(a_taddr + s * (kTcKS * 8), av);
-                if (has_b) {
-                    uint8_t* slot = sB + s * L.stage + boff;
-#pragma unroll
-                    for (int j = 0; j < kTcKS; ++j) {
+                for (int k = 0; k < kTcBTasks; ++k) {
+                    if (!(BSM_TC_ABL & 8) && tid + k * kTcBWarps * 32 < ntask) {
                         uint32_t bv[8];
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) bv[c] = tc_sign_bytes(b[j] << (7 - c));
-                        *reinterpret_cast<uint4*>(slot + j * L.sub) = make_uint4(bv[0], bv[1], bv[2], bv[3]);
-                        *reinterpret_cast<uint4*>(slot + j * L.sub + 128) = make_uint4(bv[4], bv[5], bv[6], bv[7]);
+                        for (int c = 0; c < 8; ++c) bv[c] = tc_sign_bytes(b[k] << (7 - c));
+                        *reinterpret_cast<uint4*>(slot + tdst[k]) = make_uint4(bv[0], bv[1], bv[2], bv[3]);
+                        *reinterpret_cast<uint4*>(slot + tdst[k] + 128) = make_uint4(bv[4], bv[5], bv[6], bv[7]);
                     }
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B rows -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full + s);
+            }
+        }
+    } else if (warp >= kTcAWarp0) {
+        // ---------------- A producers ----------------
+        // warp: TMEM lane quarter q = warp & 3 (its rows 32 q .. +31), words
+        // [h KS/2, +KS/2) of each stage; packed words by plain loads, prefetched
+        // one stage ahead (these warps write only TMEM: no proxy fence drains them).
+        const int q = warp & 3, h = (warp - kTcAWarp0) >> 2;
+        const int arow = q * 32 + lane;
+        constexpr int WH = kTcKS / kTcAHalves;  // words per warp per stage
+        const uint32_t a_taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(kTcAcol + 8 * WH * h);
+        int t = 0;
+        uint32_t g = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
+            const TcItem w = tc_item(it, ndd, ndir, dir0, Dc, D);
+            const size_t pix = size_t(min(w.p0 + arow, npix - 1));
+            const uint32_t* pa = (w.dir ? r_ref : l_ref) + pix;
+            const uint32_t* pm = (w.dir ? r_mask : l_mask) + pix;
+            uint32_t na[WH], nm[WH];
+            auto load = [&](int st) {
+#pragma unroll
+                for (int j = 0; j < WH; ++j) {
+                    const int k = st * kTcKS + h * WH + j;
+                    const size_t o = size_t(min(k, NW - 1)) * size_t(P);
+                    const uint32_t km = k < NW ? 0xFFFFFFFFu : 0u;
+                    na[j] = __ldg(pa + o) & km;
+                    nm[j] = MASKED ? (__ldg(pm + o) & km) : km;
+                }
+            };
+            load(0);
+            uint32_t base = 0;
+            for (int st = 0; st < nst; ++st, ++g) {
+                uint32_t a[WH], m[WH];
+#pragma unroll
+                for (int j = 0; j < WH; ++j) {
+                    a[j] = na[j];
+                    m[j] = nm[j];
+                }
+                if (st + 1 < nst) load(st + 1);
+                const uint32_t s = g % kTcStages;
+                tc_wait(empty + s, ((g / kTcStages) & 1u) ^ 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int j0 = 0; j0 < WH; j0 += 2) {
+                    // A: byte = m ? (a ? -1 : +1) : 0; column c of a word = bit c of each byte
+                    uint32_t av[16];
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const uint32_t u = a[j0 + jj] & m[j0 + jj];
+                        base += __popc(u);
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            uint32_t v;
+                            asm("lop3.b32 %0, %1, %2, 0x01010101, 0xF8;"  // a | (b & c)
+                                : "=r"(v)
+                                : "r"(tc_sign_bytes(u << (7 - c))), "r"(m[j0 + jj] >> c));
+                            av[8 * jj + c] = v;
+                        }
+                    }
+                    __syncwarp();
+                    tc_st16(a_taddr + s * (kTcKS * 8) + j0 * 8, av);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(full + s);
             }
             // popc(a & m) of this tile's pixels (this warp's words), for the epilogue
             const int par = t & 1;
-            mbar_wait(base_empty + par, (uint32_t(t >> 1) & 1u) ^ 1u);
-            sbase[(par * kTcKS + jw) * kTcRows + arow] = base;
+            tc_wait(base_empty + par, (uint32_t(t >> 1) & 1u) ^ 1u);
+            sbase[(par * kTcAHalves + h) * kTcRows + arow] = base;
             __syncwarp();
             if (lane == 0) mbar_arrive(base_full + par);
         }
@@ -276,16 +364,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (!pix_ok || uhi < ulo) uhi = ulo;
             const uint32_t span = uint32_t(uhi - ulo);
             const int par = t & 1;
-            mbar_wait(base_full + par, uint32_t(t >> 1) & 1u);
+            tc_wait(base_full + par, uint32_t(t >> 1) & 1u);
             uint32_t base = 0;
 #pragma unroll
-            for (int j = 0; j < kTcKS; ++j) base += sbase[(par * kTcKS + j) * kTcRows + r];
+            for (int j = 0; j < kTcAHalves; ++j) base += sbase[(par * kTcAHalves + j) * kTcRows + r];
             __syncwarp();
             if (lane == 0) mbar_arrive(base_empty + par);
-            mbar_wait(acc_full, uint32_t(t) & 1u);
+            tc_wait(acc_full, uint32_t(t) & 1u);
             tc_fence_after();
             uint32_t best = 0xFFFFFFFFu;
-            const int cend = q * 32 + 32 + w.dq;  // last column any lane of this warp uses, + 1
+            const int cend = (BSM_TC_ABL & 32) ? 0 : q * 32 + 32 + w.dq;  // last column this warp uses, + 1
             for (int c0 = q * 32; c0 < cend; c0 += 32) {
                 uint32_t v[32];
                 __syncwarp();
@@ -324,15 +412,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint32_t g = 0;
         int t = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
-            mbar_wait(acc_empty, (uint32_t(t) & 1u) ^ 1u);
+            tc_wait(acc_empty, (uint32_t(t) & 1u) ^ 1u);
             tc_fence_after();
             for (int st = 0; st < nst; ++st, ++g) {
                 const uint32_t s = g % kTcStages;
-                mbar_wait(full + s, (g / kTcStages) & 1u);
+                tc_wait(full + s, (g / kTcStages) & 1u);
                 tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
-                    for (int j = 0; j < kTcKS; ++j) {
+                    for (int j = 0; j < kTcKS && !(BSM_TC_ABL & 4); ++j) {
                         const uint32_t a_t = tmem + uint32_t(kTcAcol) + s * (kTcKS * 8) + j * 8;
                         const uint32_t b_addr = sB_addr + s * L.stage + j * L.sub;
                         const uint32_t acc = (st > 0 || j > 0) ? 1u : 0u;
@@ -348,33 +436,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
         }
     } else {
-        // ---------------- TMA loader (lane 0 issues; the warp waits with it) ----------------
+        // ---------------- TMA loader of the span words (lane 0 issues) ----------------
         uint32_t g = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const TcItem w = tc_item(it, ndd, ndir, dir0, Dc, D);
             const int q0 = w.dir ? w.p0 + w.d0 : w.p0 - w.d0 - w.dq;  // span row 0 (a multiple of 4)
+            // A span box wholly outside the field is not loaded (a box starting
+            // further left than its width traps): its rows only meet out-of-image
+            // cells, so stale words are harmless.
+            const bool b0 = q0 + half > 0 && q0 < npix, b1 = q0 + 2 * half > 0 && q0 + half < npix;
+            const uint32_t hb = uint32_t(half) * kTcKS * 4;
             for (int st = 0; st < nst; ++st, ++g) {
-                const uint32_t r = g % kTcRawStages;
-                mbar_wait(raw_empty + r, ((g / kTcRawStages) & 1u) ^ 1u);
+                const uint32_t r = g % nraw;
+                tc_wait(raw_empty + r, ((g / nraw) & 1u) ^ 1u);
                 if (lane == 0) {
-                    uint32_t* dst = sraw + r * (L.raw / 4);
-                    uint32_t* db = dst + (L.raw_a / 4) * (MASKED ? 2 : 1);
+                    uint32_t* db = sraw + r * (L.raw / 4);
                     // the tensor maps are addressed directly (a runtime-selected pointer
                     // to a __grid_constant__ parameter would be a local copy)
-                    auto issue = [&](const CUtensorMap* mr, const CUtensorMap* mm, const CUtensorMap* mo) {
-// A span box wholly outside the field is not loaded (a box
-                        // starting further left than its width traps): its rows
-                        // only meet out-of-image cells, so stale words are harmless.
-                        const bool b0 = q0 + half > 0 && q0 < npix, b1 = q0 + 2 * half > 0 && q0 + half < npix;
-                        const uint32_t hb = uint32_t(half) * kTcKS * 4;
-                        mbar_expect_tx(raw_full + r, L.raw_a * (MASKED ? 2 : 1) + (b0 ? hb : 0) + (b1 ? hb : 0));
-                        tma_load_2d(dst, mr, w.p0, st * kTcKS, raw_full + r);
-                        if (MASKED) tma_load_2d(dst + L.raw_a / 4, mm, w.p0, st * kTcKS, raw_full + r);
+                    auto issue = [&](const CUtensorMap* mo) {
+                        if (BSM_TC_ABL & 16) { mbar_arrive(raw_full + r); return; }
+                        mbar_expect_tx(raw_full + r, (b0 ? hb : 0) + (b1 ? hb : 0));
                         if (b0) tma_load_2d(db, mo, q0, st * kTcKS, raw_full + r);
                         if (b1) tma_load_2d(db + half * kTcKS, mo, q0 + half, st * kTcKS, raw_full + r);
                     };
-                    if (w.dir) issue(&r_ref, &r_mask, &r_oth);
-                    else issue(&l_ref, &l_mask, &l_oth);
+                    if (w.dir) issue(&r_oth);
+                    else issue(&l_oth);
                 }
                 __syncwarp();
             }
