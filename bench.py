@@ -20,10 +20,12 @@ run one pair per rank (replicas).
           batch, bsm_pipeline_u8 / _rgb for one pair) with pinned HOST
           buffers: the H2D of every view and the D2H of every refined map
           (float + valid) are inside the timed region
-  roofline  the fused cost + WTA kernel (K3) against the nominal issue bound
-          of its integer pipes (ALU 64 LOP3 + XU 16 POPC per clk per SM: the
-          carry-save mix needs 2 LOP3 + 0.5 POPC per word-op, so 32 word-ops
-          per clk per SM); the live microbenchmark of that mix beside it;
+  roofline  the fused cost + WTA kernel (K3, tensor cores) against the live
+          dense FP4 MMA rate of this GPU (algorithmic flops: one MAC per
+          descriptor bit per in-bounds evaluation); beside it the MMA's busy
+          fraction (band waste included), the shared-memory bandwidth that
+          binds the kernel, and the same work as popcount word-ops against
+          the integer-pipe roofline of the popcount formulation;
           `roofline_mask` does the same for the mask kernel (K2) against its
           shared-memory gather floor
   cpu_baseline  the reference library compiled in place (oracle/_ref), all
@@ -56,7 +58,6 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
 WORDOPS_PER_CLK_SM = 32  # ALU: 64 LOP3/clk/SM at 2 LOP3 per word-op; XU: 16 POPC/clk/SM at 0.5 per word-op
-ISSUE_WORDOPS_PER_CLK_SM = 128 * 64 / 208  # 128 thread-instructions/clk/SM, 208 per 64 word-ops (K3's loop)
 WORKLOADS_CLI = ["c1", "c2", "c3", "c4", "c5", "c2rgb"]
 
 
@@ -139,6 +140,24 @@ class ClockSampler:
         reasons = sorted(set().union(*(s[2] for s in self.samples)))
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples), "source": self.source}
+
+
+def k3_tc_geometry(W: int, rows: int, D: int, nbits: int = 4096, masked: bool = True) -> dict:
+    """Work of one k_cost_wta_tc launch (both directions), mirroring its host
+    launch (bsm_kernels.cu wta_device_tc) and kern_cost_tc.cuh: 128-pixel tiles,
+    d-blocks of <= 256, ncols accumulator columns, stages of 8 u32 words."""
+    Wq = (W + 3) // 4 * 4
+    tiles = (rows * Wq + 127) // 128
+    ndd = (D + 255) // 256
+    Dc = D if ndd == 1 else ((D + ndd - 1) // ndd + 3) // 4 * 4
+    ncols = (128 + ((Dc + 2) & ~3) + 31) // 32 * 32
+    NW = 2 * ((nbits + 63) // 64)
+    nst = (NW + 7) // 8
+    items = tiles * ndd * 2
+    issued = 2.0 * items * 128 * ncols * nst * 8 * 32
+    operand = (128 + ncols) * 8 * 16 * 2  # A + B rows x 8 words x 16 B, written and read
+    raw = ((2 if masked else 1) * 8 * 128 * 4 + 8 * ncols * 4) * 2  # TMA-staged words, written and read
+    return {"ncols": ncols, "items": items, "issued_flops": issued, "smem_bytes": float(items) * nst * (operand + raw)}
 
 
 def in_bounds_evals(W, H, D):
@@ -509,41 +528,50 @@ def main():
             prof.setdefault(k, []).append(v)
     ctx.set_profiling(False)
     prof_ms = {k: float(np.mean(v)) for k, v in prof.items() if np.mean(v) > 0}
-    popc_peak, csa_peak = ctx.measure_word_peaks()  # live microbenchmarks, word-ops/s
+    mma_peak = ctx.measure_mma_peak()  # live dense FP4 tensor rate, flop/s
 
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
     clk = line["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
-    pipe_peak = WORDOPS_PER_CLK_SM * sms * clk * 1e6  # nominal word-ops/s
+    pipe_peak = WORDOPS_PER_CLK_SM * sms * clk * 1e6  # nominal word-ops/s of the popcount formulation
     rows_c = (min(H, y1 + cfg.vote_radius) - max(0, y0 - cfg.vote_radius)) if bands else H
     evals_dir = in_bounds_evals(W, rows_c, D)
     wta_ms = prof_ms.get("wta", 0.0) + prof_ms.get("wta_left", 0.0) + prof_ms.get("wta_right", 0.0)
-    achieved = 2 * evals_dir * (4096 // 32) / (wta_ms * 1e-3)  # both directions per launch set
+    sec = wta_ms * 1e-3
+    k3 = k3_tc_geometry(W, rows_c, D, nbits=4096)
+    alg_flops = 2.0 * 2 * evals_dir * 4096  # one MAC per descriptor bit per in-bounds (x, y, d, direction)
     hbm_peak = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     alg_bytes = 2 * W * rows_c * (3 * 4096 // 8 + 4)  # per direction: ref desc + ref mask + other desc, + key
-    hbm_ach = alg_bytes / (wta_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.workload)
+    smem_peak = 128 * sms * clk * 1e6  # B/s: 128 B/clk/SM
     line["roofline"] = {
-        "bound": "int-pipes (ALU LOP3 + XU POPC)", "kernel": "k_cost_wta (fused masked Hamming + WTA, both "
-                                                               "directions)",
-        "achieved": achieved / 1e9, "peak": pipe_peak / 1e9, "unit": "Gword-ops/s", "frac": achieved / pipe_peak,
-        "traffic": traffic,
-        "peak_source": f"nominal: {WORDOPS_PER_CLK_SM} word-ops/clk/SM (64 LOP3/clk/SM at 2 per word-op = 16 "
-                       f"POPC/clk/SM at 0.5 per word-op) x {sms} SMs x {clk:.0f} MHz",
-        "achievable_peak": csa_peak / 1e9, "frac_of_achievable": achieved / csa_peak,
-        # the carry-save loop issues 208 instructions per 64 word-ops per lane (128 LOP3 + 32 POPC
-        # + 32 IMAD + 10 LDS.128 + 6): against 4 schedulers x 32 lanes per clk per SM
-        "issue_peak": ISSUE_WORDOPS_PER_CLK_SM * sms * clk * 1e6 / 1e9,
-        "frac_of_issue": achieved / (ISSUE_WORDOPS_PER_CLK_SM * sms * clk * 1e6),
-        "achievable_source": "live register-only microbenchmark of the kernel's carry-save instruction mix",
-        "popc_only_peak": popc_peak / 1e9,
-        "kernel_ms": wta_ms, "alg_word_ops": 2 * evals_dir * 128,
-        "unit_def": "word-op = one u32 (a^b)&m + popcount; 128 per in-bounds (x, y, d, direction)",
-        "hbm_achieved_gbs": hbm_ach, "hbm_peak_gbs": hbm_peak, "hbm_frac": hbm_ach / hbm_peak,
+        "bound": "tensor (tcgen05 kind::mxf4, dense FP4)",
+        "kernel": "k_cost_wta_tc (masked Hamming as a banded FP4 MMA + fused WTA, both directions)",
+        "achieved": alg_flops / sec / 1e12, "peak": mma_peak / 1e12, "unit": "TFLOP/s",
+        "frac": alg_flops / sec / mma_peak, "traffic": traffic,
+        "peak_source": "live: kind::mxf4 M128 N256 K64 MMAs issued back to back, one CTA per SM "
+                       "(bsm_measure_mma_peak); nominal dense FP4 9000 TFLOP/s",
+        "unit_def": "algorithmic flop = 2 per descriptor bit per in-bounds (x, y, d, direction): "
+                    "popc((a^b)&m) = popc(a&m) + sum m(1-2a)b",
+        "kernel_ms": wta_ms, "alg_flops": alg_flops,
+        "issued_flops": k3["issued_flops"], "mma_busy_frac": k3["issued_flops"] / sec / mma_peak,
+        "band_efficiency": alg_flops / k3["issued_flops"],
+        # what binds it: every operand byte is written by the producers and read by the
+        # tensor core through shared memory, and the packed words are staged there by TMA
+        "smem": {"bytes": k3["smem_bytes"], "achieved_gbs": k3["smem_bytes"] / sec / 1e9,
+                 "peak_gbs": smem_peak / 1e9, "frac": k3["smem_bytes"] / sec / smem_peak,
+                 "peak_source": f"128 B/clk/SM x {sms} SMs x {clk:.0f} MHz"},
+        "int_pipe_equiv": {"achieved_gwordops": 2 * evals_dir * 128 / sec / 1e9,
+                           "int_pipe_peak_gwordops": pipe_peak / 1e9,
+                           "x_int_pipe_roofline": 2 * evals_dir * 128 / sec / pipe_peak,
+                           "note": "the same work as u32 (a^b)&m + popcount word-ops against the nominal "
+                                   "ALU+XU bound of the popcount formulation (32 word-ops/clk/SM)"},
+        "hbm_achieved_gbs": alg_bytes / sec / 1e9, "hbm_peak_gbs": hbm_peak,
+        "hbm_frac": alg_bytes / sec / 1e9 / hbm_peak,
     }
     mask_ms = prof_ms.get("mask", 0.0)
     if mask_ms > 0 and not colour:

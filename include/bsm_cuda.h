@@ -235,6 +235,9 @@ int bsm_last_launch_count(bsm_ctx* ctx, int* count);
  * 4 LOP3 + POPC + IMAD).  Either pointer may be NULL. */
 int bsm_measure_popc_peak(bsm_ctx* ctx, double* ops_per_s);
 int bsm_measure_word_peaks(bsm_ctx* ctx, double* popc_words_per_s, double* csa_words_per_s);
+/* Live dense FP4 tensor peak of this device (tcgen05 kind::mxf4, M128 N256
+ * K64, issued back to back), flop/s: the tensor-core cost kernel's roofline. */
+int bsm_measure_mma_peak(bsm_ctx* ctx, double* flops_per_s);
 /* The device restatement of libm's exp used for refine weights, evaluated on
  * n arguments (validation / tests). */
 int bsm_device_exp(bsm_ctx* ctx, const double* x, int n, double* out);

@@ -215,6 +215,12 @@ class Context:
         check(lib().bsm_measure_word_peaks(self.handle, C.byref(a), C.byref(b)))
         return float(a.value), float(b.value)
 
+    def measure_mma_peak(self) -> float:
+        """Dense FP4 tensor rate (kind::mxf4 MMAs back to back) of this GPU, flop/s."""
+        v = C.c_double()
+        check(lib().bsm_measure_mma_peak(self.handle, C.byref(v)))
+        return float(v.value)
+
 
 _tls = threading.local()
 

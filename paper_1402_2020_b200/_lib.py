@@ -122,6 +122,7 @@ _SIGS = {
     "bsm_last_launch_count": [_P, C.POINTER(C.c_int)],
     "bsm_measure_popc_peak": [_P, C.POINTER(C.c_double)],
     "bsm_measure_word_peaks": [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "bsm_measure_mma_peak": [_P, C.POINTER(C.c_double)],
 }
 _RET = {"bsm_last_error": C.c_char_p, "bsm_version": C.c_char_p, "bsm_timing_names": C.c_char_p}
 

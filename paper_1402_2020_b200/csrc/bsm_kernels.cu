@@ -441,21 +441,23 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
     const int ndir = both ? 2 : 1;
     if (tiles * ndd * ndir > 0x7FFFFFFFLL) return set_err(BSM_UNSUPPORTED, "bsm: image too large for the cost kernel");
     const int items = int(tiles * ndd * ndir);
-    CUtensorMap lo, ro;  // span words of the other view; an unused slot is a copy of a valid map
-    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, ncols / 2, kTcKS));
-    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
+    CUtensorMap lr, lm, lo, rr, rm, ro;  // unused slots are copies of a valid map
     const uint32_t* ml_ = ml ? ml : dl;
     const uint32_t* mr_ = mr ? mr : dr;
-    const TcSmem L(ncols);
+    BSM_TRY(field_tensor_map(&lr, use_l ? dl : dr, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&lm, use_l ? ml_ : mr_, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&lo, use_l ? dr : dl, W, c->NW, rows, ncols / 2, kTcKS));
+    BSM_TRY(field_tensor_map(&rr, use_r ? dr : dl, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&rm, use_r ? mr_ : ml_, W, c->NW, rows, kTcRows, kTcKS));
+    BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
+    const TcSmem L(ncols, masked);
     if (L.nraw < 2) return set_err(BSM_UNSUPPORTED, "bsm: cost kernel shared-memory layout");
     const size_t sm = L.total;  // > 114 KB: one CTA per SM (it allocates all 512 TMEM columns)
     const int grid = std::min(items, c->sm_count);
     auto launch = [&](auto kern) -> int {
         BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<grid, kTcThreads, sm, c->stream>>>(lo, ro, use_l ? dl : dr, use_l ? ml_ : mr_, use_r ? dr : dl,
-                                                  use_r ? mr_ : ml_, W, Wq, int(npix), int(field_plane(W, rows)),
-                                                  c->NW, d_max, Dc, ncols, ndd, ndir, both ? 0 : dir, items, keys_l,
-                                                  keys_r);
+        kern<<<grid, kTcThreads, sm, c->stream>>>(lr, lm, lo, rr, rm, ro, W, Wq, int(npix), c->NW, d_max, Dc, ncols,
+                                                  ndd, ndir, both ? 0 : dir, items, keys_l, keys_r);
         return BSM_OK;
     };
     BSM_TRY(masked ? launch(k_cost_wta_tc<true>) : launch(k_cost_wta_tc<false>));
@@ -1594,6 +1596,33 @@ int bsm_last_launch_count(bsm_ctx* c, int* count) {
 
 int bsm_measure_popc_peak(bsm_ctx* c, double* ops_per_s) {
     return bsm_measure_word_peaks(c, ops_per_s, nullptr);
+}
+
+int bsm_measure_mma_peak(bsm_ctx* c, double* flops_per_s) {
+    if (!c || !flops_per_s) return set_err(BSM_INVALID_ARGUMENT, "bsm: null argument");
+    BSM_CUDA(cudaSetDevice(c->device));
+    const int iters = 65536;
+    BSM_TRY(c->popc_out.ensure(size_t(c->sm_count) * 4));
+    BSM_CUDA(cudaFuncSetAttribute(k_mxf4_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+    cudaEvent_t e0, e1;
+    BSM_CUDA(cudaEventCreate(&e0));
+    BSM_CUDA(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, c->stream);
+        // 120 KB of dynamic shared memory: one CTA (and one TMEM allocation) per SM
+        k_mxf4_peak<<<c->sm_count, 128, 120 * 1024, c->stream>>>(iters, c->popc_out.as<uint32_t>());
+        cudaEventRecord(e1, c->stream);
+        BSM_CUDA(cudaEventSynchronize(e1));
+        BSM_CUDA(cudaGetLastError());
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *flops_per_s = 2.0 * 128 * 256 * 64 * double(iters) * c->sm_count / (double(best) * 1e-3);
+    return BSM_OK;
 }
 
 int bsm_measure_word_peaks(bsm_ctx* c, double* popc_words_per_s, double* csa_words_per_s) {

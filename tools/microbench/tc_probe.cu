@@ -97,7 +97,7 @@ int main(int argc, char** argv) {
     const int items = tiles * ndd * ndir;
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    const size_t sm = TcSmem(ncols).total;
+    const size_t sm = TcSmem(ncols, masked).total;
     auto kern = masked ? k_cost_wta_tc<true> : k_cost_wta_tc<false>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     const int grid = std::min(items, nsm);
@@ -114,13 +114,14 @@ int main(int argc, char** argv) {
         if (r != CUDA_SUCCESS) { std::printf("tensor map failed %d\n", int(r)); std::exit(1); }
         return m;
     };
-    const CUtensorMap m_dr_o = tmap(gdr, ncols / 2), m_dl_o = tmap(gdl, ncols / 2);
+    const CUtensorMap m_dl = tmap(gdl, kTcRows), m_ml = tmap(gml, kTcRows), m_dr_o = tmap(gdr, ncols / 2);
+    const CUtensorMap m_dr = tmap(gdr, kTcRows), m_mr = tmap(gmr, kTcRows), m_dl_o = tmap(gdl, ncols / 2);
     auto run = [&]() {
         if (ndd > 1) {
             CK(cudaMemset(kl, 0xFF, size_t(W) * H * 4));
             CK(cudaMemset(kr, 0xFF, size_t(W) * H * 4));
         }
-        kern<<<grid, kTcThreads, sm>>>(m_dr_o, m_dl_o, gdl, gml, gdr, gmr, W, Wq, npix, int(P), NW, D, Dc, ncols, ndd, ndir, dir0,
+        kern<<<grid, kTcThreads, sm>>>(m_dl, m_ml, m_dr_o, m_dr, m_mr, m_dl_o, W, Wq, npix, NW, D, Dc, ncols, ndd, ndir, dir0,
                                        items, kl, kr);
     };
     run();
@@ -175,7 +176,7 @@ int main(int argc, char** argv) {
     evals *= H;
     std::printf("W %d H %d NW %d D %d masked %d: ncols %d ndd %d items %d grid %d smem %zu nraw %u: %.3f ms both directions, "
                 "%.1f G word-ops/s, %.0f Mdisp-evals/s (cost only, x2 dirs)\n",
-                W, H, NW, D, int(masked), ncols, ndd, items, grid, sm, TcSmem(ncols).nraw, best, evals * NW / best / 1e6,
+                W, H, NW, D, int(masked), ncols, ndd, items, grid, sm, TcSmem(ncols, masked).nraw, best, evals * NW / best / 1e6,
                 evals / 2 / best / 1e3);
     return bad ? 2 : 0;
 }
