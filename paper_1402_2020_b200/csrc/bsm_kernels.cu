@@ -450,7 +450,11 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
     BSM_TRY(field_tensor_map(&rr, use_r ? dr : dl, W, c->NW, rows, kTcRows, kTcKS));
     BSM_TRY(field_tensor_map(&rm, use_r ? mr_ : ml_, W, c->NW, rows, kTcRows, kTcKS));
     BSM_TRY(field_tensor_map(&ro, use_r ? dl : dr, W, c->NW, rows, ncols / 2, kTcKS));
-    const TcSmem L(ncols, masked);
+    // A operand in TMEM for accumulators up to 320 columns (measured on B200,
+    // tools/microbench/tc_probe: c4 -1.1%, c1/c3 -4%; at 384 columns (c2, c5)
+    // +0.6%); BSM_K3_VARIANT bit 5 forces A into shared memory
+    const bool at = ncols <= 320 && !(c->k3_variant & 32);
+    const TcSmem L(ncols, masked, at);
     if (L.nraw < 2) return set_err(BSM_UNSUPPORTED, "bsm: cost kernel shared-memory layout");
     const size_t sm = L.total;  // > 114 KB: one CTA per SM (it allocates all 512 TMEM columns)
     const int grid = std::min(items, c->sm_count);
@@ -460,7 +464,8 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
                                                   ndd, ndir, both ? 0 : dir, items, keys_l, keys_r);
         return BSM_OK;
     };
-    BSM_TRY(masked ? launch(k_cost_wta_tc<true>) : launch(k_cost_wta_tc<false>));
+    if (at) BSM_TRY(masked ? launch(k_cost_wta_tc<true, true>) : launch(k_cost_wta_tc<false, true>));
+    else BSM_TRY(masked ? launch(k_cost_wta_tc<true, false>) : launch(k_cost_wta_tc<false, false>));
     return check_launch(c, "cost_wta_tc");
 }
 

@@ -54,6 +54,7 @@ constexpr int kTcStages = 2;                      // expanded operand ring (smem
 constexpr int kTcMaxRaw = 8;                      // TMA ring of packed words (as many as fit)
 constexpr int kTcMaxDc = 256;                     // disparities per d-block
 constexpr int kTcMaxCols = 384;                   // accumulator columns (128 + 256 -> 384)
+constexpr int kTcAcol = 384;                      // A operand ring in TMEM (AT kernels): kTcStages x 32 columns
 constexpr int kTcSfCol = 448;                     // scale factors: SFA cols 448-479, SFB 480-511 (all 1.0)
 constexpr uint32_t kTcSmemLimit = 227 * 1024;     // dynamic shared memory per CTA
 constexpr int kTcProdWarps = 16;                  // producers: warps 0-15
@@ -64,7 +65,8 @@ constexpr int kTcATasks = kTcRows * kTcKS;        // (row, word) A tasks per sta
 constexpr int kTcTasks = (kTcATasks + kTcMaxCols * kTcKS + kTcProdWarps * 32 - 1) / (kTcProdWarps * 32);
 static_assert(kTcATasks % (kTcProdWarps * 32) == 0, "A tasks fill whole task slots");
 constexpr int kTcASlots = kTcATasks / (kTcProdWarps * 32);  // task slots that are A tasks (2)
-static_assert(kTcMaxCols <= kTcSfCol, "TMEM: accumulator + scale factors");
+static_assert(kTcMaxCols <= kTcAcol && kTcAcol + kTcStages * kTcKS * 4 <= kTcSfCol,
+              "TMEM: accumulator, A ring and scale factors");
 
 __device__ __forceinline__ void tc_wait(uint32_t bar_saddr, uint32_t parity) {
     asm volatile(
@@ -108,6 +110,21 @@ __device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint64_t a_desc, ui
         "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
         : "memory");
+}
+// The same MMA with A read from tensor memory (row r = TMEM lane r, 8 packed
+// E2M1 per 32-bit column: the bytes of the shared-memory K-major row in order).
+__device__ __forceinline__ void tc_mma_mxf4_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+__device__ __forceinline__ void tc_st4(uint32_t taddr, const uint4& v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
@@ -162,10 +179,10 @@ __device__ __forceinline__ TcItem tc_item(int it, int ndd, int ndir, int dir0, i
 // at most kTcMaxRaw), the per-tile popcount bases and the barriers.
 struct TcSmem {
     uint32_t a_sub, b_sub, a_stage, stage, raw_a, raw, nraw, ring, raw_ring, base, bars, total;
-    __host__ __device__ TcSmem(int ncols, bool masked) {
+    __host__ __device__ TcSmem(int ncols, bool masked, bool atmem) {
         a_sub = kTcRows * 32u;                       // one K-step (64 FP4) of A rows
         b_sub = uint32_t(ncols) * 32u;               // one K-step of B rows
-        a_stage = a_sub * (kTcKS / 2);
+        a_stage = atmem ? 0u : a_sub * (kTcKS / 2);  // A in TMEM: the ring holds B only
         stage = a_stage + b_sub * (kTcKS / 2);       // [A K-steps][B K-steps]
         raw_a = kTcKS * kTcRows * 4u;                // one [KS x 128] word box
         raw = raw_a * (masked ? 2u : 1u) + kTcKS * uint32_t(ncols) * 4u;
@@ -180,7 +197,7 @@ struct TcSmem {
     }
 };
 
-template <bool MASKED>
+template <bool MASKED, bool AT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_cost_wta_tc(const __grid_constant__ CUtensorMap l_ref, const __grid_constant__ CUtensorMap l_mask,
                   const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_ref,
@@ -188,7 +205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   int Wq, int npix, int NW, int D, int Dc, int ncols, int ndd, int ndir, int dir0, int items,
                   uint32_t* __restrict__ keys_l, uint32_t* __restrict__ keys_r) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    const TcSmem L(ncols, MASKED);
+    const TcSmem L(ncols, MASKED, AT);
     uint8_t* sop = tsm + L.ring;                                         // [S][A: KS/2 x 128 x 32 B][B: KS/2 x ncols x 32 B]
     uint32_t* sraw = reinterpret_cast<uint32_t*>(tsm + L.raw_ring);      // [nraw][desc | mask | span box 0 | box 1]
     uint32_t* sbase = reinterpret_cast<uint32_t*>(tsm + L.base);         // [2 tiles][4 partials][128]
@@ -268,6 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
         const int aw0 = tid / kTcRows;  // word of A slot 0 (slot k: aw0 + 4 k)
+        const uint32_t a_taddr = tmem + (uint32_t((warp & 3) * 32) << 16) + kTcAcol;
         TcRing rr, sr;  // raw ring, operand ring
         int t = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
@@ -291,6 +309,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) mbar_arrive(raw_empty + r);
                 tc_wait(empty + s, sr.phase ^ 1u);
                 uint8_t* slot = sop + s * L.stage;
+                if constexpr (AT) tc_fence_after();  // the MMAs that read this A slot have completed
 #pragma unroll
                 for (int k = 0; k < kTcTasks; ++k) {
                     if (tid + k * kTcProdWarps * 32 < ntask && !(BSM_TC_ABL & 8)) {
@@ -300,11 +319,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             base += __popc(u);
                             o = make_uint4(tc_fp4_a<0>(u, mm[k]), tc_fp4_a<1>(u, mm[k]), tc_fp4_a<2>(u, mm[k]),
                                            tc_fp4_a<3>(u, mm[k]));
+                            // A row (tid % 128) = TMEM lane: this warp's lane quarter is warp % 4;
+                            // word w of slot s -> columns kTcAcol + 32 s + 4 w
+                            if constexpr (AT) {
+                                tc_st4(a_taddr + s * (kTcKS * 4) + 4 * (aw0 + 4 * k), o);
+                                continue;
+                            }
                         } else {
                             o = make_uint4(tc_fp4_b<0>(x[k]), tc_fp4_b<1>(x[k]), tc_fp4_b<2>(x[k]), tc_fp4_b<3>(x[k]));
                         }
                         *reinterpret_cast<uint4*>(slot + tdst[k]) = o;
                     }
+                }
+                if constexpr (AT) {
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands -> tensor-core reads
                 __syncwarp();
@@ -405,11 +434,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         const uint32_t a_addr = sop_addr + s * L.stage + j * L.a_sub;
                         const uint32_t b_addr = sop_addr + s * L.stage + L.a_stage + j * L.b_sub;
                         const uint32_t acc = (st > 0 || j > 0) ? 1u : 0u;
-                        const uint64_t ad = tc_smem_desc(a_addr);
-                        tc_mma_mxf4(tmem, ad, tc_smem_desc(b_addr), id1, sfa, sfb, acc);
-                        if (n2 > 0)
-                            tc_mma_mxf4(tmem + uint32_t(n1), ad, tc_smem_desc(b_addr + uint32_t(n1 / 8) * 256u), id2,
-                                        sfa, sfb, acc);
+                        if constexpr (AT) {
+                            const uint32_t at = tmem + kTcAcol + s * (kTcKS * 4) + j * 8;
+                            tc_mma_mxf4_ts(tmem, at, tc_smem_desc(b_addr), id1, sfa, sfb, acc);
+                            if (n2 > 0)
+                                tc_mma_mxf4_ts(tmem + uint32_t(n1), at, tc_smem_desc(b_addr + uint32_t(n1 / 8) * 256u),
+                                               id2, sfa, sfb, acc);
+                        } else {
+                            const uint64_t ad = tc_smem_desc(a_addr);
+                            tc_mma_mxf4(tmem, ad, tc_smem_desc(b_addr), id1, sfa, sfb, acc);
+                            if (n2 > 0)
+                                tc_mma_mxf4(tmem + uint32_t(n1), ad, tc_smem_desc(b_addr + uint32_t(n1 / 8) * 256u),
+                                            id2, sfa, sfb, acc);
+                        }
                     }
                     tc_commit(empty + s);
                 }
