@@ -131,6 +131,7 @@ struct bsm_ctx {
     // pattern
     int n = 0, window = 0, half = 0, NW = 0, u = 0;
     int mslots = 0;                 // rank-table slots used by the mask kernels
+    int nfill = 0;                  // entries of k_mask4's fill-order table (d_uoff)
     std::vector<int> slot_used;     // slot -> used-offset index (-1: empty)
     int mch = 4;                    // k_mask4 / k_mask_f32 chunks of 32 positions per lane (1, 2, 4)
     std::vector<int> order;         // bit position -> pair index (identity unless permuted)
@@ -262,8 +263,34 @@ int ensure_mask_offsets(bsm_ctx* c, int TW) {
         const int dy = c->used[size_t(ui)] / side - c->half, dx = c->used[size_t(ui)] % side - c->half;
         o[size_t(k)] = dy * TW + dx;
     }
-    BSM_TRY(c->d_uoff.ensure(std::max<size_t>(4, o.size() * 4)));
-    BSM_CUDA(cudaMemcpy(c->d_uoff.p, o.data(), o.size() * 4, cudaMemcpyHostToDevice));
+    // k_mask4's fill order: groups of 32 slots in which lane b writes a slot of
+    // shared-memory bank b (slot % 32 == b: conflict-free stores) and every slot is
+    // the g-th of its bank in raster order of its window offset, so one group's
+    // tile reads fall within a few window rows (the slot order itself, chosen for
+    // the pair gathers, scatters them: 2-3 wavefronts per read, ncu at c4).
+    // Entry = (slot << 16) | (offset + h TW + h).  Banks with fewer slots repeat
+    // their last one (the same value stored twice).
+    {
+        std::vector<std::vector<std::pair<int, int>>> bank(32);
+        for (int k = 0; k < c->mslots; ++k) bank[size_t(k % 32)].push_back({o[size_t(k)] + c->half * TW + c->half, k});
+        size_t groups = 0;
+        for (auto& b : bank) {
+            std::sort(b.begin(), b.end());
+            groups = std::max(groups, b.size());
+        }
+        std::vector<uint32_t> fill(groups * 32, 0);
+        for (size_t g = 0; g < groups; ++g)
+            for (int b = 0; b < 32; ++b) {
+                if (bank[size_t(b)].empty()) return set_err(BSM_UNSUPPORTED, "bsm: fewer rank-table slots than banks");
+                const auto& e = bank[size_t(b)][std::min(g, bank[size_t(b)].size() - 1)];
+                if (e.first < 0 || e.first > 0xFFFF || e.second > 0xFFFF)
+                    return set_err(BSM_UNSUPPORTED, "bsm: mask window too large for the fill table");
+                fill[g * 32 + size_t(b)] = uint32_t(e.second) << 16 | uint32_t(e.first);
+            }
+        BSM_TRY(c->d_uoff.ensure(std::max<size_t>(4, fill.size() * 4)));
+        BSM_CUDA(cudaMemcpy(c->d_uoff.p, fill.data(), fill.size() * 4, cudaMemcpyHostToDevice));
+        c->nfill = int(fill.size());
+    }
     // the same slots as (dy << 16) | (dx & 0xFFFF) for the float-plane kernel
     std::vector<int32_t> xy(size_t(c->mslots), 0);
     for (int k = 0; k < c->mslots; ++k) {
@@ -323,7 +350,7 @@ int check_pattern(bsm_ctx* c) {
 
 size_t mask4_smem(const bsm_ctx* c) {
     const int TW = mask4_tw(c->half), TH = 2 * c->half + 1;
-    return size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * mask4_stage_stride(c->mch) * 4 + 512 +
+    return 2 * size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * mask4_stage_stride(c->mch) * 4 + 1024 +
            size_t(TW) * TH;
 }
 
@@ -357,8 +384,8 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
             const bool packed = c->mch <= 4 && !(c->mask_variant & 1);
             kern<<<grid3, 32, sm4, c->stream>>>(img, W, H, ybeg, rows,
                                                 c->d_pqb.as<uint4>() + (packed ? 2 * kPqTable / 4 : 0),
-                                                c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<int32_t>(),
-                                                c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
+                                                c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<uint32_t>(),
+                                                c->nfill, c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
                                                 c->half, mask4_tw(c->half), c->NW, Wq, P, mask);
             return BSM_OK;
         };

@@ -331,14 +331,14 @@ __host__ __device__ constexpr int mask4_stage_stride(int mch) { return 32 * mch 
 template <int MCH, bool PACKED = false>
 __global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
-            const uint4* __restrict__ q4, int n, const int32_t* __restrict__ uoff, int u, int rho_words,
+            const uint4* __restrict__ q4, int n, const uint32_t* __restrict__ ufill, int nfill, int u, int rho_words,
             const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask) {
     extern __shared__ __align__(16) uint32_t dsm[];
-    uint32_t* rho = dsm;                                  // rho_words (u + sentinel, padded)
+    uint32_t* rho2 = dsm;                                 // 2 x rho_words (u + sentinel, padded): two passes' tables
     constexpr int STG = mask4_stage_stride(MCH);
-    uint32_t* stage = rho + rho_words;                    // [kM3Px][STG]
-    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * STG);  // 2 x 256
-    uint8_t* tile = rrows + 512;                                            // (2h+1) x TW
+    uint32_t* stage = rho2 + 2 * rho_words;               // [kM3Px][STG]
+    uint8_t* rrows = reinterpret_cast<uint8_t*>(stage + kM3Px * STG);  // 4 x 256: rank rows of 4 centres
+    uint8_t* tile = rrows + 1024;                                           // (2h+1) x TW
     const int G = (n + 31) >> 5;
     const int TH = 2 * half + 1;
     const int lane = threadIdx.x;
@@ -367,25 +367,41 @@ __global__ void __launch_bounds__(32, 16)
             tile[idx] = __ldg(img + size_t(gy) * W + gx);
         }
     }
-    if (lane == 0) rho[u] = 0x00FF00FFu;  // sentinel: a = 255 for both pixels
+    if (lane < 2) rho2[lane * rho_words + u] = 0x00FF00FFu;  // sentinels: a = 255 for both pixels
     __syncwarp();
 
     const int k = max(1, n / 4);
     const int c0 = half * TW + sh + half;  // tile index of pixel x0
-    // rank rows of the next pass's two centre pixels, loaded one pass ahead
-    uint4 rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (lane >> 4)])) + (lane & 15));
+    // rank rows of the next two passes' four centre pixels, loaded two passes ahead
+    uint4 rr0 = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (lane >> 4)])) + (lane & 15));
+    uint4 rr1 = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + 2 + (lane >> 4)])) + (lane & 15));
 #pragma unroll 1
     for (int q = 0; q < kM3Px; q += 2) {
-        const int cia = c0 + q, cib = cia + 1;
-        reinterpret_cast<uint4*>(rrows)[lane] = rr;
-        if (q + 2 < kM3Px)
-            rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[cia + 2 + (lane >> 4)])) + (lane & 15));
-        __syncwarp();
-        for (int j = lane; j < u; j += 32) {
-            const int o = __ldg(uoff + j);
-            rho[j] = uint32_t(rrows[tile[cia + o]]) | (uint32_t(rrows[256 + tile[cib + o]]) << 16);
+        uint32_t* rho = rho2 + ((q >> 1) & 1) * rho_words;
+        if ((q & 2) == 0) {
+            // the tables of passes q and q + 2 (pixels q .. q + 3) in one sweep: entry
+            // j = (slot << 16) | (window offset + h TW + h); lane b of every group of
+            // 32 writes a slot of bank b, and a group's offsets lie within a few
+            // window rows (host fill order), so stores and tile reads stay
+            // conflict-free or nearly
+            reinterpret_cast<uint4*>(rrows)[lane] = rr0;
+            reinterpret_cast<uint4*>(rrows)[32 + lane] = rr1;
+            if (q + 4 < kM3Px) {
+                rr0 = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + q + 4 + (lane >> 4)])) + (lane & 15));
+                rr1 = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + q + 6 + (lane >> 4)])) + (lane & 15));
+            }
+            __syncwarp();
+            const uint8_t* tq = tile + sh + q;
+            for (int j = lane; j < nfill; j += 32) {
+                const uint32_t e = __ldg(ufill + j);
+                const uint8_t* tp = tq + (e & 0xFFFFu);
+                const uint32_t v0 = uint32_t(rrows[tp[0]]) | (uint32_t(rrows[256 + tp[1]]) << 16);
+                const uint32_t v1 = uint32_t(rrows[512 + tp[2]]) | (uint32_t(rrows[768 + tp[3]]) << 16);
+                rho2[e >> 16] = v0;
+                rho2[rho_words + (e >> 16)] = v1;
+            }
+            __syncwarp();
         }
-        __syncwarp();
 
         // a = max(rhoP, rhoQ) of 32 positions of chunk m for both pixels, as
         // byte registers wa (pixel A) and wb (pixel B)

@@ -88,5 +88,7 @@ def test_gpu_line_json_contract():
     assert d["gpu_launches"] >= 7 * 3  # descriptor, mask (x2 each), WTA, LR check, vmap, refine per step
     rf = d["roofline"]
     assert 0 < rf["frac"] <= 1.0 and rf["achieved"] > 0 and rf["peak"] > 0
+    assert "roofline_cost" in d and "roofline_mask" in d  # K3 and K2; `roofline` is the larger of the two
+    assert rf["kernel_ms"] == max(d["roofline_cost"]["kernel_ms"], d["roofline_mask"]["kernel_ms"])
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] > 0
     assert isinstance(d["clocks"]["reasons"], list)
