@@ -1,0 +1,35 @@
+#!/bin/bash
+# Round-2 evidence in one GPU call (tensor-core K3).  Usage (under gpurun): bash tools/gpu_final3.sh <tag>
+T=${1:-r02}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > gpurun_out/${T}_smi.txt
+lscpu > gpurun_out/${T}_lscpu.txt 2>&1; nproc >> gpurun_out/${T}_lscpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest_gpu.log
+BSM_GUARD=1 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest_gpu_guard.log 2>&1; echo "guard pytest rc=$?"; tail -2 gpurun_out/${T}_pytest_gpu_guard.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench_default.json 2> gpurun_out/${T}_bench_default.err; echo "bench default rc=$?"
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${T}_bench_reference.json 2> gpurun_out/${T}_bench_reference.err; echo "bench reference rc=$?"
+for wl in c1 c2 c3 c5 c2rgb; do
+  timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 > gpurun_out/${T}_bench_$wl.json 2> gpurun_out/${T}_bench_$wl.err; echo "bench $wl rc=$?"
+done
+timeout 900 python bench.py --impl reference --workload c2 --steps 10 --warmup 3 > gpurun_out/${T}_bench_reference_c2.json 2>&1; echo "bench reference c2 rc=$?"
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
+    bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_bench_torchrun.json 2> gpurun_out/${T}_bench_torchrun.err; echo "torchrun rc=$?"
+timeout 120 tools/microbench/mma_issue > gpurun_out/${T}_mma_issue.txt 2>&1
+timeout 900 python tools/k3_ab.py c1 c2 c3 c4 c5 -- 0 32 16 > gpurun_out/${T}_k3_ab.txt 2>&1; echo "k3 ab rc=$?"
+timeout 600 python bench.py --steps 1 --warmup 1 --profile-only --pairs 4 > gpurun_out/${T}_plain_bench.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_c4.csv \
+    python bench.py --steps 1 --warmup 1 --profile-only --pairs 4 > gpurun_out/${T}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout 300 python tools/profile_pipeline.py c4 1 > gpurun_out/${T}_plain.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_cost_wta|k_mask4|k_descriptor4|k_vote_refine_fold|k_lr_check_keys" -c 5 \
+    -o gpurun_out/${T}_c4_full python tools/profile_pipeline.py c4 1 > gpurun_out/${T}_ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tools/summarize_ncu.py gpurun_out/${T}_c4_full.ncu-rep > gpurun_out/${T}_ncu_kernels_c4.txt 2>&1
+for wl in c1 c2 c3 c4 c5; do
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_cost_wta|k_mask4" -c 3 --csv \
+      --log-file gpurun_out/${T}_traffic_$wl.csv python tools/profile_pipeline.py $wl 1 > /dev/null 2>&1; echo "traffic $wl rc=$?"
+done
+timeout 300 python tools/profile_colour.py > gpurun_out/${T}_colour_plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_mask_f32|k_descriptor_f32|k_rgb_planes" -c 4 \
+      -o gpurun_out/${T}_colour python tools/profile_colour.py > gpurun_out/${T}_colour_ncu.log 2>&1; echo "ncu colour rc=$?"
+python tools/summarize_ncu.py gpurun_out/${T}_colour.ncu-rep > gpurun_out/${T}_ncu_kernels_c2rgb.txt 2>&1
+echo done

@@ -1,4 +1,6 @@
-"""A/B of the cost kernel's variants (BSM_K3_VARIANT bits: 1 = thread-0
+"""A/B of the cost kernel variants (BSM_K3_VARIANT bits: 16 = the integer-pipe
+kernel K3p instead of the tensor-core K3, 32 = K3 with A in shared memory; for
+K3p: 1 = thread-0
 refill with empty barriers instead of last-warp refill, 2 = one launch per
 direction) on device-resident workloads; every variant's refined map must
 equal the first one's.
