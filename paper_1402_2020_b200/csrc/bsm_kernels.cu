@@ -389,6 +389,22 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
                                                 c->half, mask4_tw(c->half), c->NW, Wq, P, mask);
             return BSM_OK;
         };
+        // MCH = 2, 4 (1024 < n <= 4096): four pixels per pass over u8 ranks,
+        // two warps per CTA (k_mask_q); BSM_MASK_VARIANT bit 1 keeps k_mask4
+        if ((c->mch == 2 || c->mch == 4) && !(c->mask_variant & 3)) {
+            const size_t smq = size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * mask4_stage_stride(c->mch) * 4 +
+                               64 + 1024 + size_t(mask4_tw(c->half)) * (2 * c->half + 1);
+            auto launch_q = [&](auto kern) -> int {
+                BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smq)));
+                kern<<<grid3, 64, smq, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * kPqTable / 4,
+                                                    c->n, c->d_uoff.as<uint32_t>(), c->nfill, c->mslots,
+                                                    round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(), c->half,
+                                                    mask4_tw(c->half), c->NW, Wq, P, mask);
+                return BSM_OK;
+            };
+            BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1>) : launch_q(k_mask_q<2>));
+            return check_launch(c, "mask");
+        }
         // chunks of 32 positions per lane: the work scales with n
         // MCH <= 4: the packed P | Q << 16 index table (half the index loads;
         // the split runs on the FMA pipe): -3% mask time at c2 / c4

@@ -489,6 +489,230 @@ __global__ void __launch_bounds__(32, 16)
 }
 
 // ---------------------------------------------------------------------------
+// K2q -- the mask for four pixels per pass: the rank table holds one byte per
+// pixel (the ranks are dense ranks of <= 256 distinct distances, so they fit
+// u8), so one u32 gather serves four pixels -- half the rank-gather and
+// index-load wavefronts per pixel of k_mask4.  The per-byte max runs as two
+// VIMNMX.U16x2 on the even / odd byte lanes (masked operands); the four
+// pixels' planes (8 x MCH x 4 words) are split over two warps: warp w owns
+// chunks [w MCH/2, (w + 1) MCH/2) of every lane, i.e. the same 32-lane gather
+// groups of the bank-balanced index tables as k_mask4 (so every gather is still
+// one wavefront), and the MSB-first select adds the two warps' counts through
+// shared memory with one CTA barrier per bit (the four pixels in lockstep).
+// Output words: lane l, chunk m of the MCH -> word MCH l + m, as in k_mask4.
+// Four pixels' select, MW chunks per lane in this warp; counts of the other warp
+// arrive through xchg (double-buffered by bit parity: the barrier of round j - 1
+// separates round j's reads from round j - 2's writes).
+// bytes_to_planes_x with the right shifts as multiply-high (FMA pipe): for the
+// ALU-bound k_mask_q (3 LOP3 + 2 IMAD per swap instead of SHF + 3 LOP3 + IMAD).
+__device__ __forceinline__ void bytes_to_planes_xf(const uint32_t (&src)[8], uint32_t (&w)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = src[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t t = (__umulhi(w[k], 1u << 28) ^ w[k + 4]) & 0x0F0F0F0Fu;
+        w[k + 4] ^= t;
+        w[k] ^= t * 16u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k & 2) continue;
+        const uint32_t t = (__umulhi(w[k], 1u << 30) ^ w[k + 2]) & 0x33333333u;
+        w[k + 2] ^= t;
+        w[k] ^= t * 4u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        const uint32_t t = (__umulhi(w[k], 1u << 31) ^ w[k + 1]) & 0x55555555u;
+        w[k + 1] ^= t;
+        w[k] ^= t * 2u;
+    }
+}
+
+template <int MW>
+__device__ __forceinline__ void select_le4x(const uint32_t (&pl)[4][8][MW], int k, uint32_t (&o)[4][MW],
+                                            uint32_t* xchg, int warp, int lane) {
+    uint32_t e[4][MW], l[4][MW];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int m = 0; m < MW; ++m) {
+            e[p][m] = ~0u;
+            l[p][m] = 0u;
+        }
+    int kk[4] = {k, k, k, k};
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+        uint32_t z[4][MW];
+        int cs[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int m = 0; m < MW; ++m) {
+                z[p][m] = e[p][m] & ~pl[p][j][m];
+                c += __popc(z[p][m]);
+            }
+            cs[p] = int(__reduce_add_sync(0xFFFFFFFFu, c));
+        }
+        uint32_t* buf = xchg + (j & 1) * 8;
+        if (lane == 0)
+            *reinterpret_cast<uint4*>(buf + 4 * warp) = make_uint4(uint32_t(cs[0]), uint32_t(cs[1]), uint32_t(cs[2]),
+                                                                   uint32_t(cs[3]));
+        __syncthreads();
+        const uint4 ot = *reinterpret_cast<const uint4*>(buf + 4 * (warp ^ 1));
+        const int tot[4] = {cs[0] + int(ot.x), cs[1] + int(ot.y), cs[2] + int(ot.z), cs[3] + int(ot.w)};
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (tot[p] < kk[p]) {  // block-uniform
+                kk[p] -= tot[p];
+#pragma unroll
+                for (int m = 0; m < MW; ++m) {
+                    l[p][m] |= z[p][m];
+                    e[p][m] &= pl[p][j][m];
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < MW; ++m) e[p][m] = z[p][m];
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int m = 0; m < MW; ++m) o[p][m] = l[p][m] | e[p][m];
+}
+
+template <int MW>
+__global__ void __launch_bounds__(64, 8)
+    k_mask_q(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ pq4, int n,
+             const uint32_t* __restrict__ ufill, int nfill, int u, int rho_words, const uint8_t* __restrict__ rank,
+             int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask) {
+    constexpr int MCH = 2 * MW;
+    constexpr int STG = mask4_stage_stride(MCH);
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t* rho = dsm;                                   // rho_words: u8 ranks of 4 pixels per slot
+    uint32_t* stage = rho + rho_words;                     // [kM3Px][STG]
+    uint32_t* xchg = stage + kM3Px * STG;                  // [2][2 warps][4 pixels]
+    uint8_t* rrows = reinterpret_cast<uint8_t*>(xchg + 16);  // 4 x 256
+    uint8_t* tile = rrows + 1024;                          // (2h+1) x TW
+    const int G = (n + 31) >> 5;
+    const int TH = 2 * half + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int x0 = blockIdx.x * kM3Px;
+    const int ly = blockIdx.y;
+    const int y = ybeg + ly;
+    const int a0 = (x0 - half) & ~3, ay0 = y - half;
+    const int sh = x0 - half - a0;
+    if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(img) & 3) == 0 && a0 >= 0 && a0 + TW <= W && ay0 >= 0 &&
+        ay0 + TH <= H) {
+        const int nw = TW >> 2;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(img + size_t(ay0) * W + a0);
+        for (int idx = tid; idx < TH * nw; idx += 64) {
+            const int r = idx / nw;
+            reinterpret_cast<uint32_t*>(tile)[idx] = __ldg(src + size_t(r) * (W >> 2) + (idx - r * nw));
+        }
+    } else {
+        for (int idx = tid; idx < TW * TH; idx += 64) {
+            const int r = idx / TW, c = idx - r * TW;
+            const int gx = min(max(a0 + c, 0), W - 1);
+            const int gy = min(max(ay0 + r, 0), H - 1);
+            tile[idx] = __ldg(img + size_t(gy) * W + gx);
+        }
+    }
+    if (tid == 0) rho[u] = 0xFFFFFFFFu;  // sentinel: a = 255 for all four pixels
+    __syncthreads();
+
+    const int k = max(1, n / 4);
+    const int c0 = half * TW + sh + half;  // tile index of pixel x0
+    uint4 rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (tid >> 4)])) + (tid & 15));
+#pragma unroll 1
+    for (int q = 0; q < kM3Px; q += 4) {
+        reinterpret_cast<uint4*>(rrows)[tid] = rr;  // rank rows of pixels q .. q + 3
+        if (q + 4 < kM3Px)
+            rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + q + 4 + (tid >> 4)])) + (tid & 15));
+        __syncthreads();
+        const uint8_t* tq = tile + sh + q;
+        for (int j = tid; j < nfill; j += 64) {  // host fill order (see k_mask4)
+            const uint32_t e = __ldg(ufill + j);
+            const uint8_t* tp = tq + (e & 0xFFFFu);
+            const uint32_t v01 = uint32_t(rrows[tp[0]]) | (uint32_t(rrows[256 + tp[1]]) << 8);
+            const uint32_t v23 = uint32_t(rrows[512 + tp[2]]) | (uint32_t(rrows[768 + tp[3]]) << 8);
+            rho[e >> 16] = v01 | (v23 << 16);
+        }
+        __syncthreads();
+
+        uint32_t pl[4][8][MW];
+#pragma unroll
+        for (int mw = 0; mw < MW; ++mw) {
+            const int m = warp * MW + mw;  // chunk of the shared index tables
+            uint32_t wa[8], wb[8], wc[8], wd[8];
+#pragma unroll
+            for (int t4 = 0; t4 < 8; ++t4) {
+                // one load of P | Q << 16, split on the FMA pipe (k_mask4)
+                const uint4 X = __ldg(pq4 + (m * 8 + t4) * 32 + lane);
+                const uint4 Q = make_uint4(__umulhi(X.x, 65536u), __umulhi(X.y, 65536u), __umulhi(X.z, 65536u),
+                                           __umulhi(X.w, 65536u));
+                const uint4 Pp = make_uint4(X.x - Q.x * 65536u, X.y - Q.y * 65536u, X.z - Q.z * 65536u,
+                                            X.w - Q.w * 65536u);
+                const uint32_t p0 = lds_u32(rho, Pp.x), q0 = lds_u32(rho, Q.x);
+                const uint32_t p1 = lds_u32(rho, Pp.y), q1 = lds_u32(rho, Q.y);
+                const uint32_t p2 = lds_u32(rho, Pp.z), q2 = lds_u32(rho, Q.z);
+                const uint32_t p3 = lds_u32(rho, Pp.w), q3 = lds_u32(rho, Q.w);
+                // The high byte of a u16 max is the max of the high bytes (ties
+                // included), so max.u16x2 of the words gives pixels 1, 3 in bytes 1, 3
+                // and of the words shifted left by 8 (IMAD, FMA pipe) pixels 0, 2.
+                const uint32_t e0 = vmax_u16x2(p0 * 256u, q0 * 256u);  // [. A . C]
+                const uint32_t e1 = vmax_u16x2(p1 * 256u, q1 * 256u);
+                const uint32_t e2 = vmax_u16x2(p2 * 256u, q2 * 256u);
+                const uint32_t e3 = vmax_u16x2(p3 * 256u, q3 * 256u);
+                const uint32_t o0 = vmax_u16x2(p0, q0);  // [. B . D]
+                const uint32_t o1 = vmax_u16x2(p1, q1);
+                const uint32_t o2 = vmax_u16x2(p2, q2);
+                const uint32_t o3 = vmax_u16x2(p3, q3);
+                const uint32_t x01 = __byte_perm(e0, e1, 0x7351);  // [A0 A1 C0 C1]
+                const uint32_t x23 = __byte_perm(e2, e3, 0x7351);  // [A2 A3 C2 C3]
+                const uint32_t y01 = __byte_perm(o0, o1, 0x7351);  // [B0 B1 D0 D1]
+                const uint32_t y23 = __byte_perm(o2, o3, 0x7351);
+                wa[t4] = __byte_perm(x01, x23, 0x5410);
+                wc[t4] = __byte_perm(x01, x23, 0x7632);
+                wb[t4] = __byte_perm(y01, y23, 0x5410);
+                wd[t4] = __byte_perm(y01, y23, 0x7632);
+            }
+            uint32_t t[8];
+            bytes_to_planes_xf(wa, t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl[0][j][mw] = t[j];
+            bytes_to_planes_xf(wb, t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl[1][j][mw] = t[j];
+            bytes_to_planes_xf(wc, t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl[2][j][mw] = t[j];
+            bytes_to_planes_xf(wd, t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pl[3][j][mw] = t[j];
+        }
+        uint32_t o[4][MW];
+        select_le4x<MW>(pl, k, o, xchg, warp, lane);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) store_words<MW>(stage + (q + p) * STG + MCH * lane + MW * warp, o[p]);
+        __syncthreads();  // rho / rrows are rewritten by the next pass
+    }
+    // thread = (word offset w % 8, pixel j)
+    const int rem = n & 31;
+    const uint32_t tail = rem ? (1u << rem) - 1u : ~0u;
+    const int jl = tid & (kM3Px - 1), wl = tid / kM3Px;
+    if (x0 + jl >= Wq) return;
+    uint32_t* dst = mask + size_t(wl) * P + size_t(ly) * Wq + x0 + jl;
+#pragma unroll 4
+    for (int w = wl; w < NW; w += 64 / kM3Px, dst += size_t(64 / kM3Px) * P) {
+        const uint32_t v = stage[jl * STG + w];
+        *dst = w < G - 1 ? v : (w == G - 1 ? v & tail : 0u);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Colour / float-plane path (compute_field on arbitrary GrayImage + LabImage,
 // run_pipeline on RGB).  Same contracts as K1/K2 with float planes.
 //
