@@ -230,7 +230,8 @@ int bsm_debug_check_guards(bsm_ctx* ctx, long long* damaged, int* enabled);
 /* Kernel launches issued by the last pipeline call. */
 int bsm_last_launch_count(bsm_ctx* ctx, int* count);
 /* Measured masked-XOR-popcount word-op throughput of this device (words/s),
- * register-only microbenchmarks of the cost kernel's two instruction mixes:
+ * register-only microbenchmarks of the integer-pipe cost kernel's (K3p,
+ * BSM_K3_VARIANT=16) two instruction mixes:
  * direct (LOP3 + POPC + IADD per word) and carry-save (per two words:
  * 4 LOP3 + POPC + IMAD).  Either pointer may be NULL. */
 int bsm_measure_popc_peak(bsm_ctx* ctx, double* ops_per_s);
