@@ -177,7 +177,8 @@ struct bsm_ctx {
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
                      // 2 x SMs tiles, bit 4 the popcount kernel instead of
-                     // the tensor-core one (bits 0-3 apply to the popcount kernel)
+                     // the tensor-core one (bits 0-3 apply to the popcount kernel),
+                     // bit 5 A in shared memory, bit 7 two operand stages (tensor-core kernel)
     DevBuf popc_out;
     // batch pipelining (bsm_pipeline_batch_u8): two slots of input views and
     // refined maps, an H2D and a D2H copy stream ordered by events
@@ -497,7 +498,11 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
     // tools/microbench/tc_probe: c4 -1.1%, c1/c3 -4%; at 384 columns (c2, c5)
     // +0.6%); BSM_K3_VARIANT bit 5 forces A into shared memory
     const bool at = ncols <= 320 && !(c->k3_variant & 32);
-    const TcSmem L(ncols, masked, at);
+    // with A in TMEM the accumulator (<= 320 columns) leaves room for a third
+    // operand stage in TMEM and shared memory: c4 -1.9%, c1 -2.5%, c3 -3.6%
+    // (tools/microbench/tc_probe); BSM_K3_VARIANT bit 7 keeps two
+    const int stages = at && ncols <= tc_acol(3) && !(c->k3_variant & 128) ? 3 : 2;
+    const TcSmem L(ncols, masked, at, stages);
     if (L.nraw < 2) return set_err(BSM_UNSUPPORTED, "bsm: cost kernel shared-memory layout");
     const size_t sm = L.total;  // > 114 KB: one CTA per SM (it allocates all 512 TMEM columns)
     const int grid = std::min(items, c->sm_count);
@@ -507,7 +512,8 @@ int wta_device_tc(bsm_ctx* c, const uint32_t* dl, const uint32_t* ml, const uint
                                                   ndd, ndir, both ? 0 : dir, items, keys_l, keys_r);
         return BSM_OK;
     };
-    if (at) BSM_TRY(masked ? launch(k_cost_wta_tc<true, true>) : launch(k_cost_wta_tc<false, true>));
+    if (stages == 3) BSM_TRY(masked ? launch(k_cost_wta_tc<true, true, 3>) : launch(k_cost_wta_tc<false, true, 3>));
+    else if (at) BSM_TRY(masked ? launch(k_cost_wta_tc<true, true>) : launch(k_cost_wta_tc<false, true>));
     else BSM_TRY(masked ? launch(k_cost_wta_tc<true, false>) : launch(k_cost_wta_tc<false, false>));
     return check_launch(c, "cost_wta_tc");
 }

@@ -51,10 +51,11 @@
 constexpr int kTcRows = 128;                      // MMA M: reference pixels per tile
 constexpr int kTcKS = 8;                          // u32 words per stage (2 words per MMA K-step)
 constexpr int kTcStages = 2;                      // expanded operand ring (smem A + B)
+constexpr int kTcMaxStages = 3;                   // with A in TMEM and <= 320 accumulator columns
 constexpr int kTcMaxRaw = 8;                      // TMA ring of packed words (as many as fit)
 constexpr int kTcMaxDc = 256;                     // disparities per d-block
 constexpr int kTcMaxCols = 384;                   // accumulator columns (128 + 256 -> 384)
-constexpr int kTcAcol = 384;                      // A operand ring in TMEM (AT kernels): kTcStages x 32 columns
+constexpr int kTcAcol = 384;                      // A operand ring in TMEM (AT kernels): S x 32 columns below kTcSfCol
 constexpr int kTcSfCol = 448;                     // scale factors: SFA cols 448-479, SFB 480-511 (all 1.0)
 constexpr uint32_t kTcSmemLimit = 227 * 1024;     // dynamic shared memory per CTA
 constexpr int kTcProdWarps = 16;                  // producers: warps 0-15
@@ -65,8 +66,10 @@ constexpr int kTcATasks = kTcRows * kTcKS;        // (row, word) A tasks per sta
 constexpr int kTcTasks = (kTcATasks + kTcMaxCols * kTcKS + kTcProdWarps * 32 - 1) / (kTcProdWarps * 32);
 static_assert(kTcATasks % (kTcProdWarps * 32) == 0, "A tasks fill whole task slots");
 constexpr int kTcASlots = kTcATasks / (kTcProdWarps * 32);  // task slots that are A tasks (2)
-static_assert(kTcMaxCols <= kTcAcol && kTcAcol + kTcStages * kTcKS * 4 <= kTcSfCol,
+static_assert(kTcMaxCols <= kTcAcol && kTcAcol + kTcStages * kTcKS * 4 <= kTcSfCol &&
+                  320 <= kTcSfCol - kTcMaxStages * kTcKS * 4,
               "TMEM: accumulator, A ring and scale factors");
+__host__ __device__ constexpr int tc_acol(int stages) { return kTcSfCol - stages * kTcKS * 4; }
 
 __device__ __forceinline__ void tc_wait(uint32_t bar_saddr, uint32_t parity) {
     asm volatile(
@@ -179,7 +182,7 @@ __device__ __forceinline__ TcItem tc_item(int it, int ndd, int ndir, int dir0, i
 // at most kTcMaxRaw), the per-tile popcount bases and the barriers.
 struct TcSmem {
     uint32_t a_sub, b_sub, a_stage, stage, raw_a, raw, nraw, ring, raw_ring, base, bars, total;
-    __host__ __device__ TcSmem(int ncols, bool masked, bool atmem) {
+    __host__ __device__ TcSmem(int ncols, bool masked, bool atmem, int stages = kTcStages) {
         a_sub = kTcRows * 32u;                       // one K-step (64 FP4) of A rows
         b_sub = uint32_t(ncols) * 32u;               // one K-step of B rows
         a_stage = atmem ? 0u : a_sub * (kTcKS / 2);  // A in TMEM: the ring holds B only
@@ -187,17 +190,17 @@ struct TcSmem {
         raw_a = kTcKS * kTcRows * 4u;                // one [KS x 128] word box
         raw = raw_a * (masked ? 2u : 1u) + kTcKS * uint32_t(ncols) * 4u;
         ring = 0;
-        raw_ring = ring + kTcStages * stage;
-        const uint32_t fixed = 2 * 4 * kTcRows * 4 + (2 * kTcStages + 2 * kTcMaxRaw + 6) * 8 + 16;
+        raw_ring = ring + uint32_t(stages) * stage;
+        const uint32_t fixed = 2 * 4 * kTcRows * 4 + (2 * kTcMaxStages + 2 * kTcMaxRaw + 6) * 8 + 16;
         const uint32_t room = kTcSmemLimit > raw_ring + fixed ? kTcSmemLimit - raw_ring - fixed : 0;
         nraw = room / raw < uint32_t(kTcMaxRaw) ? room / raw : uint32_t(kTcMaxRaw);
         base = raw_ring + nraw * raw;
         bars = base + 2 * 4 * kTcRows * 4;
-        total = bars + (2 * kTcStages + 2 * kTcMaxRaw + 6) * 8 + 16;
+        total = bars + (2 * kTcMaxStages + 2 * kTcMaxRaw + 6) * 8 + 16;
     }
 };
 
-template <bool MASKED, bool AT>
+template <bool MASKED, bool AT, int S = kTcStages>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_cost_wta_tc(const __grid_constant__ CUtensorMap l_ref, const __grid_constant__ CUtensorMap l_mask,
                   const __grid_constant__ CUtensorMap l_oth, const __grid_constant__ CUtensorMap r_ref,
@@ -205,14 +208,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   int Wq, int npix, int NW, int D, int Dc, int ncols, int ndd, int ndir, int dir0, int items,
                   uint32_t* __restrict__ keys_l, uint32_t* __restrict__ keys_r) {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    const TcSmem L(ncols, MASKED, AT);
+    const TcSmem L(ncols, MASKED, AT, S);
+    constexpr int ACOL = tc_acol(S);  // AT: the A ring's first TMEM column
     uint8_t* sop = tsm + L.ring;                                         // [S][A: KS/2 x 128 x 32 B][B: KS/2 x ncols x 32 B]
     uint32_t* sraw = reinterpret_cast<uint32_t*>(tsm + L.raw_ring);      // [nraw][desc | mask | span box 0 | box 1]
     uint32_t* sbase = reinterpret_cast<uint32_t*>(tsm + L.base);         // [2 tiles][4 partials][128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(tsm + L.bars);
     uint64_t* full = bars;                               // [S] producers -> MMA (one arrival per warp)
-    uint64_t* empty = full + kTcStages;                  // [S] MMA commit -> producers
-    uint64_t* raw_full = empty + kTcStages;              // [nraw] TMA bytes -> producers
+    uint64_t* empty = full + kTcMaxStages;               // [S] MMA commit -> producers
+    uint64_t* raw_full = empty + kTcMaxStages;           // [nraw] TMA bytes -> producers
     uint64_t* raw_empty = raw_full + kTcMaxRaw;          // [nraw] producers (one arrival per warp) -> loader
     uint64_t* acc_full = raw_empty + kTcMaxRaw;          // MMA commit -> epilogue
     uint64_t* acc_empty = acc_full + 1;                  // epilogue (4 warps) -> MMA
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(full + s, kTcProdWarps);
             mbar_init(empty + s, 1);
         }
@@ -285,12 +289,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
         const int aw0 = tid / kTcRows;  // word of A slot 0 (slot k: aw0 + 4 k)
-        const uint32_t a_taddr = tmem + (uint32_t((warp & 3) * 32) << 16) + kTcAcol;
+        const uint32_t a_taddr = tmem + (uint32_t((warp & 3) * 32) << 16) + ACOL;
         TcRing rr, sr;  // raw ring, operand ring
         int t = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
             uint32_t base = 0;
-            for (int st = 0; st < nst; ++st, rr.next(nraw), sr.next(kTcStages)) {
+            for (int st = 0; st < nst; ++st, rr.next(nraw), sr.next(S)) {
                 const uint32_t r = rr.slot, s = sr.slot;
                 tc_wait(raw_full + r, rr.phase);
                 const uint32_t* raw = sraw + r * (L.raw / 4);
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++t) {
             tc_wait(acc_empty, (uint32_t(t) & 1u) ^ 1u);
             tc_fence_after();
-            for (int st = 0; st < nst; ++st, sr.next(kTcStages)) {
+            for (int st = 0; st < nst; ++st, sr.next(S)) {
                 const uint32_t s = sr.slot;
                 tc_wait(full + s, sr.phase);
                 tc_fence_after();
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         const uint32_t b_addr = sop_addr + s * L.stage + L.a_stage + j * L.b_sub;
                         const uint32_t acc = (st > 0 || j > 0) ? 1u : 0u;
                         if constexpr (AT) {
-                            const uint32_t at = tmem + kTcAcol + s * (kTcKS * 4) + j * 8;
+                            const uint32_t at = tmem + ACOL + s * (kTcKS * 4) + j * 8;
                             tc_mma_mxf4_ts(tmem, at, tc_smem_desc(b_addr), id1, sfa, sfb, acc);
                             if (n2 > 0)
                                 tc_mma_mxf4_ts(tmem + uint32_t(n1), at, tc_smem_desc(b_addr + uint32_t(n1 / 8) * 256u),

@@ -58,6 +58,7 @@ int main(int argc, char** argv) {
     const int reps = argc > 6 ? std::atoi(argv[6]) : 5;
     const int dirsel = argc > 7 ? std::atoi(argv[7]) : 2;  // 0 left only, 1 right only, 2 both
     const bool at = argc > 8 ? std::atoi(argv[8]) != 0 : true;  // A operand in TMEM
+    const int stages = argc > 9 ? std::atoi(argv[9]) : 2;         // operand ring depth (3: A in TMEM only)
     const int Wq = (W + 3) / 4 * 4;
     const int npix = H * Wq;
     const size_t P = (size_t(npix) + 31) / 32 * 32;
@@ -98,9 +99,10 @@ int main(int argc, char** argv) {
     const int items = tiles * ndd * ndir;
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    const size_t sm = TcSmem(ncols, masked, at).total;
-    auto kern = masked ? (at ? k_cost_wta_tc<true, true> : k_cost_wta_tc<true, false>)
-                       : (at ? k_cost_wta_tc<false, true> : k_cost_wta_tc<false, false>);
+    const size_t sm = TcSmem(ncols, masked, at, stages).total;
+    auto kern = stages == 3 ? (masked ? k_cost_wta_tc<true, true, 3> : k_cost_wta_tc<false, true, 3>)
+                : masked ? (at ? k_cost_wta_tc<true, true> : k_cost_wta_tc<true, false>)
+                         : (at ? k_cost_wta_tc<false, true> : k_cost_wta_tc<false, false>);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     const int grid = std::min(items, nsm);
     auto tmap = [&](const uint32_t* field, int box_x) {
@@ -178,7 +180,7 @@ int main(int argc, char** argv) {
     evals *= H;
     std::printf("W %d H %d NW %d D %d masked %d: ncols %d ndd %d items %d grid %d smem %zu nraw %u: %.3f ms both directions, "
                 "%.1f G word-ops/s, %.0f Mdisp-evals/s (cost only, x2 dirs)\n",
-                W, H, NW, D, int(masked), ncols, ndd, items, grid, sm, TcSmem(ncols, masked, at).nraw, best, evals * NW / best / 1e6,
+                W, H, NW, D, int(masked), ncols, ndd, items, grid, sm, TcSmem(ncols, masked, at, stages).nraw, best, evals * NW / best / 1e6,
                 evals / 2 / best / 1e3);
     return bad ? 2 : 0;
 }
