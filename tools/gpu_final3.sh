@@ -21,11 +21,11 @@ timeout 600 python bench.py --steps 1 --warmup 1 --profile-only --pairs 4 > gpur
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_c4.csv \
     python bench.py --steps 1 --warmup 1 --profile-only --pairs 4 > gpurun_out/${T}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 300 python tools/profile_pipeline.py c4 1 > gpurun_out/${T}_plain.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_cost_wta|k_mask4|k_descriptor4|k_vote_refine_fold|k_lr_check_keys" -c 5 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_cost_wta|k_mask|k_descriptor4|k_vote_refine_fold|k_lr_check_keys" -c 5 \
     -o gpurun_out/${T}_c4_full python tools/profile_pipeline.py c4 1 > gpurun_out/${T}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 python tools/summarize_ncu.py gpurun_out/${T}_c4_full.ncu-rep > gpurun_out/${T}_ncu_kernels_c4.txt 2>&1
 for wl in c1 c2 c3 c4 c5; do
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_cost_wta|k_mask4" -c 3 --csv \
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_cost_wta|k_mask" -c 3 --csv \
       --log-file gpurun_out/${T}_traffic_$wl.csv python tools/profile_pipeline.py $wl 1 > /dev/null 2>&1; echo "traffic $wl rc=$?"
 done
 timeout 300 python tools/profile_colour.py > gpurun_out/${T}_colour_plain.log 2>&1 && \
