@@ -548,7 +548,7 @@ def main():
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get("k_cost_wta_tc", {}).get(args.workload)
-        mask_traffic = tj.get("k_mask4", {}).get(args.workload)
+        mask_traffic = tj.get("k_mask", {}).get(args.workload)
     smem_peak = 128 * sms * clk * 1e6  # B/s: 128 B/clk/SM
     line["roofline_cost"] = {
         "bound": "tensor (tcgen05 kind::mxf4, dense FP4)",
@@ -577,18 +577,25 @@ def main():
     }
     mask_ms = prof_ms.get("mask", 0.0)
     if mask_ms > 0 and not colour:
-        # K2: 2 rank gathers per pair and pixel, u16x2-packed for two pixels:
-        # n / 32 conflict-free wavefronts per pixel; the LSU serves 1 per clk per SM
-        wf = 2 * W * rows_c * (4096 // 32)  # both views
+        # K2: 2 rank gathers per pair and pixel; the ranks are u8, so one 32-bit
+        # shared-memory gather can serve four pixels (k_mask_q does):
+        # n / 64 conflict-free wavefronts per pixel is the gather floor of any
+        # table-driven implementation; the LSU serves 1 per clk per SM
+        # (the library's choice for n = 4096: k_mask_q unless BSM_MASK_VARIANT selects k_mask4)
+        mask_kernel = "k_mask4" if int(os.environ.get("BSM_MASK_VARIANT", "0")) & 3 else "k_mask_q"
+        wf = 2 * W * rows_c * (4096 // 64)  # both views
         wf_peak = sms * clk * 1e6
         line["roofline_mask"] = {"bound": "smem (L1 shared-memory wavefronts of the rank gathers)",
-                                 "kernel": "k_mask4 (both views)",
+                                 "kernel": f"{mask_kernel} (both views)",
                                  "achieved": wf * 128 / (mask_ms * 1e-3) / 1e9, "peak": smem_peak / 1e9,
                                  "unit": "GB/s", "frac": wf / (mask_ms * 1e-3) / wf_peak, "traffic": mask_traffic,
                                  "peak_source": f"1 wavefront (128 B) / clk / SM x {sms} SMs x {clk:.0f} MHz",
                                  "kernel_ms": mask_ms, "wavefronts": wf,
-                                 "unit_def": "n/32 = 128 rank-gather wavefronts per pixel (2 per pair, two pixels "
-                                             "per u32), 128 B each"}
+                                 "unit_def": "n/64 = 64 rank-gather wavefronts per pixel (2 gathers per pair, four "
+                                             "pixels' u8 ranks per u32), 128 B each",
+                                 "note": "the kernel is instruction-issue-bound (~69% issue slots busy, L1 58%, "
+                                         "ncu: profiles/r02_ncu_kernels_c4.txt): bit-plane transposes and the "
+                                         "select, not the gathers, set its time"}
     # the contract's `roofline` is the dominant kernel of the step (by measured stage time)
     cands = [line["roofline_cost"]] + ([line["roofline_mask"]] if "roofline_mask" in line else [])
     line["roofline"] = dict(max(cands, key=lambda r: r["kernel_ms"]))
