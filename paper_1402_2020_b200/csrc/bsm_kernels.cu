@@ -185,6 +185,12 @@ struct bsm_ctx {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     DevBuf bimg[2][2], bout_d[2], bout_v[2];
     cudaEvent_t ev_in[2] = {}, ev_free[2] = {}, ev_done[2] = {}, ev_out[2] = {};
+    // batches: the check + refine of pair i (phase B) run on s_ref, a
+    // high-priority stream, beside the fields of pair i + 1 (phase A) on
+    // `stream`; two sets of WTA keys alternate between the phases
+    cudaStream_t s_ref = nullptr;
+    cudaEvent_t ev_a[2] = {}, ev_b[2] = {};
+    DevBuf keys_l2, keys_r2;
 };
 
 namespace {
@@ -194,7 +200,7 @@ std::vector<DevBuf*> ctx_bufs(bsm_ctx* c) {
             &c->d_uxy, &c->d_rank, &c->d_wtab, &c->d_s2col, &c->img_l, &c->img_r, &c->fdl, &c->fml, &c->fdr,
             &c->fmr, &c->keys_l, &c->keys_r, &c->keys_u, &c->chk_d, &c->chk_v, &c->ref_d, &c->ref_v, &c->lw_d,
             &c->rw_d, &c->un_d, &c->counters, &c->inv, &c->vmap, &c->d_etab, &c->d_elam, &c->d_lab256, &c->aux0,
-            &c->aux1, &c->aux2, &c->aux3, &c->popc_out, &c->bimg[0][0], &c->bimg[0][1], &c->bimg[1][0],
+            &c->keys_l2, &c->keys_r2, &c->aux1, &c->aux2, &c->aux3, &c->popc_out, &c->bimg[0][0], &c->bimg[0][1], &c->bimg[1][0],
             &c->bimg[1][1], &c->bout_d[0], &c->bout_d[1], &c->bout_v[0], &c->bout_v[1]};
 }
 
@@ -725,8 +731,10 @@ struct Views {
     const float4* lr = nullptr;
 };
 
+// phases: 1 = fields + WTA (A), 2 = check + refine (B), 3 = both; the WTA
+// keys go to keys_l/keys_r, or to the second set with alt_keys (batches).
 int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_rows, const bsm_params* p,
-                    bool want_unmasked) {
+                    bool want_unmasked, int phases = 3, bool alt_keys = false) {
     BSM_TRY(check_pattern(c));
     BSM_TRY(validate_params(p));
     const int r0 = std::max(0, out0 - p->vote_radius);
@@ -751,6 +759,9 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
     BSM_TRY(c->counters.ensure(64));
     BSM_TRY(c->inv.ensure(px * 4));
 
+    uint32_t* kl = (alt_keys ? c->keys_l2 : c->keys_l).as<uint32_t>();
+    uint32_t* kr = (alt_keys ? c->keys_r2 : c->keys_r).as<uint32_t>();
+    if (phases & 1) {
     if (v.u8l) {
         BSM_TRY(field_device(c, v.u8l, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
         BSM_TRY(field_device(c, v.u8r, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
@@ -760,25 +771,24 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
     }
     if (c->k3_variant & 2) {  // one launch per direction
         BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
-                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 0, true, c->keys_l.as<uint32_t>(),
-                           c->keys_r.as<uint32_t>(), T_WTA));
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 0, true, kl, kr, T_WTA));
         BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
-                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 1, true, c->keys_l.as<uint32_t>(),
-                           c->keys_r.as<uint32_t>(), T_WTA));
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, false, 1, true, kl, kr, T_WTA));
     } else {
         BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), c->fdr.as<uint32_t>(),
-                           c->fmr.as<uint32_t>(), W, rows, p->d_max, true, 0, true, c->keys_l.as<uint32_t>(),
-                           c->keys_r.as<uint32_t>(), T_WTA));
+                           c->fmr.as<uint32_t>(), W, rows, p->d_max, true, 0, true, kl, kr, T_WTA));
     }
     if (want_unmasked)
         BSM_TRY(wta_device(c, c->fdl.as<uint32_t>(), nullptr, c->fdr.as<uint32_t>(), nullptr, W, rows, p->d_max, false,
                            0, false, c->keys_u.as<uint32_t>(), nullptr, T_WTA_U));
+    }
+    if (!(phases & 2)) return BSM_OK;
     {
         Scope s(c, T_LR);
         BSM_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
         const int tb = 256;
         (c->peer.n > 0 ? k_lr_check_keys<true> : k_lr_check_keys<false>)<<<unsigned((px + tb - 1) / tb), tb, 0, c->stream>>>(
-            c->keys_l.as<uint32_t>(), c->keys_r.as<uint32_t>(), W, rows, p->lr_tolerance, c->chk_d.as<float>(),
+            kl, kr, W, rows, p->lr_tolerance, c->chk_d.as<float>(),
             c->chk_v.as<uint8_t>(), c->lw_d.as<float>(), c->rw_d.as<float>(), out0 - r0, out0 - r0 + out_rows,
             c->counters.as<int>(), c->inv.as<int>(), c->peer);
         BSM_TRY(check_launch(c, "lr_check"));
@@ -876,6 +886,35 @@ int invalid_list(bsm_ctx* c, size_t px, double lim, int& max_bin) {
     return BSM_OK;
 }
 
+// One pair of a batch in two phases: A (fields + WTA, keys set i % 2) on the
+// context stream, then B (check + refine) on the high-priority s_ref, so that
+// pair i's latency-bound refine runs beside pair i+1's descriptor / mask
+// kernels (the block scheduler serves the higher-priority stream's CTAs as
+// SMs free up).  Pair i+2's WTA waits until pair i's check has read that key
+// set; phase B's buffers (check, refine, counters) are serial on s_ref.  After
+// the call, s_ref holds pair i's remaining work (the caller appends its copies
+// there); batch_join orders the context stream after all of it.
+int batch_pair(bsm_ctx* c, int i, const Views& v, int W, int H, const bsm_params* params) {
+    const int k = i & 1;
+    if (i >= 2) BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_b[k], 0));  // key set k read by pair i-2
+    BSM_TRY(pipeline_device(c, v, W, H, 0, H, params, false, 1, k == 1));
+    BSM_CUDA(cudaEventRecord(c->ev_a[k], c->stream));
+    BSM_CUDA(cudaStreamWaitEvent(c->s_ref, c->ev_a[k], 0));
+    const cudaStream_t main = c->stream;
+    c->stream = c->s_ref;
+    const int rc = pipeline_device(c, v, W, H, 0, H, params, false, 2, k == 1);
+    c->stream = main;
+    BSM_TRY(rc);
+    return cudaEventRecord(c->ev_b[k], c->s_ref) == cudaSuccess ? BSM_OK
+                                                                : set_err(BSM_CUDA_ERROR, "CUDA: event record failed");
+}
+
+int batch_join(bsm_ctx* c) {
+    BSM_CUDA(cudaEventRecord(c->ev_a[0], c->s_ref));
+    BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_a[0], 0));
+    return BSM_OK;
+}
+
 // Copy streams, events and the two slots of views / refined maps used to
 // overlap pair i's compute with pair i+1's upload and pair i-1's download.
 int ensure_batch(bsm_ctx* c, size_t px) {
@@ -883,9 +922,14 @@ int ensure_batch(bsm_ctx* c, size_t px) {
         BSM_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
         BSM_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s)
-            for (cudaEvent_t* e : {&c->ev_in[s], &c->ev_free[s], &c->ev_done[s], &c->ev_out[s]})
+            for (cudaEvent_t* e : {&c->ev_in[s], &c->ev_free[s], &c->ev_done[s], &c->ev_out[s], &c->ev_a[s], &c->ev_b[s]})
                 BSM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        int lo = 0, hi = 0;
+        BSM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        BSM_CUDA(cudaStreamCreateWithPriority(&c->s_ref, cudaStreamNonBlocking, hi));
     }
+    BSM_TRY(c->keys_l2.ensure(px * 4));
+    BSM_TRY(c->keys_r2.ensure(px * 4));
     for (int s = 0; s < 2; ++s) {
         BSM_TRY(c->bimg[s][0].ensure(px));
         BSM_TRY(c->bimg[s][1].ensure(px));
@@ -994,10 +1038,11 @@ int bsm_ctx_destroy(bsm_ctx* c) {
     cudaSetDevice(c->device);
     for (DevBuf* b : ctx_bufs(c)) b->release();
     for (int s = 0; s < 2; ++s) {
-        for (cudaEvent_t e : {c->ev_in[s], c->ev_free[s], c->ev_done[s], c->ev_out[s]})
+        for (cudaEvent_t e : {c->ev_in[s], c->ev_free[s], c->ev_done[s], c->ev_out[s], c->ev_a[s], c->ev_b[s]})
             if (e) cudaEventDestroy(e);
     }
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_ref) cudaStreamDestroy(c->s_ref);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (int t = 0; t < T_COUNT; ++t)
         for (int s = 0; s < bsm_ctx::kEvPerSlot; ++s) {
@@ -1359,13 +1404,13 @@ int bsm_pipeline_batch_u8(bsm_ctx* c, int n_pairs, const uint8_t* const* lefts, 
         BSM_CUDA(cudaMemcpyAsync(c->bimg[s][1].p, rights[i], px, cudaMemcpyHostToDevice, c->s_h2d));
         BSM_CUDA(cudaEventRecord(c->ev_in[s], c->s_h2d));
         BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
-        BSM_TRY(pipeline_device(c, u8views(c->bimg[s][0].as<uint8_t>(), c->bimg[s][1].as<uint8_t>()), W, H, 0, H,
-                                params, false));
-        BSM_CUDA(cudaEventRecord(c->ev_free[s], c->stream));
-        if (i >= 2) BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out[s], 0));  // slot map downloaded
-        BSM_CUDA(cudaMemcpyAsync(c->bout_d[s].p, c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
-        BSM_CUDA(cudaMemcpyAsync(c->bout_v[s].p, c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
-        BSM_CUDA(cudaEventRecord(c->ev_done[s], c->stream));
+        const Views v = u8views(c->bimg[s][0].as<uint8_t>(), c->bimg[s][1].as<uint8_t>());
+        BSM_TRY(batch_pair(c, i, v, W, H, params));  // phase B of pair i on s_ref from here
+        BSM_CUDA(cudaEventRecord(c->ev_free[s], c->s_ref));  // views consumed (the refine reads the left one)
+        if (i >= 2) BSM_CUDA(cudaStreamWaitEvent(c->s_ref, c->ev_out[s], 0));  // slot map downloaded
+        BSM_CUDA(cudaMemcpyAsync(c->bout_d[s].p, c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->s_ref));
+        BSM_CUDA(cudaMemcpyAsync(c->bout_v[s].p, c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->s_ref));
+        BSM_CUDA(cudaEventRecord(c->ev_done[s], c->s_ref));
         BSM_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_done[s], 0));
         if (refined_d && refined_d[i])
             BSM_CUDA(cudaMemcpyAsync(refined_d[i], c->bout_d[s].p, px * 4, cudaMemcpyDeviceToHost, c->s_d2h));
@@ -1373,6 +1418,7 @@ int bsm_pipeline_batch_u8(bsm_ctx* c, int n_pairs, const uint8_t* const* lefts, 
             BSM_CUDA(cudaMemcpyAsync(refined_v[i], c->bout_v[s].p, px, cudaMemcpyDeviceToHost, c->s_d2h));
         BSM_CUDA(cudaEventRecord(c->ev_out[s], c->s_d2h));
     }
+    BSM_TRY(batch_join(c));
     BSM_CUDA(cudaStreamSynchronize(c->s_d2h));
     return sync(c);
 }
@@ -1389,14 +1435,16 @@ int bsm_pipeline_batch_u8_device(bsm_ctx* c, int n_pairs, const uint8_t* const* 
     BSM_TRY(check_batch_ptrs(n_pairs, reinterpret_cast<const void* const*>(d_lefts),
                              reinterpret_cast<const void* const*>(d_rights)));
     const size_t px = size_t(W) * H;
+    if (n_pairs == 0) return BSM_OK;
+    BSM_TRY(ensure_batch(c, px));
     for (int i = 0; i < n_pairs; ++i) {
-        BSM_TRY(pipeline_device(c, u8views(d_lefts[i], d_rights[i]), W, H, 0, H, params, false));
+        BSM_TRY(batch_pair(c, i, u8views(d_lefts[i], d_rights[i]), W, H, params));
         if (d_refined_d && d_refined_d[i])
-            BSM_CUDA(cudaMemcpyAsync(d_refined_d[i], c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->stream));
+            BSM_CUDA(cudaMemcpyAsync(d_refined_d[i], c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice, c->s_ref));
         if (d_refined_v && d_refined_v[i])
-            BSM_CUDA(cudaMemcpyAsync(d_refined_v[i], c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->stream));
+            BSM_CUDA(cudaMemcpyAsync(d_refined_v[i], c->ref_v.p, px, cudaMemcpyDeviceToDevice, c->s_ref));
     }
-    return BSM_OK;
+    return batch_join(c);
 }
 
 // Guard mode (BSM_GUARD=1): damaged guard bytes over every device buffer of
