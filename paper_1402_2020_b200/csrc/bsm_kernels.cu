@@ -173,7 +173,7 @@ struct bsm_ctx {
     PeerOut peer{};  // peer-memory band outputs during bsm_pipeline_frame_bands_p2p_u8 (n = 0 otherwise)
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
     int maskf_force_low = 0;  // test hook (BSM_MASKF_FORCE_LOW=1): k_mask_f32 resolves every low byte
-    int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4
+    int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4 (implies k_mask4), bit 1 k_mask4 instead of k_mask_q
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
                      // 2 x SMs tiles, bit 4 the popcount kernel instead of
