@@ -214,15 +214,17 @@ int bsm_pipeline_pairs_sharded_u8(bsm_ctx* c, bsm_comm* m, int n_pairs, const ui
             BSM_CUDA(cudaMemcpyAsync(c->bimg[s][1].p, rights[i], px, cudaMemcpyHostToDevice, c->s_h2d));
             BSM_CUDA(cudaEventRecord(c->ev_in[s], c->s_h2d));
             BSM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
-            BSM_TRY(pipeline_device(c, u8views(c->bimg[s][0].as<uint8_t>(), c->bimg[s][1].as<uint8_t>()), W, H, 0, H,
-                                    params, false));
-            BSM_CUDA(cudaEventRecord(c->ev_free[s], c->stream));
+            // two phases per pair (batch_pair): this pair's refine beside the next one's fields
+            BSM_TRY(batch_pair(c, i - u0, u8views(c->bimg[s][0].as<uint8_t>(), c->bimg[s][1].as<uint8_t>()), W, H,
+                               params));
+            BSM_CUDA(cudaEventRecord(c->ev_free[s], c->s_ref));
             const size_t k = size_t(i - u0);
             BSM_CUDA(cudaMemcpyAsync(m->shard_d.as<float>() + k * px, c->ref_d.p, px * 4, cudaMemcpyDeviceToDevice,
-                                     c->stream));
+                                     c->s_ref));
             BSM_CUDA(cudaMemcpyAsync(m->shard_v.as<uint8_t>() + k * px, c->ref_v.p, px, cudaMemcpyDeviceToDevice,
-                                     c->stream));
+                                     c->s_ref));
         }
+        BSM_TRY(batch_join(c));
     }
     NcclApi& a = nccl();
     const float* own_d = m->shard_d.as<float>();
