@@ -917,7 +917,9 @@ int batch_join(bsm_ctx* c) {
 
 // Copy streams, events and the two slots of views / refined maps used to
 // overlap pair i's compute with pair i+1's upload and pair i-1's download.
-int ensure_batch(bsm_ctx* c, size_t px) {
+// slots: the host-buffer batch's two slots of device views and maps (the
+// device batch needs only the streams, events and the second key set).
+int ensure_batch(bsm_ctx* c, size_t px, bool slots = true) {
     if (!c->s_h2d) {
         BSM_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
         BSM_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
@@ -930,7 +932,7 @@ int ensure_batch(bsm_ctx* c, size_t px) {
     }
     BSM_TRY(c->keys_l2.ensure(px * 4));
     BSM_TRY(c->keys_r2.ensure(px * 4));
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 2 && slots; ++s) {
         BSM_TRY(c->bimg[s][0].ensure(px));
         BSM_TRY(c->bimg[s][1].ensure(px));
         BSM_TRY(c->bout_d[s].ensure(px * 4));
@@ -1436,7 +1438,7 @@ int bsm_pipeline_batch_u8_device(bsm_ctx* c, int n_pairs, const uint8_t* const* 
                              reinterpret_cast<const void* const*>(d_rights)));
     const size_t px = size_t(W) * H;
     if (n_pairs == 0) return BSM_OK;
-    BSM_TRY(ensure_batch(c, px));
+    BSM_TRY(ensure_batch(c, px, false));
     for (int i = 0; i < n_pairs; ++i) {
         BSM_TRY(batch_pair(c, i, u8views(d_lefts[i], d_rights[i]), W, H, params));
         if (d_refined_d && d_refined_d[i])
