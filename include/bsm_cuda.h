@@ -133,13 +133,16 @@ int bsm_pipeline_u8(bsm_ctx* ctx, const uint8_t* left, const uint8_t* right, int
  * (BASELINE configs[3]), host buffers: lefts[i] / rights[i] are W x H views,
  * refined_d[i] / refined_v[i] receive pair i's refined map (either array, or
  * any entry, may be NULL).  Uploads, compute and downloads of consecutive pairs
- * overlap (two device slots, separate copy streams); returns when every map
- * has landed.  Pinned host buffers make the copies asynchronous. */
+ * overlap (two device slots, separate copy streams), and each pair's check +
+ * refine runs on an internal high-priority stream beside the next pair's
+ * descriptor / mask kernels; returns when every map has landed.  Pinned host
+ * buffers make the copies asynchronous. */
 int bsm_pipeline_batch_u8(bsm_ctx* ctx, int n_pairs, const uint8_t* const* lefts, const uint8_t* const* rights,
                           int W, int H, const bsm_params* params, float* const* refined_d,
                           uint8_t* const* refined_v);
 /* Device-resident batch: d_lefts / d_rights / d_refined_* are host arrays of
- * DEVICE pointers; work is queued on bsm_stream() and not synchronised. */
+ * DEVICE pointers; work is queued on bsm_stream() (the internal refine stream
+ * is joined back into it before the call returns) and not synchronised. */
 int bsm_pipeline_batch_u8_device(bsm_ctx* ctx, int n_pairs, const uint8_t* const* d_lefts,
                                  const uint8_t* const* d_rights, int W, int H, const bsm_params* params,
                                  float* const* d_refined_d, uint8_t* const* d_refined_v);
