@@ -363,7 +363,11 @@ size_t mask4_smem(const bsm_ctx* c) {
 
 
 // Descriptors + masks of rows [ybeg, ybeg + rows) of a W x H view on device.
-int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask) {
+// With img2 (desc2, mask2): the second view of a pair in the same launches
+// (grid.z), one launch tail per kernel instead of two.
+int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int rows, uint32_t* desc, uint32_t* mask,
+                 const uint8_t* img2 = nullptr, uint32_t* desc2 = nullptr, uint32_t* mask2 = nullptr) {
+    const int nviews = img2 ? 2 : 1;
     const int Wp = round_up(W, 128), Wq = field_pitch(W);
     const size_t P = field_plane(W, rows);
     BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
@@ -375,17 +379,19 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         dim3 grid(Wp / (kD2TX * 4), (rows + kD2TY * kD2Rows - 1) / (kD2TY * kD2Rows));
         // split the word range over grid.z until there are ~16 CTAs per SM (the
         // tail of a partial last wave dominates otherwise; c2: 759 -> 3036 CTAs)
-        grid.z = unsigned(std::max(1, std::min((c->NW + 7) / 8, (16 * c->sm_count + int(grid.x * grid.y) - 1) /
-                                                                    int(grid.x * grid.y))));
+        const int zsplit = std::max(1, std::min((c->NW + 7) / 8, (16 * c->sm_count + int(grid.x * grid.y) - 1) /
+                                                                   int(grid.x * grid.y)));
+        grid.z = unsigned(zsplit * nviews);
         BSM_CUDA(cudaFuncSetAttribute(k_descriptor4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
         k_descriptor4<<<grid, dim3(kD2TX, kD2TY), sm, c->stream>>>(img, W, H, ybeg, rows, c->d_desc4.as<int2>(),
-                                                                    c->n, c->half, TWs, c->NW, Wq, P, desc);
+                                                                    c->n, c->half, TWs, c->NW, Wq, P, desc, img2,
+                                                                    desc2, zsplit);
         BSM_TRY(check_launch(c, "descriptor"));
     }
     {
         Scope s(c, T_MASK);
         const size_t sm4 = mask4_smem(c);
-        dim3 grid3((Wq + kM3Px - 1) / kM3Px, rows);
+        dim3 grid3((Wq + kM3Px - 1) / kM3Px, rows, nviews);
         auto launch = [&](auto kern) -> int {
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm4)));
             const bool packed = c->mch <= 4 && !(c->mask_variant & 1);
@@ -393,7 +399,7 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
                                                 c->d_pqb.as<uint4>() + (packed ? 2 * kPqTable / 4 : 0),
                                                 c->d_pqb.as<uint4>() + kPqTable / 4, c->n, c->d_uoff.as<uint32_t>(),
                                                 c->nfill, c->mslots, round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(),
-                                                c->half, mask4_tw(c->half), c->NW, Wq, P, mask);
+                                                c->half, mask4_tw(c->half), c->NW, Wq, P, mask, img2, mask2);
             return BSM_OK;
         };
         // MCH = 2, 4 (1024 < n <= 4096): four pixels per pass over u8 ranks,
@@ -406,7 +412,7 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
                 kern<<<grid3, 64, smq, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * kPqTable / 4,
                                                     c->n, c->d_uoff.as<uint32_t>(), c->nfill, c->mslots,
                                                     round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(), c->half,
-                                                    mask4_tw(c->half), c->NW, Wq, P, mask);
+                                                    mask4_tw(c->half), c->NW, Wq, P, mask, img2, mask2);
                 return BSM_OK;
             };
             BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1>) : launch_q(k_mask_q<2>));
@@ -763,8 +769,8 @@ int pipeline_device(bsm_ctx* c, const Views& v, int W, int H, int out0, int out_
     uint32_t* kr = (alt_keys ? c->keys_r2 : c->keys_r).as<uint32_t>();
     if (phases & 1) {
     if (v.u8l) {
-        BSM_TRY(field_device(c, v.u8l, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
-        BSM_TRY(field_device(c, v.u8r, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
+        BSM_TRY(field_device(c, v.u8l, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>(), v.u8r,
+                             c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));
     } else {
         BSM_TRY(field_device_f32(c, v.gl, v.ll, W, H, r0, rows, c->fdl.as<uint32_t>(), c->fml.as<uint32_t>()));
         BSM_TRY(field_device_f32(c, v.gr, v.lr, W, H, r0, rows, c->fdr.as<uint32_t>(), c->fmr.as<uint32_t>()));

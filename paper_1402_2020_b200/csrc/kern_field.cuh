@@ -31,7 +31,15 @@ __device__ __forceinline__ uint32_t ld_off(const uint32_t* base, int off) {
 __global__ void __launch_bounds__(kD2TX* kD2TY)
     k_descriptor4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows,
                   const int2* __restrict__ ptab, int n, int half, int TWs, int NW, int Wq, size_t P,
-                  uint32_t* __restrict__ desc) {
+                  uint32_t* __restrict__ desc, const uint8_t* __restrict__ img2, uint32_t* __restrict__ desc2,
+                  int zsplit) {
+    // grid.z = views x zsplit word ranges: both views of a pair in one launch
+    // (one tail instead of two)
+    const int view = int(blockIdx.z) / zsplit, zz = int(blockIdx.z) - view * zsplit;
+    if (view) {
+        img = img2;
+        desc = desc2;
+    }
     // tile: clamped bytes; t4[i] = bytes i..i+3 of the tile, so the 4 samples
     // of a thread's 4 pixels at any offset are one aligned 32-bit load.
     extern __shared__ __align__(16) uint32_t dsm[];
@@ -63,8 +71,8 @@ __global__ void __launch_bounds__(kD2TX* kD2TY)
     const int rowW = TWs >> 2;
     const int full = n >> 5;
     // blockIdx.z splits the word range (small images: more CTAs than SMs)
-    const int wper = (NW + gridDim.z - 1) / gridDim.z;
-    const int wbeg = blockIdx.z * wper, wend = min(NW, wbeg + wper);
+    const int wper = (NW + zsplit - 1) / zsplit;
+    const int wbeg = zz * wper, wend = min(NW, wbeg + wper);
     for (int w = wbeg; w < wend; ++w) {
         uint32_t acc[kD2Rows][4];
 #pragma unroll
@@ -332,7 +340,12 @@ template <int MCH, bool PACKED = false>
 __global__ void __launch_bounds__(32, 16)
     k_mask4(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ p4,
             const uint4* __restrict__ q4, int n, const uint32_t* __restrict__ ufill, int nfill, int u, int rho_words,
-            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask) {
+            const uint8_t* __restrict__ rank, int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask,
+            const uint8_t* __restrict__ img2, uint32_t* __restrict__ mask2) {
+    if (blockIdx.z) {  // second view of the pair (grid.z = 2)
+        img = img2;
+        mask = mask2;
+    }
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho2 = dsm;                                 // 2 x rho_words (u + sentinel, padded): two passes' tables
     constexpr int STG = mask4_stage_stride(MCH);
@@ -587,7 +600,12 @@ template <int MW>
 __global__ void __launch_bounds__(64, 8)
     k_mask_q(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ pq4, int n,
              const uint32_t* __restrict__ ufill, int nfill, int u, int rho_words, const uint8_t* __restrict__ rank,
-             int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask) {
+             int half, int TW, int NW, int Wq, size_t P, uint32_t* __restrict__ mask, const uint8_t* __restrict__ img2,
+             uint32_t* __restrict__ mask2) {
+    if (blockIdx.z) {  // second view of the pair (grid.z = 2)
+        img = img2;
+        mask = mask2;
+    }
     constexpr int MCH = 2 * MW;
     constexpr int STG = mask4_stage_stride(MCH);
     extern __shared__ __align__(16) uint32_t dsm[];
