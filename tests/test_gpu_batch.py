@@ -102,3 +102,34 @@ def test_repeated_runs_bit_identical(ctx):
         assert again.refined == first.refined and again.checked == first.checked
         assert np.array_equal(again.left_wta.disparity, first.left_wta.disparity)
         assert np.array_equal(again.right_wta.disparity, first.right_wta.disparity)
+
+
+def test_batches_back_to_back_without_sync(ctx):
+    """The batch calls run each pair's check + refine on an internal
+    high-priority stream and join it back into bsm_stream(): a device batch
+    left unsynchronised, then a host batch of another shape, then a single-pair
+    call on the same context must all equal the single-pair pipeline."""
+    import torch
+    from paper_1402_2020_b200._lib import bsm_params, check, lib
+    cfg_a = bsm.BsmConfig(d_max=33, vote_radius=7)
+    pairs_a = [synth_pair(0, 300 + i, 120, 41) for i in range(4)]
+    cfg_b = bsm.BsmConfig(d_max=21)
+    pairs_b = [synth_pair(0, 400 + i, 77, 29) for i in range(3)]
+    want_a = [bsm.run_pipeline(l, r, cfg_a, ctx=ctx, outputs="refined").refined for l, r in pairs_a]
+    want_b = [bsm.run_pipeline(l, r, cfg_b, ctx=ctx, outputs="refined").refined for l, r in pairs_b]
+    dl = [torch.from_numpy(l).cuda() for l, _ in pairs_a]
+    dr = [torch.from_numpy(r).cuda() for _, r in pairs_a]
+    od = [torch.empty((41, 120), dtype=torch.float32, device="cuda") for _ in pairs_a]
+    ov = [torch.empty((41, 120), dtype=torch.uint8, device="cuda") for _ in pairs_a]
+    arr = lambda ts: (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    torch.cuda.synchronize()
+    p = bsm_params(33, 9.0, 16.0, 1.0, 7)
+    check(lib().bsm_pipeline_batch_u8_device(ctx.handle, 4, arr(dl), arr(dr), 120, 41, C.byref(p), arr(od),
+                                             arr(ov)))
+    got_b = bsm.run_pipeline_batch(pairs_b, cfg_b, ctx=ctx)  # host batch on the same streams, no sync between
+    one = bsm.run_pipeline(pairs_b[0][0], pairs_b[0][1], cfg_b, ctx=ctx, outputs="refined").refined
+    torch.cuda.ExternalStream(ctx.stream_ptr()).synchronize()
+    for w, d, v in zip(want_a, od, ov):
+        assert np.array_equal(d.cpu().numpy(), w.disparity) and np.array_equal(v.cpu().numpy(), w.valid)
+    assert all(g == w for g, w in zip(got_b, want_b))
+    assert one == want_b[0]
