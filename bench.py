@@ -527,7 +527,7 @@ def main():
         for k, v in ctx.last_timings().items():
             prof.setdefault(k, []).append(v)
     ctx.set_profiling(False)
-    prof_ms = {k: float(np.mean(v)) for k, v in prof.items() if np.mean(v) > 0}
+    prof_ms = {k: float(np.median(v)) for k, v in prof.items() if np.median(v) > 0}  # median: robust to one slow run
     mma_peak = ctx.measure_mma_peak()  # live dense FP4 tensor rate, flop/s
 
     props = torch.cuda.get_device_properties(dev)
