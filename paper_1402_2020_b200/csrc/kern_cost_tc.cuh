@@ -38,8 +38,10 @@
 //   * one thread issues the MMAs (N <= 256 each, two per K-step for
 //     ncols > 256) and commits the slot back to the producers;
 //   * after the last stage, four epilogue warps read their 32 lanes'
-//     accumulator columns (tcgen05.ld) and reduce the keys (cost << 16) | d
-//     to the per-pixel minimum (ties -> smaller d, matcher.hpp:68-75), then
+//     accumulator columns (tcgen05.ld) and reduce them to the per-pixel
+//     minimum of (cost, d) (ties -> smaller d, matcher.hpp:68-75): within a
+//     32-column chunk on floats acc + e/512 (one FADD + FMNMX per column,
+//     exact), one decode per chunk into the key (cost << 16) | d; then they
 //     release the accumulator.
 // CTAs are persistent (one per SM: the whole 512-column TMEM), walking the
 // (tile, direction x d-block) items tile-major like k_cost_wta.
@@ -388,25 +390,37 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 tc_ld32(lane_taddr + uint32_t(c0), v);
                 const int u0 = c0 - r - ulo;  // element i is valid iff (unsigned)(u0 + i) < span
-                // acc is an exact integer in fp32: bits(acc + 1.5 * 2^23) = 0x4B400000 + acc,
-                // and 0x4B400000 << 16 vanishes mod 2^32, so
-                // key = (base + acc) << 16 | d = (bits << 16) + (base << 16) + d, u = c0 + i - r
-                const uint32_t kb = (base << 16) + uint32_t(w.dir ? w.d0 + c0 - r : w.d0 + w.dq - c0 + r);
-                if (w.dir) {
+                // float keys: f = acc + e_i / 512 (e_i = i right, 31 - i left) orders (cost, d)
+                // and is exact; one decode per chunk
+                auto chunk = [&](auto dirc) {
+                    constexpr bool R = decltype(dirc)::value;
+                    const float inf = __int_as_float(0x7F800000);
+                    float m0 = inf, m1 = inf, m2 = inf, m3 = inf;
+                    if (u0 >= 0 && u0 + 32 <= int(span)) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const uint32_t bits = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), 12582912.0f));
-                        const uint32_t key = (bits << 16) + kb + uint32_t(i);
-                        if (uint32_t(u0 + i) < span) best = min(best, key);
-                    }
-                } else {
+                        for (int i = 0; i < 32; i += 4) {
+                            m0 = fminf(m0, __fadd_rn(__uint_as_float(v[i]), float(R ? i : 31 - i) * (1.0f / 512.0f)));
+                            m1 = fminf(m1, __fadd_rn(__uint_as_float(v[i + 1]), float(R ? i + 1 : 30 - i) * (1.0f / 512.0f)));
+                            m2 = fminf(m2, __fadd_rn(__uint_as_float(v[i + 2]), float(R ? i + 2 : 29 - i) * (1.0f / 512.0f)));
+                            m3 = fminf(m3, __fadd_rn(__uint_as_float(v[i + 3]), float(R ? i + 3 : 28 - i) * (1.0f / 512.0f)));
+                        }
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const uint32_t bits = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), 12582912.0f));
-                        const uint32_t key = (bits << 16) + kb - uint32_t(i);
-                        if (uint32_t(u0 + i) < span) best = min(best, key);
+                        for (int i = 0; i < 32; ++i) {
+                            const float f = __fadd_rn(__uint_as_float(v[i]), float(R ? i : 31 - i) * (1.0f / 512.0f));
+                            if (uint32_t(u0 + i) < span) m0 = fminf(m0, f);
+                        }
                     }
-                }
+                    const float mm = fminf(fminf(m0, m1), fminf(m2, m3));
+                    if (mm != inf) {
+                        const float fl = floorf(mm);
+                        const int e = __float2int_rn((mm - fl) * 512.0f);
+                        const int d = R ? w.d0 + c0 - r + e : w.d0 + w.dq - c0 + r - (31 - e);
+                        best = min(best, (uint32_t(int(base) + __float2int_rn(fl)) << 16) | uint32_t(d));
+                    }
+                };
+                if (w.dir) chunk(std::true_type{});
+                else chunk(std::false_type{});
             }
             tc_fence_before();
             __syncwarp();
