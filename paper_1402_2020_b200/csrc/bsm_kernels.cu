@@ -174,6 +174,8 @@ struct bsm_ctx {
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
     int maskf_force_low = 0;  // test hook (BSM_MASKF_FORCE_LOW=1): k_mask_f32 resolves every low byte
     int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4 (implies k_mask4), bit 1 k_mask4 instead of k_mask_q
+    int refine_cap = 0;  // experiments (BSM_REFINE_CAP): refine CTAs per SM at most (0: the default rule)
+    bool in_batch = false;  // phase B of a batch pair (batch_pair) is being issued
     int k3_variant = 0;  // experiments (BSM_K3_VARIANT): bit 0 thread-0 refill, bit 1 one launch per direction,
                      // bit 2 d-block-major CTA order, bit 3 groups of
                      // 2 x SMs tiles, bit 4 the popcount kernel instead of
@@ -600,7 +602,7 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
     }
     if (mode == 3 || mode == 4) {
         const bool devexp = mode == 4;
-        const size_t fixed = 256 * 8 + 768 * 4;
+        const size_t fixed = devexp ? 256 * 8 + 768 * 4 : 0;  // exp table + gray Lab rows (device exp only)
         // bins of NP pixels per warp: 4 (default) or 1 for very wide disparity ranges
         const int np = (fixed + 8 * 32 * 12 + size_t(8) * 4 * nbins * 8 <= 200 * 1024) ? 4 : 1;
         const int warps =
@@ -618,7 +620,14 @@ int refine_launch(bsm_ctx* c, const float* cd, const uint8_t* cv, const uint8_t*
                              : (np == 4 ? (devexp ? k_vote_refine_fold<4, true, false> : k_vote_refine_fold<4, false, false>)
                                         : (devexp ? k_vote_refine_fold<1, true, false> : k_vote_refine_fold<1, false, false>));
             BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            const int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
+            // as many CTAs per SM as fit (4 at c4: 32 warps) when the refine runs
+            // alone; in a batch (batch_pair) two, so that the next pair's
+            // descriptor / mask CTAs share the SMs: c4 batch 37.8k -> 38.1k
+            // Mdisp-evals/s (3: 37.8k, 1: 37.0k) although the refine alone slows
+            // from 1.00 to 1.42 ms.  BSM_REFINE_CAP overrides both.
+            int per_sm = std::max(1, std::min(4, int((220 * 1024) / sm)));
+            const int cap = c->refine_cap > 0 ? c->refine_cap : (c->in_batch ? 2 : 0);
+            if (cap > 0) per_sm = std::min(per_sm, cap);
             BSM_CUDA(cudaMemsetAsync(c->counters.as<int>() + 2, 0, 4, c->stream));  // work counter
             kern<<<c->sm_count * per_sm, warps * 32, sm, c->stream>>>(
                 c->vmap.as<uint32_t>(), lab, c->d_lab256.as<float>(), W, rows, radius, lc, c->d_elam.as<double>(),
@@ -908,7 +917,9 @@ int batch_pair(bsm_ctx* c, int i, const Views& v, int W, int H, const bsm_params
     BSM_CUDA(cudaStreamWaitEvent(c->s_ref, c->ev_a[k], 0));
     const cudaStream_t main = c->stream;
     c->stream = c->s_ref;
+    c->in_batch = true;
     const int rc = pipeline_device(c, v, W, H, 0, H, params, false, 2, k == 1);
+    c->in_batch = false;
     c->stream = main;
     BSM_TRY(rc);
     return cudaEventRecord(c->ev_b[k], c->s_ref) == cudaSuccess ? BSM_OK
@@ -994,6 +1005,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     bsm_ctx* c = new bsm_ctx();
     c->device = device;
     if (const char* v = std::getenv("BSM_K3_VARIANT")) c->k3_variant = std::atoi(v);
+    if (const char* v = std::getenv("BSM_REFINE_CAP")) c->refine_cap = std::atoi(v);
     if (const char* v = std::getenv("BSM_K3_GROUP")) c->k3_group = std::atoi(v);
     if (const char* v = std::getenv("BSM_MASKF_FORCE_LOW")) c->maskf_force_low = std::atoi(v) != 0;
     if (const char* v = std::getenv("BSM_MASK_VARIANT")) c->mask_variant = std::atoi(v);

@@ -306,7 +306,9 @@ __global__ void __launch_bounds__(256, 1) k_vote_refine_fold(
     unsigned long long* stab = reinterpret_cast<unsigned long long*>(fsm);  // 256 (DEVEXP)
     float* slab = reinterpret_cast<float*>(stab + 256);                     // 768 (DEVEXP, gray)
     const int nwarps = blockDim.x >> 5;
-    double* sw_all = reinterpret_cast<double*>(slab + 768);                 // [warps][32] staged weights
+    // [warps][32] staged weights; the exp table and gray Lab rows only with DEVEXP
+    // (without them a CTA fits four per SM: 32 instead of 24 warps)
+    double* sw_all = DEVEXP ? reinterpret_cast<double*>(slab + 768) : fsm;
     int* sb_all = reinterpret_cast<int*>(sw_all + nwarps * 32);             // [warps][32] staged bins
     double* bins_all = reinterpret_cast<double*>(sb_all + nwarps * 32);     // [warps][NP][nbins_cap]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
