@@ -173,6 +173,7 @@ struct bsm_ctx {
     PeerOut peer{};  // peer-memory band outputs during bsm_pipeline_frame_bands_p2p_u8 (n = 0 otherwise)
     int k3_group = 0;    // experiments (BSM_K3_GROUP): tiles per CTA-order group
     int maskf_force_low = 0;  // test hook (BSM_MASKF_FORCE_LOW=1): k_mask_f32 resolves every low byte
+    int mq_px = 16;        // pixels per k_mask_q CTA (8, 16 or 32; BSM_MASKQ_PX)
     int mask_variant = 0;  // experiments (BSM_MASK_VARIANT): bit 0 separate P and Q index tables in k_mask4 (implies k_mask4), bit 1 k_mask4 instead of k_mask_q
     int refine_cap = 0;  // experiments (BSM_REFINE_CAP): refine CTAs per SM at most (0: the default rule)
     bool in_batch = false;  // phase B of a batch pair (batch_pair) is being issued
@@ -260,7 +261,7 @@ int ensure_desc4_table(bsm_ctx* c) {
 
 // Row stride of the k_mask4 / k_mask_f32 window tiles: kM3Px + 2h columns plus
 // up to 3 of alignment slack, a multiple of 4 (word-wide tile loads).
-int mask4_tw(int half) { return round_up(kM3Px + 2 * half + 3, 4); }
+int mask4_tw(int half, int px = kM3Px) { return round_up(px + 2 * half + 3, 4); }
 
 int ensure_mask_offsets(bsm_ctx* c, int TW) {
     if (c->uoff_tw == TW) return BSM_OK;
@@ -372,7 +373,10 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
     const int nviews = img2 ? 2 : 1;
     const int Wp = round_up(W, 128), Wq = field_pitch(W);
     const size_t P = field_plane(W, rows);
-    BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
+    // MCH = 2, 4 (1024 < n <= 4096): k_mask_q (its own tile width)
+    const bool use_q = (c->mch == 2 || c->mch == 4) && !(c->mask_variant & 3);
+    const int mq_px = c->mq_px;
+    BSM_TRY(ensure_mask_offsets(c, use_q ? mask4_tw(c->half, mq_px) : mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
         BSM_TRY(ensure_desc4_table(c));
@@ -406,18 +410,24 @@ int field_device(bsm_ctx* c, const uint8_t* img, int W, int H, int ybeg, int row
         };
         // MCH = 2, 4 (1024 < n <= 4096): four pixels per pass over u8 ranks,
         // two warps per CTA (k_mask_q); BSM_MASK_VARIANT bit 1 keeps k_mask4
-        if ((c->mch == 2 || c->mch == 4) && !(c->mask_variant & 3)) {
-            const size_t smq = size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(kM3Px) * mask4_stage_stride(c->mch) * 4 +
-                               64 + 1024 + size_t(mask4_tw(c->half)) * (2 * c->half + 1);
+        if (use_q) {
+            const size_t smq = size_t(round_up(c->mslots + 1, 4)) * 4 + size_t(mq_px) * mask4_stage_stride(c->mch) * 4 +
+                               64 + 1024 + size_t(mask4_tw(c->half, mq_px)) * (2 * c->half + 1);
+            const dim3 gridq((Wq + mq_px - 1) / mq_px, rows, nviews);
             auto launch_q = [&](auto kern) -> int {
                 BSM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smq)));
-                kern<<<grid3, 64, smq, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * kPqTable / 4,
+                kern<<<gridq, 64, smq, c->stream>>>(img, W, H, ybeg, rows, c->d_pqb.as<uint4>() + 2 * kPqTable / 4,
                                                     c->n, c->d_uoff.as<uint32_t>(), c->nfill, c->mslots,
                                                     round_up(c->mslots + 1, 4), c->d_rank.as<uint8_t>(), c->half,
-                                                    mask4_tw(c->half), c->NW, Wq, P, mask, img2, mask2);
+                                                    mask4_tw(c->half, mq_px), c->NW, Wq, P, mask, img2, mask2);
                 return BSM_OK;
             };
-            BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1>) : launch_q(k_mask_q<2>));
+            if (mq_px == 32)
+                BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1, 32>) : launch_q(k_mask_q<2, 32>));
+            else if (mq_px == 16)
+                BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1, 16>) : launch_q(k_mask_q<2, 16>));
+            else
+                BSM_TRY(c->mch == 2 ? launch_q(k_mask_q<1>) : launch_q(k_mask_q<2>));
             return check_launch(c, "mask");
         }
         // chunks of 32 positions per lane: the work scales with n
@@ -689,7 +699,9 @@ int field_device_f32(bsm_ctx* c, const float* gray, const float4* lab, int W, in
     const int Wq = field_pitch(W);
     const size_t P = field_plane(W, rows);
     BSM_TRY(ensure_descf_table(c));
-    BSM_TRY(ensure_mask_offsets(c, mask4_tw(c->half)));
+    // k_mask_f32 reads only d_uxy, which does not depend on the tile width: keep
+    // the gray kernels' fill table as it is (no re-upload between colour and gray calls)
+    BSM_TRY(ensure_mask_offsets(c, c->uoff_tw > 0 ? c->uoff_tw : mask4_tw(c->half)));
     {
         Scope s(c, T_DESC);
         const int TW = kDfTX + 2 * c->half, TH = kDfTY * kDfPY + 2 * c->half;
@@ -1009,6 +1021,7 @@ int bsm_ctx_create(int device, bsm_ctx** out) {
     if (const char* v = std::getenv("BSM_K3_GROUP")) c->k3_group = std::atoi(v);
     if (const char* v = std::getenv("BSM_MASKF_FORCE_LOW")) c->maskf_force_low = std::atoi(v) != 0;
     if (const char* v = std::getenv("BSM_MASK_VARIANT")) c->mask_variant = std::atoi(v);
+    if (const char* v = std::getenv("BSM_MASKQ_PX")) c->mq_px = std::atoi(v) == 32 ? 32 : std::atoi(v) == 8 ? 8 : 16;
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;

@@ -596,7 +596,7 @@ __device__ __forceinline__ void select_le4x(const uint32_t (&pl)[4][8][MW], int 
         for (int m = 0; m < MW; ++m) o[p][m] = l[p][m] | e[p][m];
 }
 
-template <int MW>
+template <int MW, int PX = kM3Px>
 __global__ void __launch_bounds__(64, 8)
     k_mask_q(const uint8_t* __restrict__ img, int W, int H, int ybeg, int rows, const uint4* __restrict__ pq4, int n,
              const uint32_t* __restrict__ ufill, int nfill, int u, int rho_words, const uint8_t* __restrict__ rank,
@@ -610,14 +610,14 @@ __global__ void __launch_bounds__(64, 8)
     constexpr int STG = mask4_stage_stride(MCH);
     extern __shared__ __align__(16) uint32_t dsm[];
     uint32_t* rho = dsm;                                   // rho_words: u8 ranks of 4 pixels per slot
-    uint32_t* stage = rho + rho_words;                     // [kM3Px][STG]
-    uint32_t* xchg = stage + kM3Px * STG;                  // [2][2 warps][4 pixels]
+    uint32_t* stage = rho + rho_words;                     // [PX][STG]
+    uint32_t* xchg = stage + PX * STG;                     // [2][2 warps][4 pixels]
     uint8_t* rrows = reinterpret_cast<uint8_t*>(xchg + 16);  // 4 x 256
     uint8_t* tile = rrows + 1024;                          // (2h+1) x TW
     const int G = (n + 31) >> 5;
     const int TH = 2 * half + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int x0 = blockIdx.x * kM3Px;
+    const int x0 = blockIdx.x * PX;
     const int ly = blockIdx.y;
     const int y = ybeg + ly;
     const int a0 = (x0 - half) & ~3, ay0 = y - half;
@@ -645,9 +645,9 @@ __global__ void __launch_bounds__(64, 8)
     const int c0 = half * TW + sh + half;  // tile index of pixel x0
     uint4 rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + (tid >> 4)])) + (tid & 15));
 #pragma unroll 1
-    for (int q = 0; q < kM3Px; q += 4) {
+    for (int q = 0; q < PX; q += 4) {
         reinterpret_cast<uint4*>(rrows)[tid] = rr;  // rank rows of pixels q .. q + 3
-        if (q + 4 < kM3Px)
+        if (q + 4 < PX)
             rr = __ldg(reinterpret_cast<const uint4*>(rank + 256 * int(tile[c0 + q + 4 + (tid >> 4)])) + (tid & 15));
         __syncthreads();
         const uint8_t* tq = tile + sh + q;
@@ -720,11 +720,11 @@ __global__ void __launch_bounds__(64, 8)
     // thread = (word offset w % 8, pixel j)
     const int rem = n & 31;
     const uint32_t tail = rem ? (1u << rem) - 1u : ~0u;
-    const int jl = tid & (kM3Px - 1), wl = tid / kM3Px;
+    const int jl = tid & (PX - 1), wl = tid / PX;
     if (x0 + jl >= Wq) return;
     uint32_t* dst = mask + size_t(wl) * P + size_t(ly) * Wq + x0 + jl;
 #pragma unroll 4
-    for (int w = wl; w < NW; w += 64 / kM3Px, dst += size_t(64 / kM3Px) * P) {
+    for (int w = wl; w < NW; w += 64 / PX, dst += size_t(64 / PX) * P) {
         const uint32_t v = stage[jl * STG + w];
         *dst = w < G - 1 ? v : (w == G - 1 ? v & tail : 0u);
     }
