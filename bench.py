@@ -591,6 +591,10 @@ def main():
                                  "unit": "GB/s", "frac": wf / (mask_ms * 1e-3) / wf_peak, "traffic": mask_traffic,
                                  "peak_source": f"1 wavefront (128 B) / clk / SM x {sms} SMs x {clk:.0f} MHz",
                                  "kernel_ms": mask_ms, "wavefronts": wf,
+                                 # HBM side (both views): one image byte in, n/8 mask bytes out per pixel
+                                 "hbm_achieved_gbs": 2 * W * rows_c * (1 + 4096 // 8) / (mask_ms * 1e-3) / 1e9,
+                                 "hbm_peak_gbs": hbm_peak,
+                                 "hbm_frac": 2 * W * rows_c * (1 + 4096 // 8) / (mask_ms * 1e-3) / 1e9 / hbm_peak,
                                  "unit_def": "n/64 = 64 rank-gather wavefronts per pixel (2 gathers per pair, four "
                                              "pixels' u8 ranks per u32), 128 B each",
                                  "note": "the kernel is instruction-issue-bound (~69% issue slots busy, L1 58%, "
